@@ -1,0 +1,239 @@
+/*
+ * smallkv.h — C ABI of libsmallkv.so, the sm_100a (B200) decode hot path of
+ * SmallKV (arXiv 2508.02751, "small model assisted compensation of KV cache
+ * compression").
+ *
+ * Citations: "P:n" = PAPER.md line n (section / equation named beside it),
+ * "S:n" = SPEC.md line n.  The readings of ambiguous passages are listed in
+ * DESIGN.md §3 ("readings") and referred to here as R1..R12.
+ *
+ * The three hot-path calls follow the decode branch of Algorithm 1
+ * (P:196-209):
+ *   smallkv_select  — Alg. 1 l.7 + l.9: score the SLM's current query row over
+ *                     its full, never-compressed cache C^s_all and split
+ *                     every row f(i) the head map references into critical /
+ *                     marginal / evicted sets (Eq. 4, Eq. 6).
+ *   smallkv_attend  — Alg. 1 l.12-14: per LLM layer, O = O_c + O_m with O_c the
+ *                     exact softmax over the critical ∪ recent K/V (P:203,
+ *                     App. D) and O_m = Σ_{k∈marginal} A'_{f(i)}[k]·V[k]
+ *                     (Eq. 6 second branch P:147, App. D).
+ *   smallkv_match_heads — prefill-time Eq. 2 (TopK Jaccard) and
+ *                     Eq. 3 (f(i) = argmax_j S).
+ *
+ * Conventions (all calls):
+ *  - Every pointer marked "device" is caller-owned device memory (e.g. torch
+ *    tensors); the library never allocates, never synchronises the device and
+ *    keeps no state between calls.  All device work is enqueued on `stream`
+ *    (a cudaStream_t passed as void*; NULL = legacy default stream), so the
+ *    calls are CUDA-graph capturable.
+ *  - bf16 arrays are passed as `const uint16_t*` (raw bfloat16 bits).
+ *  - Return value: SMALLKV_OK (0) or an error code; on error nothing has been
+ *    enqueued (host-side validation happens before any launch) except for
+ *    SMALLKV_ERR_CUDA, which reports a launch failure.  smallkv_last_error()
+ *    returns a thread-local message describing the last non-OK return.
+ *  - Data-dependent conditions are NOT errors: budgets larger than a sequence
+ *    are clamped on the device (R5: R' = min(R,n), K' = min(K,n-R'),
+ *    M' = min(M,n-R'-K')); NaN/Inf inputs give unspecified results.
+ *  - Results are deterministic: bit-identical across runs, page-table
+ *    permutations and batch partitions.
+ *  - Only sm_100 devices are accepted (SMALLKV_ERR_DEVICE otherwise).
+ */
+#ifndef SMALLKV_H_
+#define SMALLKV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum smallkv_status {
+  SMALLKV_OK = 0,
+  SMALLKV_ERR_NULL = 1,        /* a required pointer is NULL                    */
+  SMALLKV_ERR_SHAPE = 2,       /* unsupported or inconsistent dimensions        */
+  SMALLKV_ERR_ALIGN = 3,       /* a device pointer is not 16-byte aligned       */
+  SMALLKV_ERR_WORKSPACE = 4,   /* workspace NULL or smaller than *_workspace_size */
+  SMALLKV_ERR_DEVICE = 5,      /* current device is not sm_100                  */
+  SMALLKV_ERR_CUDA = 6,        /* a CUDA API call or kernel launch failed       */
+  SMALLKV_ERR_UNSUPPORTED = 7  /* valid request for a variant not built yet     */
+};
+
+/* Thread-local, NUL-terminated description of the last non-OK return. */
+const char* smallkv_last_error(void);
+/* Library version string, e.g. "smallkv-b200 0.1". */
+const char* smallkv_version(void);
+
+/*
+ * One model's paged KV cache, all layers ("V_i ∈ R^{n×d}").
+ * Layout of k and v (bf16, head-major within a page, "HND"):
+ *     [num_layers][num_pages][num_kv_heads][page_size][head_dim]
+ * so the page_size rows of one kv-head inside one page are contiguous.
+ * Token `pos` of sequence b lives in physical page block_table[b*max_blocks +
+ * pos/page_size] at row pos%page_size.  Physical pages are shared by all
+ * layers (one block table per model).
+ *   k, v        device; v may be NULL for the SLM (its V is never read, R11).
+ *   block_table device int32 [B][max_blocks].
+ *   num_pages   physical pages per layer (for index validation / TMA maps).
+ *   page_size   power of two, 1..256.
+ *   head_dim    64 or 128.  num_q_heads % num_kv_heads == 0.
+ */
+typedef struct smallkv_cache {
+  const uint16_t* k;
+  const uint16_t* v;
+  const int32_t* block_table;
+  int64_t num_pages;
+  int32_t max_blocks;
+  int32_t page_size;
+  int32_t num_layers;
+  int32_t num_q_heads;
+  int32_t num_kv_heads;
+  int32_t head_dim;
+} smallkv_cache;
+
+/*
+ * The decode batch.  seq_lens[b] = n_b counts cached tokens INCLUDING the
+ * current one, whose K/V the caller has already appended to both caches (R12).
+ *   seq_lens    device int32 [B], 1 <= n_b <= max_seq_len.
+ *   max_seq_len host; row stride of slm_logits and a sizing bound.
+ */
+typedef struct smallkv_batch {
+  const int32_t* seq_lens;
+  int32_t batch;
+  int32_t max_seq_len;
+} smallkv_batch;
+
+/*
+ * Per-sequence token budgets (critical : recent : marginal = 2:1:2;
+ * Eq. 6's K and P-K).  Device int32 [B] each; clamped on the device
+ * (R5).  max_crit / max_marg (host) are the row strides of the selection
+ * lists and must bound every k_crit[b] / k_marg[b].
+ */
+typedef struct smallkv_budgets {
+  const int32_t* k_crit;
+  const int32_t* n_recent;
+  const int32_t* k_marg;
+  int32_t max_crit;
+  int32_t max_marg;
+} smallkv_budgets;
+
+/*
+ * Host helper: token counts from a KV budget fraction tau (R6):
+ *   K = floor(tau*n/2), R = floor(tau*n/4), M = floor(tau*n/2)
+ * i.e. 2:1:2 with marginal tokens at half cost (V only), so that
+ * K + R + M/2 <= tau*n.  tau in (0,1]; n >= 0.  Returns SMALLKV_ERR_SHAPE for
+ * tau outside (0,1] or n < 0, SMALLKV_ERR_NULL for NULL outputs.
+ */
+int smallkv_budget_from_tau(double tau, int32_t n, int32_t* k_crit,
+                            int32_t* n_recent, int32_t* k_marg);
+
+/*
+ * Head map convention (Eq. 3; R9): head_map is device int32
+ * [L * H], entry (layer*H + h) = flat SLM head j = slm_layer*H_s + slm_head,
+ * 0 <= j < l*H_s.  Maps may cross layers (R9).
+ */
+
+/* Bytes of workspace smallkv_select needs (0 on invalid arguments). */
+size_t smallkv_select_workspace_size(const smallkv_cache* slm,
+                                     const smallkv_batch* batch,
+                                     int32_t n_llm_heads);
+
+/*
+ * smallkv_select — SLM score rows + three-way split (Alg. 1 l.7, l.9).
+ *
+ * For every flat SLM head j in image(head_map) and every sequence b
+ * ("performs eviction for the i cache of LLM based on the f(i)-th (full)
+ * cache of SLM"; Eq. 6; R1 current-row score, R4 marginal band,
+ * R3 tie-break):
+ *   s'_v  = q'_j · K'_{kv(j)}[v] / sqrt(d_s),   v in [0, n)         (fp32)
+ *   m'    = max_v s'_v,  lse' = m' + ln Σ_v exp(s'_v - m')
+ *   a'_v  = exp(s'_v - lse')        (the SLM attention row A'_{f(i)})
+ *   recent R' = [n-R', n); positions [0, n-R') ranked by (s' desc, v asc):
+ *   critical = first K', marginal = next M', evicted = the rest.
+ * Inputs:
+ *   slm_q       device bf16 [l][B][H_s][d_s] (post-RoPE current-token queries).
+ *   slm         SLM cache (v unused).
+ *   head_map    device int32 [n_llm_heads] (see above).
+ * Outputs (indexed by flat SLM head j; rows not in image(f) untouched):
+ *   slm_logits  device fp32 [l*H_s][B][max_seq_len]   s'_v for v < n.
+ *   slm_lse     device fp32 [l*H_s][B][2]            (m', lse').
+ *   crit_idx    device int32 [l*H_s][B][max_crit]    ascending positions.
+ *   marg_idx    device int32 [l*H_s][B][max_marg]    ascending positions.
+ *   marg_w      device fp32 [l*H_s][B][max_marg]     a'_v at marg_idx.
+ *   counts      device int32 [l*H_s][B][2]           (K', M') after clamping.
+ *   acc         must be NULL (current-row score, R1).  The accumulated-score
+ *               variant (Eq. 1 running sums) is not built yet and
+ *               returns SMALLKV_ERR_UNSUPPORTED.
+ *   ws          device workspace, >= smallkv_select_workspace_size bytes.
+ * Errors: NULL pointers, H_s % H_kv_s != 0, head_dim not in {64,128},
+ * page_size not a power of two in [1,256], misaligned pointers, small ws,
+ * non-sm_100 device.
+ */
+int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm,
+                   const smallkv_batch* batch, const int32_t* head_map,
+                   int32_t n_llm_heads, const smallkv_budgets* budgets,
+                   float* slm_logits, float* slm_lse, int32_t* crit_idx,
+                   int32_t* marg_idx, float* marg_w, int32_t* counts,
+                   float* acc, void* ws, size_t ws_bytes, void* stream);
+
+/* Bytes of workspace smallkv_attend needs (0 on invalid arguments). */
+size_t smallkv_attend_workspace_size(const smallkv_cache* llm,
+                                     const smallkv_batch* batch);
+
+/*
+ * smallkv_attend — compensated decode attention for one LLM layer
+ * (Alg. 1 l.11-14; App. D SmallKV_attention_forward P:788-793).
+ *
+ * For every sequence b and LLM query head h of layer `llm_layer`, with
+ * j = head_map[llm_layer*H + h], kv-head g = h / (H/H_kv), the lists written
+ * by smallkv_select for (j, b) and R' from n_recent (R2, R10):
+ *   l_k = q_h · K_g[k] / sqrt(d)              for k in C ∪ R'
+ *   w_k = exp(l_k - max) / Σ_{C∪R'} exp(.)     (O_c = 0 if C ∪ R' is empty)
+ *   O_c = Σ w_k V_g[k];  O_m = Σ_{k∈M} a'_j[k] V_g[k];  out = O_c + O_m
+ * with a'_j[k] = exp(slm_logits[j][b][k] - lse'[j][b]) (= marg_w, Eq. 6).
+ * Inputs:
+ *   llm_layer   index into head_map's layer dimension (0 <= llm_layer < L).
+ *   cache_layer layer slot of `llm`'s pools holding this layer's K/V
+ *               (lets a caller rotate a resident subset of layers).
+ *   q           device bf16 [B][H][d].
+ *   n_llm_layers L (head_map has L*H entries).
+ *   slm_logits, slm_lse, crit_idx, marg_idx, counts: smallkv_select outputs
+ *               (slm_row_stride = max_seq_len of that call).
+ *   out         device fp32 [B][H][d].
+ *   ws          device workspace, >= smallkv_attend_workspace_size bytes,
+ *               ZERO-FILLED before its first use; every call leaves its
+ *               completion counters zero again.
+ * Errors: as smallkv_select, plus H/H_kv > 8 (SMALLKV_ERR_SHAPE).
+ */
+int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
+                   const smallkv_cache* llm, const smallkv_batch* batch,
+                   const int32_t* head_map, int32_t n_llm_layers,
+                   int32_t slm_heads_total, const smallkv_budgets* budgets,
+                   const float* slm_logits, const float* slm_lse,
+                   const int32_t* crit_idx, const int32_t* marg_idx,
+                   const int32_t* counts, float* out, void* ws,
+                   size_t ws_bytes, void* stream);
+
+/*
+ * smallkv_match_heads — prefill similarity matching (Eq. 2-3).
+ *   llm_F  device fp32 [n_llm][w]  accumulative scores F(A_i, C) (Eq. 1) of
+ *          every LLM head over the matching window (R8).
+ *   slm_F  device fp32 [n_slm][w]  same for every SLM head.
+ *   k_match TopK size, 1 <= k_match <= w <= 512 (SPEC default
+ *          max(16, ceil(0.2 w))).
+ *   head_map out, device int32 [n_llm]: argmax_j Jaccard(TopK(F_i), TopK(F'_j)),
+ *          ties -> smallest j.  TopK ties -> lower index.
+ *   jaccard out, device fp32 [n_llm]: the winning Jaccard value.
+ */
+int smallkv_match_heads(const float* llm_F, int32_t n_llm, const float* slm_F,
+                        int32_t n_slm, int32_t w, int32_t k_match,
+                        int32_t* head_map, float* jaccard, void* stream);
+
+/* Zero-fill `bytes` of device memory at `ws` on `stream` (workspace init). */
+int smallkv_workspace_init(void* ws, size_t bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SMALLKV_H_ */
