@@ -224,10 +224,16 @@ int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
  *   head_map out, device int32 [n_llm]: argmax_j Jaccard(TopK(F_i), TopK(F'_j)),
  *          ties -> smallest j.  TopK ties -> lower index.
  *   jaccard out, device fp32 [n_llm]: the winning Jaccard value.
+ *   ws     device workspace >= smallkv_match_heads_workspace_size(n_llm, n_slm)
+ *          bytes (TopK bitsets; no initialisation needed).
+ * Errors: NULL pointers, w outside [1,512], k_match outside [1,w], n_llm or
+ * n_slm < 1, small workspace, non-sm_100 device.
  */
+size_t smallkv_match_heads_workspace_size(int32_t n_llm, int32_t n_slm);
 int smallkv_match_heads(const float* llm_F, int32_t n_llm, const float* slm_F,
                         int32_t n_slm, int32_t w, int32_t k_match,
-                        int32_t* head_map, float* jaccard, void* stream);
+                        int32_t* head_map, float* jaccard, void* ws,
+                        size_t ws_bytes, void* stream);
 
 /* Zero-fill `bytes` of device memory at `ws` on `stream` (workspace init). */
 int smallkv_workspace_init(void* ws, size_t bytes, void* stream);

@@ -1,0 +1,84 @@
+// kernels.h — internal launch interfaces of libsmallkv (not part of the ABI).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace skv {
+
+// ---------------------------------------------------------------- K1 slm_score
+struct SlmScoreParams {
+  const uint16_t* q;          // [l][B][H_s][d]
+  const int32_t* block_table; // [B][max_blocks]
+  const int32_t* seq_lens;    // [B]
+  const uint8_t* row_needed;  // [l*H_s]
+  float* logits;              // [l*H_s][B][row_stride]
+  int64_t num_pages;
+  int32_t max_blocks, page_size, layers, heads, kv_heads, head_dim, batch;
+  int32_t row_stride;         // max_seq_len
+  int32_t chunk_tokens;       // tokens per CTA (multiple of 64)
+  int32_t box_rows;           // TMA box rows = min(page_size, 64)
+  uint32_t swz;               // 7 = 128B swizzle, 0 = none
+  float scale;                // 1/sqrt(d)
+};
+cudaError_t launch_slm_score(const SlmScoreParams& p, const CUtensorMap& map, int max_seq_len,
+                             cudaStream_t s);
+
+// row flags + compact list of the head map's image
+cudaError_t launch_row_flags(const int32_t* head_map, int32_t n_llm_heads, int32_t n_slm_heads,
+                             uint8_t* row_needed, int32_t* rows, int32_t* n_rows,
+                             cudaStream_t s);
+
+// ---------------------------------------------------------------- K2 select
+struct SelectParams {
+  const float* logits;        // [l*H_s][B][row_stride]
+  const int32_t* seq_lens;
+  const int32_t* rows;        // compact image(f)
+  const int32_t* n_rows;      // device count
+  const int32_t *k_crit, *n_recent, *k_marg;
+  float* lse;                 // [l*H_s][B][2]
+  int32_t* crit_idx;          // [l*H_s][B][max_crit]
+  int32_t* marg_idx;          // [l*H_s][B][max_marg]
+  float* marg_w;
+  int32_t* counts;            // [l*H_s][B][2]
+  int32_t batch, row_stride, max_crit, max_marg;
+};
+cudaError_t launch_select(const SelectParams& p, int32_t max_rows, int32_t max_seq_len,
+                          cudaStream_t s);
+
+// ---------------------------------------------------------------- K3 gather_attend (+K4)
+struct AttendParams {
+  const uint16_t* q;          // [B][H][d]
+  const uint16_t* k;          // pool base
+  const uint16_t* v;
+  const int32_t* block_table;
+  const int32_t* seq_lens;
+  const int32_t* head_map;    // [L*H]
+  const int32_t* n_recent;
+  const float* logits;        // [l*H_s][B][row_stride]
+  const float* lse;           // [l*H_s][B][2]
+  const int32_t* crit_idx;
+  const int32_t* marg_idx;
+  const int32_t* counts;
+  float* out;                 // [B][H][d]
+  float* partials;            // [B*H][max_chunks][2 + 2d]
+  int32_t* counters;          // [B*H_kv]
+  int64_t num_pages;
+  int64_t layer_offset;       // cache_layer * num_pages * H_kv * page_size * d (elements)
+  int32_t max_blocks, page_size, heads, kv_heads, head_dim, batch, layer;
+  int32_t row_stride, max_crit, max_marg;
+  int32_t chunk;              // positions per CTA
+  int32_t max_chunks;
+  float scale_log2;           // log2(e)/sqrt(d)
+};
+cudaError_t launch_attend(const AttendParams& p, cudaStream_t s);
+size_t attend_partials_floats(int32_t batch, int32_t heads, int32_t head_dim, int32_t max_chunks);
+int32_t attend_chunk_size(int32_t max_seq_len);
+
+// ---------------------------------------------------------------- K0 match_heads
+cudaError_t launch_match_heads(const float* llm_F, int32_t n_llm, const float* slm_F,
+                               int32_t n_slm, int32_t w, int32_t k, uint32_t* bits_ws,
+                               int32_t* head_map, float* jaccard, cudaStream_t s);
+
+}  // namespace skv

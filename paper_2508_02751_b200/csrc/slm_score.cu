@@ -1,0 +1,204 @@
+// slm_score.cu — K1: the SLM's decode attention logits over its FULL cache.
+//
+// Alg. 1 l.7 "Forward process of M_s(x+t) to update A'_j", scored over
+// the never-compressed SLM cache C^s_all.  For SLM layer j_l, kv-head
+// g', sequence b this kernel streams K'[0, n) once and produces, for every
+// q-head h of the group that the head map references (rows of image(f)),
+//   s'_v = q'_h · K'[v] / sqrt(d_s)          (fp32 accumulate)
+// The softmax statistics (m', lse') and the split are computed by K2 from these
+// rows (select.cu).
+//
+// B200 design: one CTA = (token chunk, kv-head, layer*B+b); a producer warp
+// streams 64-token K' tiles with 2-D TMA (cp.async.bulk.tensor, 128-byte
+// swizzle) page by page through an mbarrier ring; 4 consumer warps each take 16
+// tokens of a tile and contract them with the whole GQA query group on the
+// tensor cores (mma.sync m16n8k16: heads = M (padded to 16), tokens = N,
+// head_dim = K).  The path is HBM-bound (≈G_s flop/B); the tensor cores only
+// keep the ALU off the critical path.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace skv {
+
+namespace {
+constexpr int kTile = 64;       // tokens per pipeline stage
+constexpr int kConsumers = 4;   // compute warps (16 tokens each)
+constexpr int kThreads = (kConsumers + 1) * 32;
+
+template <int D>
+constexpr int stages_for() { return D == 64 ? 6 : 4; }
+
+template <int D>
+constexpr int smem_bytes() {
+  return stages_for<D>() * kTile * D * 2 + 2 * stages_for<D>() * 8 + 1024;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads)
+slm_score_kernel(const __grid_constant__ CUtensorMap map, const SlmScoreParams p) {
+  constexpr int NSTAGE = stages_for<D>();
+  constexpr int HALVES = D / 64;                 // 128-byte column halves of a row
+  constexpr int STAGE_BYTES = kTile * D * 2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NSTAGE * STAGE_BYTES);
+  uint64_t* empty = full + NSTAGE;
+
+  const int kvh = blockIdx.y;
+  const int layer = blockIdx.z / p.batch, b = blockIdx.z % p.batch;
+  const int G = p.heads / p.kv_heads;
+  const int n = p.seq_lens[b];
+  const int t_begin = blockIdx.x * p.chunk_tokens;
+  if (t_begin >= n) return;
+  const int t_end = min(n, t_begin + p.chunk_tokens);
+  const int ntiles = (t_end - t_begin + kTile - 1) / kTile;
+  const int head0 = layer * p.heads + kvh * G;   // flat SLM head of the group's first q-head
+  uint32_t need = 0;
+  for (int h = 0; h < G; ++h) need |= (p.row_needed[head0 + h] ? 1u : 0u) << h;
+  if (need == 0) return;                         // no LLM head maps into this group
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumers);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == kConsumers) {
+    // ---------------- TMA producer (one elected lane)
+    if (lane == 0) {
+      prefetch_tmap(&map);
+      const int boxes_per_tile = kTile / p.box_rows;
+      for (int it = 0; it < ntiles; ++it) {
+        const int s = it % NSTAGE;
+        if (it >= NSTAGE) mbar_wait(&empty[s], ((it / NSTAGE) & 1) ^ 1);
+        const int t0 = t_begin + it * kTile;
+        int nbox = 0;
+        for (int bx = 0; bx < boxes_per_tile; ++bx) nbox += (t0 + bx * p.box_rows < n) ? 1 : 0;
+        mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(nbox * HALVES * p.box_rows * 128));
+        for (int bx = 0; bx < nbox; ++bx) {
+          const int t = t0 + bx * p.box_rows;
+          const int page = p.block_table[static_cast<int64_t>(b) * p.max_blocks + t / p.page_size];
+          const int64_t row64 =
+              ((static_cast<int64_t>(layer) * p.num_pages + page) * p.kv_heads + kvh) * p.page_size +
+              t % p.page_size;
+          const int row = static_cast<int>(row64);
+#pragma unroll
+          for (int hf = 0; hf < HALVES; ++hf)
+            tma_load_2d(smem_u32(smem + s * STAGE_BYTES + hf * kTile * 128 + bx * p.box_rows * 128),
+                        &map, &full[s], hf * 64, row);
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers: S[16 heads x 16 tokens] per warp per tile
+  const int gq = lane >> 2, tq = lane & 3;
+  const uint16_t* qg = p.q + ((static_cast<int64_t>(layer) * p.batch + b) * p.heads + kvh * G) * D;
+  uint32_t qa[D / 16][4];
+#pragma unroll
+  for (int kk = 0; kk < D / 16; ++kk) {
+    const int c = 16 * kk + 2 * tq;
+    qa[kk][0] = gq < G ? *reinterpret_cast<const uint32_t*>(qg + gq * D + c) : 0u;
+    qa[kk][1] = gq + 8 < G ? *reinterpret_cast<const uint32_t*>(qg + (gq + 8) * D + c) : 0u;
+    qa[kk][2] = gq < G ? *reinterpret_cast<const uint32_t*>(qg + gq * D + c + 8) : 0u;
+    qa[kk][3] = gq + 8 < G ? *reinterpret_cast<const uint32_t*>(qg + (gq + 8) * D + c + 8) : 0u;
+  }
+  const bool w_lo = gq < G && ((need >> gq) & 1u);
+  const bool w_hi = gq + 8 < G && ((need >> (gq + 8)) & 1u);
+  float* row_lo = w_lo ? p.logits + (static_cast<int64_t>(head0 + gq) * p.batch + b) * p.row_stride : nullptr;
+  float* row_hi = w_hi ? p.logits + (static_cast<int64_t>(head0 + gq + 8) * p.batch + b) * p.row_stride : nullptr;
+  const uint32_t swz = p.swz;
+  const int mi = lane >> 3;
+  const int r_ld = warp * 16 + ((mi >> 1) << 3) + (lane & 7);   // token row this lane addresses
+
+  for (int it = 0; it < ntiles; ++it) {
+    const int s = it % NSTAGE;
+    mbar_wait(&full[s], (it / NSTAGE) & 1);
+    const uint8_t* st = smem + s * STAGE_BYTES;
+    float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+    for (int kk = 0; kk < D / 16; ++kk) {
+      const int c = 2 * kk + (mi & 1);           // 16-byte chunk over the row
+      const int hf = c >> 3, cc = c & 7;
+      const uint32_t addr =
+          smem_u32(st + hf * kTile * 128 + r_ld * 128 + ((cc ^ (r_ld & swz)) << 4));
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4(addr, b0, b1, b2, b3);
+      mma_bf16(acc[0], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b0, b1);
+      mma_bf16(acc[1], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b2, b3);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    const int tw = t_begin + it * kTile + warp * 16;
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) {
+      const int pos = tw + ni * 8 + 2 * tq;
+      if (row_lo) {
+        if (pos < t_end) row_lo[pos] = acc[ni][0] * p.scale;
+        if (pos + 1 < t_end) row_lo[pos + 1] = acc[ni][1] * p.scale;
+      }
+      if (row_hi) {
+        if (pos < t_end) row_hi[pos] = acc[ni][2] * p.scale;
+        if (pos + 1 < t_end) row_hi[pos + 1] = acc[ni][3] * p.scale;
+      }
+    }
+  }
+}
+
+// One CTA: flags of the head map's image and its compact, ascending list.
+__global__ void row_flags_kernel(const int32_t* __restrict__ head_map, int32_t n_llm,
+                                 int32_t n_slm, uint8_t* __restrict__ needed,
+                                 int32_t* __restrict__ rows, int32_t* __restrict__ n_rows) {
+  extern __shared__ uint8_t flags[];
+  for (int i = threadIdx.x; i < n_slm; i += blockDim.x) flags[i] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n_llm; i += blockDim.x) {
+    const int j = head_map[i];
+    if (j >= 0 && j < n_slm) flags[j] = 1;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n_slm; i += blockDim.x) needed[i] = flags[i];
+  if (threadIdx.x < 32) {
+    int base = 0;
+    for (int i0 = 0; i0 < n_slm; i0 += 32) {
+      const int i = i0 + threadIdx.x;
+      const bool f = i < n_slm && flags[i];
+      const uint32_t bal = __ballot_sync(0xffffffffu, f);
+      if (f) rows[base + __popc(bal & lanemask_lt())] = i;
+      base += __popc(bal);
+    }
+    if (threadIdx.x == 0) *n_rows = base;
+  }
+}
+}  // namespace
+
+cudaError_t launch_row_flags(const int32_t* head_map, int32_t n_llm_heads, int32_t n_slm_heads,
+                             uint8_t* row_needed, int32_t* rows, int32_t* n_rows,
+                             cudaStream_t s) {
+  row_flags_kernel<<<1, 1024, n_slm_heads, s>>>(head_map, n_llm_heads, n_slm_heads, row_needed,
+                                               rows, n_rows);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_slm_score(const SlmScoreParams& p, const CUtensorMap& map, int max_seq_len,
+                             cudaStream_t s) {
+  dim3 grid((max_seq_len + p.chunk_tokens - 1) / p.chunk_tokens, p.kv_heads, p.layers * p.batch);
+  if (p.head_dim == 64) {
+    constexpr int sm = smem_bytes<64>();
+    cudaFuncSetAttribute(slm_score_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    slm_score_kernel<64><<<grid, kThreads, sm, s>>>(map, p);
+  } else {
+    constexpr int sm = smem_bytes<128>();
+    cudaFuncSetAttribute(slm_score_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    slm_score_kernel<128><<<grid, kThreads, sm, s>>>(map, p);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace skv

@@ -1,0 +1,369 @@
+// smallkv_api.cu — the C ABI of libsmallkv.so (include/smallkv.h): argument
+// validation, workspace layout, TMA descriptor encoding and kernel launches.
+// No device memory is allocated and no stream is synchronised here.
+#include <cudaTypedefs.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <mutex>
+#include <string>
+
+#include "kernels.h"
+#include "smallkv.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(SMALLKV_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
+bool pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
+size_t round256(size_t x) { return (x + 255) & ~size_t(255); }
+
+int check_device() {
+  static std::atomic<int> state[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  if (dev < 0 || dev >= 64) return fail(SMALLKV_ERR_DEVICE, "device index %d out of range", dev);
+  int st = state[dev].load(std::memory_order_relaxed);
+  if (st == 0) {
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    st = (major == 10 && minor == 0) ? 1 : 2;
+    state[dev].store(st, std::memory_order_relaxed);
+  }
+  if (st != 1) return fail(SMALLKV_ERR_DEVICE, "device %d is not sm_100 (B200)", dev);
+  return SMALLKV_OK;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+int check_cache(const smallkv_cache* c, bool need_v, const char* name) {
+  if (!c) return fail(SMALLKV_ERR_NULL, "%s cache is NULL", name);
+  if (!c->k || !c->block_table || (need_v && !c->v))
+    return fail(SMALLKV_ERR_NULL, "%s cache: k/v/block_table NULL", name);
+  if (c->head_dim != 64 && c->head_dim != 128)
+    return fail(SMALLKV_ERR_SHAPE, "%s head_dim %d not in {64,128}", name, c->head_dim);
+  if (!pow2(c->page_size) || c->page_size > 256)
+    return fail(SMALLKV_ERR_SHAPE, "%s page_size %d not a power of two in [1,256]", name,
+                c->page_size);
+  if (c->num_layers < 1 || c->num_q_heads < 1 || c->num_kv_heads < 1 || c->num_pages < 1 ||
+      c->max_blocks < 1)
+    return fail(SMALLKV_ERR_SHAPE, "%s cache: non-positive dimension", name);
+  if (c->num_q_heads % c->num_kv_heads != 0)
+    return fail(SMALLKV_ERR_SHAPE, "%s: %d q heads not a multiple of %d kv heads", name,
+                c->num_q_heads, c->num_kv_heads);
+  if (!aligned(c->k, 16) || (c->v && !aligned(c->v, 16)) || !aligned(c->block_table, 4))
+    return fail(SMALLKV_ERR_ALIGN, "%s cache pools must be 16-byte aligned", name);
+  return SMALLKV_OK;
+}
+
+int check_batch(const smallkv_batch* b, const smallkv_cache* c) {
+  if (!b || !b->seq_lens) return fail(SMALLKV_ERR_NULL, "batch or seq_lens NULL");
+  if (b->batch < 1 || b->batch > 65535 || b->max_seq_len < 1)
+    return fail(SMALLKV_ERR_SHAPE, "batch %d / max_seq_len %d out of range", b->batch,
+                b->max_seq_len);
+  if (static_cast<int64_t>(c->max_blocks) * c->page_size < b->max_seq_len)
+    return fail(SMALLKV_ERR_SHAPE, "block table covers %lld tokens < max_seq_len %d",
+                static_cast<long long>(c->max_blocks) * c->page_size, b->max_seq_len);
+  return SMALLKV_OK;
+}
+
+int check_budgets(const smallkv_budgets* bu) {
+  if (!bu || !bu->k_crit || !bu->n_recent || !bu->k_marg)
+    return fail(SMALLKV_ERR_NULL, "budgets NULL");
+  if (bu->max_crit < 1 || bu->max_marg < 1)
+    return fail(SMALLKV_ERR_SHAPE, "max_crit/max_marg must be >= 1");
+  return SMALLKV_OK;
+}
+
+struct SelectWs {
+  size_t flags, rows, nrows, total;
+};
+SelectWs select_ws_layout(int32_t n_slm) {
+  SelectWs w;
+  w.flags = 0;
+  w.rows = round256(static_cast<size_t>(n_slm));
+  w.nrows = w.rows + round256(static_cast<size_t>(n_slm) * 4);
+  w.total = w.nrows + 256;
+  return w;
+}
+
+struct AttendWs {
+  size_t counters, partials, total;
+  int32_t chunk, max_chunks;
+};
+AttendWs attend_ws_layout(const smallkv_cache* llm, const smallkv_batch* b) {
+  AttendWs w;
+  w.chunk = skv::attend_chunk_size(b->max_seq_len);
+  w.max_chunks = (b->max_seq_len + w.chunk - 1) / w.chunk;
+  w.counters = 0;
+  w.partials = round256(static_cast<size_t>(b->batch) * llm->num_kv_heads * 4);
+  w.total = w.partials + skv::attend_partials_floats(b->batch, llm->num_q_heads,
+                                                     llm->head_dim, w.max_chunks) * 4;
+  return w;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* smallkv_last_error(void) { return g_err.c_str(); }
+const char* smallkv_version(void) { return "smallkv-b200 0.1 (sm_100a)"; }
+
+int smallkv_budget_from_tau(double tau, int32_t n, int32_t* k_crit, int32_t* n_recent,
+                            int32_t* k_marg) {
+  if (!k_crit || !n_recent || !k_marg) return fail(SMALLKV_ERR_NULL, "NULL output");
+  if (!(tau > 0.0 && tau <= 1.0) || n < 0)
+    return fail(SMALLKV_ERR_SHAPE, "tau %g must be in (0,1], n %d >= 0", tau, n);
+  // 2:1:2 critical:recent:marginal; marginal costs half (V only), so the
+  // token fractions are tau/2, tau/4, tau/2.  The epsilon absorbs binary
+  // rounding of tau*n (e.g. 0.35*200 = 69.999..).
+  const double x = tau * static_cast<double>(n);
+  *k_crit = static_cast<int32_t>(std::floor(x / 2.0 + 1e-9));
+  *n_recent = static_cast<int32_t>(std::floor(x / 4.0 + 1e-9));
+  *k_marg = static_cast<int32_t>(std::floor(x / 2.0 + 1e-9));
+  return SMALLKV_OK;
+}
+
+size_t smallkv_select_workspace_size(const smallkv_cache* slm, const smallkv_batch* batch,
+                                     int32_t n_llm_heads) {
+  if (!slm || !batch || n_llm_heads < 1) return 0;
+  return select_ws_layout(slm->num_layers * slm->num_q_heads).total;
+}
+
+int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm, const smallkv_batch* batch,
+                   const int32_t* head_map, int32_t n_llm_heads, const smallkv_budgets* budgets,
+                   float* slm_logits, float* slm_lse, int32_t* crit_idx, int32_t* marg_idx,
+                   float* marg_w, int32_t* counts, float* acc, void* ws, size_t ws_bytes,
+                   void* stream) {
+  int rc;
+  if ((rc = check_cache(slm, false, "slm")) != SMALLKV_OK) return rc;
+  if ((rc = check_batch(batch, slm)) != SMALLKV_OK) return rc;
+  if ((rc = check_budgets(budgets)) != SMALLKV_OK) return rc;
+  if (!slm_q || !head_map || !slm_logits || !slm_lse || !crit_idx || !marg_idx || !marg_w ||
+      !counts)
+    return fail(SMALLKV_ERR_NULL, "smallkv_select: NULL input/output pointer");
+  if (acc)
+    return fail(SMALLKV_ERR_UNSUPPORTED,
+                "accumulated-score selection (acc != NULL) is not built yet; pass NULL");
+  if (n_llm_heads < 1) return fail(SMALLKV_ERR_SHAPE, "n_llm_heads must be >= 1");
+  const int G_s = slm->num_q_heads / slm->num_kv_heads;
+  if (G_s > 16) return fail(SMALLKV_ERR_SHAPE, "SLM GQA group %d > 16", G_s);
+  const int n_slm = slm->num_layers * slm->num_q_heads;
+  if (n_slm > 32768) return fail(SMALLKV_ERR_SHAPE, "l*H_s = %d > 32768", n_slm);
+  if (static_cast<int64_t>(slm->num_layers) * batch->batch > 65535)
+    return fail(SMALLKV_ERR_SHAPE, "l*B = %lld > 65535",
+                static_cast<long long>(slm->num_layers) * batch->batch);
+  const int64_t rows_total =
+      static_cast<int64_t>(slm->num_layers) * slm->num_pages * slm->num_kv_heads * slm->page_size;
+  if (rows_total >= (int64_t(1) << 31))
+    return fail(SMALLKV_ERR_SHAPE, "SLM pool has %lld rows (>= 2^31)",
+                static_cast<long long>(rows_total));
+  if (!aligned(slm_q, 4)) return fail(SMALLKV_ERR_ALIGN, "slm_q must be 4-byte aligned");
+  const SelectWs L = select_ws_layout(n_slm);
+  if (!ws || ws_bytes < L.total)
+    return fail(SMALLKV_ERR_WORKSPACE, "select workspace %zu < %zu bytes", ws_bytes, L.total);
+  if ((rc = check_device()) != SMALLKV_OK) return rc;
+
+  auto fn = encode_fn();
+  if (!fn) return fail(SMALLKV_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap map;
+  const int d = slm->head_dim;
+  const int box_rows = slm->page_size < 64 ? slm->page_size : 64;
+  const bool swz = slm->page_size >= 8;
+  cuuint64_t gdim[2] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(rows_total)};
+  cuuint64_t gstride[1] = {static_cast<cuuint64_t>(d) * 2};
+  cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult cr = fn(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(slm->k), gdim,
+                   gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return fail(SMALLKV_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", cr);
+
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint8_t* wsb = static_cast<uint8_t*>(ws);
+  uint8_t* flags = wsb + L.flags;
+  int32_t* rows = reinterpret_cast<int32_t*>(wsb + L.rows);
+  int32_t* nrows = reinterpret_cast<int32_t*>(wsb + L.nrows);
+  cudaError_t e = skv::launch_row_flags(head_map, n_llm_heads, n_slm, flags, rows, nrows, s);
+  if (e != cudaSuccess) return cuda_fail(e, "row_flags launch");
+
+  skv::SlmScoreParams sp;
+  sp.q = slm_q;
+  sp.block_table = slm->block_table;
+  sp.seq_lens = batch->seq_lens;
+  sp.row_needed = flags;
+  sp.logits = slm_logits;
+  sp.num_pages = slm->num_pages;
+  sp.max_blocks = slm->max_blocks;
+  sp.page_size = slm->page_size;
+  sp.layers = slm->num_layers;
+  sp.heads = slm->num_q_heads;
+  sp.kv_heads = slm->num_kv_heads;
+  sp.head_dim = d;
+  sp.batch = batch->batch;
+  sp.row_stride = batch->max_seq_len;
+  sp.chunk_tokens = 1024;
+  sp.box_rows = box_rows;
+  sp.swz = swz ? 7u : 0u;
+  sp.scale = 1.0f / std::sqrt(static_cast<float>(d));
+  e = skv::launch_slm_score(sp, map, batch->max_seq_len, s);
+  if (e != cudaSuccess) return cuda_fail(e, "slm_score launch");
+
+  skv::SelectParams se;
+  se.logits = slm_logits;
+  se.seq_lens = batch->seq_lens;
+  se.rows = rows;
+  se.n_rows = nrows;
+  se.k_crit = budgets->k_crit;
+  se.n_recent = budgets->n_recent;
+  se.k_marg = budgets->k_marg;
+  se.lse = slm_lse;
+  se.crit_idx = crit_idx;
+  se.marg_idx = marg_idx;
+  se.marg_w = marg_w;
+  se.counts = counts;
+  se.batch = batch->batch;
+  se.row_stride = batch->max_seq_len;
+  se.max_crit = budgets->max_crit;
+  se.max_marg = budgets->max_marg;
+  const int max_rows = n_slm < n_llm_heads ? n_slm : n_llm_heads;
+  e = skv::launch_select(se, max_rows, batch->max_seq_len, s);
+  if (e != cudaSuccess) return cuda_fail(e, "select launch");
+  return SMALLKV_OK;
+}
+
+size_t smallkv_attend_workspace_size(const smallkv_cache* llm, const smallkv_batch* batch) {
+  if (!llm || !batch || batch->batch < 1 || batch->max_seq_len < 1) return 0;
+  return attend_ws_layout(llm, batch).total;
+}
+
+int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
+                   const smallkv_cache* llm, const smallkv_batch* batch, const int32_t* head_map,
+                   int32_t n_llm_layers, int32_t slm_heads_total, const smallkv_budgets* budgets,
+                   const float* slm_logits, const float* slm_lse, const int32_t* crit_idx,
+                   const int32_t* marg_idx, const int32_t* counts, float* out, void* ws,
+                   size_t ws_bytes, void* stream) {
+  int rc;
+  if ((rc = check_cache(llm, true, "llm")) != SMALLKV_OK) return rc;
+  if ((rc = check_batch(batch, llm)) != SMALLKV_OK) return rc;
+  if ((rc = check_budgets(budgets)) != SMALLKV_OK) return rc;
+  if (!q || !head_map || !slm_logits || !slm_lse || !crit_idx || !marg_idx || !counts || !out)
+    return fail(SMALLKV_ERR_NULL, "smallkv_attend: NULL input/output pointer");
+  if (n_llm_layers < 1 || llm_layer < 0 || llm_layer >= n_llm_layers)
+    return fail(SMALLKV_ERR_SHAPE, "llm_layer %d outside [0,%d)", llm_layer, n_llm_layers);
+  if (cache_layer < 0 || cache_layer >= llm->num_layers)
+    return fail(SMALLKV_ERR_SHAPE, "cache_layer %d outside [0,%d)", cache_layer,
+                llm->num_layers);
+  if (slm_heads_total < 1) return fail(SMALLKV_ERR_SHAPE, "slm_heads_total must be >= 1");
+  const int G = llm->num_q_heads / llm->num_kv_heads;
+  if (G > 8) return fail(SMALLKV_ERR_SHAPE, "LLM GQA group %d > 8 not supported", G);
+  if (!aligned(q, 4) || !aligned(out, 4))
+    return fail(SMALLKV_ERR_ALIGN, "q/out must be 4-byte aligned");
+  const AttendWs L = attend_ws_layout(llm, batch);
+  if (!ws || ws_bytes < L.total)
+    return fail(SMALLKV_ERR_WORKSPACE, "attend workspace %zu < %zu bytes", ws_bytes, L.total);
+  if ((rc = check_device()) != SMALLKV_OK) return rc;
+
+  skv::AttendParams ap;
+  ap.q = q;
+  ap.k = llm->k;
+  ap.v = llm->v;
+  ap.block_table = llm->block_table;
+  ap.seq_lens = batch->seq_lens;
+  ap.head_map = head_map;
+  ap.n_recent = budgets->n_recent;
+  ap.logits = slm_logits;
+  ap.lse = slm_lse;
+  ap.crit_idx = crit_idx;
+  ap.marg_idx = marg_idx;
+  ap.counts = counts;
+  ap.out = out;
+  uint8_t* wsb = static_cast<uint8_t*>(ws);
+  ap.counters = reinterpret_cast<int32_t*>(wsb + L.counters);
+  ap.partials = reinterpret_cast<float*>(wsb + L.partials);
+  ap.num_pages = llm->num_pages;
+  ap.layer_offset = static_cast<int64_t>(cache_layer) * llm->num_pages * llm->num_kv_heads *
+                    llm->page_size * llm->head_dim;
+  ap.max_blocks = llm->max_blocks;
+  ap.page_size = llm->page_size;
+  ap.heads = llm->num_q_heads;
+  ap.kv_heads = llm->num_kv_heads;
+  ap.head_dim = llm->head_dim;
+  ap.batch = batch->batch;
+  ap.layer = llm_layer;
+  ap.row_stride = batch->max_seq_len;
+  ap.max_crit = budgets->max_crit;
+  ap.max_marg = budgets->max_marg;
+  ap.chunk = L.chunk;
+  ap.max_chunks = L.max_chunks;
+  ap.scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(llm->head_dim));
+  cudaError_t e = skv::launch_attend(ap, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "attend launch");
+  return SMALLKV_OK;
+}
+
+size_t smallkv_match_heads_workspace_size(int32_t n_llm, int32_t n_slm) {
+  if (n_llm < 1 || n_slm < 1) return 0;
+  return static_cast<size_t>(n_llm + n_slm) * 16 * 4;
+}
+
+int smallkv_match_heads(const float* llm_F, int32_t n_llm, const float* slm_F, int32_t n_slm,
+                        int32_t w, int32_t k_match, int32_t* head_map, float* jaccard, void* ws,
+                        size_t ws_bytes, void* stream) {
+  if (!llm_F || !slm_F || !head_map || !jaccard)
+    return fail(SMALLKV_ERR_NULL, "smallkv_match_heads: NULL pointer");
+  if (n_llm < 1 || n_slm < 1) return fail(SMALLKV_ERR_SHAPE, "n_llm/n_slm must be >= 1");
+  if (w < 1 || w > 512) return fail(SMALLKV_ERR_SHAPE, "window %d outside [1,512]", w);
+  if (k_match < 1 || k_match > w) return fail(SMALLKV_ERR_SHAPE, "k_match %d outside [1,%d]", k_match, w);
+  const size_t need = smallkv_match_heads_workspace_size(n_llm, n_slm);
+  if (!ws || ws_bytes < need)
+    return fail(SMALLKV_ERR_WORKSPACE, "match workspace %zu < %zu bytes", ws_bytes, need);
+  int rc;
+  if ((rc = check_device()) != SMALLKV_OK) return rc;
+  cudaError_t e = skv::launch_match_heads(llm_F, n_llm, slm_F, n_slm, w, k_match,
+                                          static_cast<uint32_t*>(ws), head_map, jaccard,
+                                          static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "match_heads launch");
+  return SMALLKV_OK;
+}
+
+int smallkv_workspace_init(void* ws, size_t bytes, void* stream) {
+  if (!ws) return fail(SMALLKV_ERR_NULL, "workspace NULL");
+  cudaError_t e = cudaMemsetAsync(ws, 0, bytes, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
+  return SMALLKV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,250 @@
+"""ctypes binding of libsmallkv.so — argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels behind the C ABI
+(include/smallkv.h).  This module only turns torch tensors into pointers,
+allocates output buffers / workspaces with torch (device memory plumbing) and
+raises on non-OK status.  There is no CPU fallback: if the library is missing
+or the device is not a B200, calls fail loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import os
+import threading
+from typing import Optional, Sequence
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsmallkv.so")
+_lock = threading.Lock()
+_lib = None
+
+STATUS = {0: "OK", 1: "ERR_NULL", 2: "ERR_SHAPE", 3: "ERR_ALIGN", 4: "ERR_WORKSPACE",
+          5: "ERR_DEVICE", 6: "ERR_CUDA", 7: "ERR_UNSUPPORTED"}
+
+# exported symbols, in the order include/smallkv.h declares them
+EXPORTS = ("smallkv_last_error", "smallkv_version", "smallkv_budget_from_tau",
+           "smallkv_select_workspace_size", "smallkv_select", "smallkv_attend_workspace_size",
+           "smallkv_attend", "smallkv_match_heads_workspace_size", "smallkv_match_heads",
+           "smallkv_workspace_init")
+
+
+class SmallKVError(RuntimeError):
+    def __init__(self, fn: str, code: int, msg: str):
+        super().__init__(f"{fn} failed: {STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class CCache(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_void_p), ("v", ctypes.c_void_p),
+                ("block_table", ctypes.c_void_p), ("num_pages", ctypes.c_int64),
+                ("max_blocks", ctypes.c_int32), ("page_size", ctypes.c_int32),
+                ("num_layers", ctypes.c_int32), ("num_q_heads", ctypes.c_int32),
+                ("num_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32)]
+
+
+class CBatch(ctypes.Structure):
+    _fields_ = [("seq_lens", ctypes.c_void_p), ("batch", ctypes.c_int32),
+                ("max_seq_len", ctypes.c_int32)]
+
+
+class CBudgets(ctypes.Structure):
+    _fields_ = [("k_crit", ctypes.c_void_p), ("n_recent", ctypes.c_void_p),
+                ("k_marg", ctypes.c_void_p), ("max_crit", ctypes.c_int32),
+                ("max_marg", ctypes.c_int32)]
+
+
+def load(path: Optional[str] = None):
+    """Load libsmallkv.so (raises if it has not been built)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        p = path or LIB_PATH
+        if not os.path.exists(p):
+            raise RuntimeError(f"{p} not found: build it with `python -m paper_2508_02751_b200.build` "
+                               "(there is no CPU fallback)")
+        lib = ctypes.CDLL(p)
+        P, i32, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_size_t
+        lib.smallkv_last_error.restype = ctypes.c_char_p
+        lib.smallkv_version.restype = ctypes.c_char_p
+        lib.smallkv_budget_from_tau.argtypes = [ctypes.c_double, i32, P, P, P]
+        lib.smallkv_select_workspace_size.argtypes = [P, P, i32]
+        lib.smallkv_select_workspace_size.restype = sz
+        lib.smallkv_select.argtypes = [P, P, P, P, i32, P, P, P, P, P, P, P, P, P, sz, P]
+        lib.smallkv_attend_workspace_size.argtypes = [P, P]
+        lib.smallkv_attend_workspace_size.restype = sz
+        lib.smallkv_attend.argtypes = [i32, i32, P, P, P, P, i32, i32, P, P, P, P, P, P, P, P, sz, P]
+        lib.smallkv_match_heads_workspace_size.argtypes = [i32, i32]
+        lib.smallkv_match_heads_workspace_size.restype = sz
+        lib.smallkv_match_heads.argtypes = [P, i32, P, i32, i32, i32, P, P, P, sz, P]
+        lib.smallkv_workspace_init.argtypes = [P, sz, P]
+        _lib = lib
+        return lib
+
+
+def _check(fn: str, rc: int):
+    if rc != 0:
+        raise SmallKVError(fn, rc, load().smallkv_last_error().decode())
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+def version() -> str:
+    return load().smallkv_version().decode()
+
+
+def budget_from_tau(tau: float, n: int):
+    """Host helper: (K, R, M) token counts for budget fraction tau."""
+    lib = load()
+    k, r, m = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    _check("smallkv_budget_from_tau",
+           lib.smallkv_budget_from_tau(float(tau), int(n), ctypes.byref(k), ctypes.byref(r),
+                                       ctypes.byref(m)))
+    return k.value, r.value, m.value
+
+
+def make_cache(k: torch.Tensor, v: Optional[torch.Tensor], block_table: torch.Tensor,
+               num_q_heads: int) -> CCache:
+    """Describe a paged pool [layers][pages][kv][page_size][d] (bf16) to the ABI."""
+    assert k.dtype == torch.bfloat16 and k.dim() == 5 and k.is_contiguous()
+    if v is not None:
+        assert v.shape == k.shape and v.dtype == torch.bfloat16 and v.is_contiguous()
+    assert block_table.dtype == torch.int32 and block_table.is_contiguous()
+    L, pages, kv, ps, d = k.shape
+    return CCache(k.data_ptr(), _ptr(v), block_table.data_ptr(), pages,
+                  block_table.shape[-1], ps, L, num_q_heads, kv, d)
+
+
+def make_batch(seq_lens: torch.Tensor, max_seq_len: int) -> CBatch:
+    assert seq_lens.dtype == torch.int32 and seq_lens.is_contiguous()
+    return CBatch(seq_lens.data_ptr(), seq_lens.shape[0], int(max_seq_len))
+
+
+def make_budgets(k_crit, n_recent, k_marg, max_crit: int, max_marg: int) -> CBudgets:
+    for t in (k_crit, n_recent, k_marg):
+        assert t.dtype == torch.int32 and t.is_contiguous()
+    return CBudgets(k_crit.data_ptr(), n_recent.data_ptr(), k_marg.data_ptr(), int(max_crit),
+                    int(max_marg))
+
+
+@dataclasses.dataclass
+class SelectOut:
+    logits: torch.Tensor   # fp32 [l*H_s][B][max_seq_len]
+    lse: torch.Tensor      # fp32 [l*H_s][B][2]
+    crit: torch.Tensor     # int32 [l*H_s][B][max_crit]
+    marg: torch.Tensor     # int32 [l*H_s][B][max_marg]
+    marg_w: torch.Tensor   # fp32 [l*H_s][B][max_marg]
+    counts: torch.Tensor   # int32 [l*H_s][B][2]
+
+
+class DecodeStep:
+    """Buffers + calls for one model pair's decode hot path on one device.
+
+    Holds the ABI descriptors, the selection outputs and both workspaces;
+    `select()` runs smallkv_select, `attend(layer, cache_layer, q, out)` runs
+    smallkv_attend.  All tensors must live on the current CUDA device.
+    """
+
+    def __init__(self, *, slm_k, slm_block_table, slm_q_heads: int, llm_k, llm_v,
+                 llm_block_table, llm_q_heads: int, llm_layers: int, seq_lens: torch.Tensor,
+                 max_seq_len: int, head_map: torch.Tensor, k_crit, n_recent, k_marg,
+                 max_crit: int, max_marg: int):
+        self.lib = load()
+        dev = seq_lens.device
+        self._keep = (slm_k, slm_block_table, llm_k, llm_v, llm_block_table, seq_lens, head_map,
+                      k_crit, n_recent, k_marg)
+        self.slm = make_cache(slm_k, None, slm_block_table, slm_q_heads)
+        self.llm = make_cache(llm_k, llm_v, llm_block_table, llm_q_heads)
+        self.batch = make_batch(seq_lens, max_seq_len)
+        self.budgets = make_budgets(k_crit, n_recent, k_marg, max_crit, max_marg)
+        assert head_map.dtype == torch.int32 and head_map.numel() == llm_layers * llm_q_heads
+        self.head_map = head_map
+        self.llm_layers = llm_layers
+        self.n_slm = self.slm.num_layers * slm_q_heads
+        B, n = self.batch.batch, int(max_seq_len)
+        f32, i32 = torch.float32, torch.int32
+        self.out = SelectOut(
+            logits=torch.zeros(self.n_slm, B, n, dtype=f32, device=dev),
+            lse=torch.zeros(self.n_slm, B, 2, dtype=f32, device=dev),
+            crit=torch.zeros(self.n_slm, B, max_crit, dtype=i32, device=dev),
+            marg=torch.zeros(self.n_slm, B, max_marg, dtype=i32, device=dev),
+            marg_w=torch.zeros(self.n_slm, B, max_marg, dtype=f32, device=dev),
+            counts=torch.zeros(self.n_slm, B, 2, dtype=i32, device=dev))
+        ws_s = self.lib.smallkv_select_workspace_size(ctypes.byref(self.slm),
+                                                      ctypes.byref(self.batch),
+                                                      head_map.numel())
+        ws_a = self.lib.smallkv_attend_workspace_size(ctypes.byref(self.llm),
+                                                      ctypes.byref(self.batch))
+        if ws_s == 0 or ws_a == 0:
+            raise SmallKVError("workspace_size", 2, "invalid dimensions")
+        self.ws_select = torch.zeros(ws_s, dtype=torch.uint8, device=dev)
+        self.ws_attend = torch.zeros(ws_a, dtype=torch.uint8, device=dev)
+
+    def select(self, slm_q: torch.Tensor, stream=None):
+        assert slm_q.dtype == torch.bfloat16 and slm_q.is_contiguous()
+        o = self.out
+        rc = self.lib.smallkv_select(
+            slm_q.data_ptr(), ctypes.byref(self.slm), ctypes.byref(self.batch),
+            self.head_map.data_ptr(), self.head_map.numel(), ctypes.byref(self.budgets),
+            o.logits.data_ptr(), o.lse.data_ptr(), o.crit.data_ptr(), o.marg.data_ptr(),
+            o.marg_w.data_ptr(), o.counts.data_ptr(), None, self.ws_select.data_ptr(),
+            self.ws_select.numel(), _stream(stream))
+        _check("smallkv_select", rc)
+        return o
+
+    def attend(self, llm_layer: int, cache_layer: int, q: torch.Tensor, out: torch.Tensor,
+               stream=None):
+        assert q.dtype == torch.bfloat16 and q.is_contiguous()
+        assert out.dtype == torch.float32 and out.is_contiguous()
+        o = self.out
+        rc = self.lib.smallkv_attend(
+            int(llm_layer), int(cache_layer), q.data_ptr(), ctypes.byref(self.llm),
+            ctypes.byref(self.batch), self.head_map.data_ptr(), self.llm_layers, self.n_slm,
+            ctypes.byref(self.budgets), o.logits.data_ptr(), o.lse.data_ptr(),
+            o.crit.data_ptr(), o.marg.data_ptr(), o.counts.data_ptr(), out.data_ptr(),
+            self.ws_attend.data_ptr(), self.ws_attend.numel(), _stream(stream))
+        _check("smallkv_attend", rc)
+        return out
+
+
+def from_problem(p) -> DecodeStep:
+    """DecodeStep for a smallkv_synth.Problem already on the GPU."""
+    return DecodeStep(slm_k=p.slm.k, slm_block_table=p.slm.block_table,
+                      slm_q_heads=p.cfg.slm.q_heads, llm_k=p.llm.k, llm_v=p.llm.v,
+                      llm_block_table=p.llm.block_table, llm_q_heads=p.cfg.llm.q_heads,
+                      llm_layers=p.cfg.llm.layers, seq_lens=p.seq_lens,
+                      max_seq_len=p.max_seq_len, head_map=p.head_map, k_crit=p.k_crit,
+                      n_recent=p.n_recent, k_marg=p.k_marg, max_crit=p.max_crit,
+                      max_marg=p.max_marg)
+
+
+def match_heads(llm_F: torch.Tensor, slm_F: torch.Tensor, k_match: int, stream=None):
+    """Eq. 2-3 on the GPU: (head_map int32 [n_llm], jaccard fp32 [n_llm])."""
+    lib = load()
+    assert llm_F.dtype == torch.float32 and slm_F.dtype == torch.float32
+    llm_F, slm_F = llm_F.contiguous(), slm_F.contiguous()
+    n_llm, w = llm_F.shape
+    n_slm = slm_F.shape[0]
+    dev = llm_F.device
+    hm = torch.empty(n_llm, dtype=torch.int32, device=dev)
+    jac = torch.empty(n_llm, dtype=torch.float32, device=dev)
+    wsb = lib.smallkv_match_heads_workspace_size(n_llm, n_slm)
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    _check("smallkv_match_heads",
+           lib.smallkv_match_heads(llm_F.data_ptr(), n_llm, slm_F.data_ptr(), n_slm, w,
+                                   int(k_match), hm.data_ptr(), jac.data_ptr(), ws.data_ptr(),
+                                   ws.numel(), _stream(stream)))
+    return hm, jac

@@ -1,0 +1,233 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle.
+
+Bars: selection bit-exact except the 1e-6 boundary band,
+counts exact; outputs row-normwise relative error <= 2e-3 with the oracle
+evaluated on the GPU's verified sets.  Inputs are seeded synthetic, at sizes
+the oracle finishes in seconds yet spanning several tiles/chunks and ragged
+tails, plus sampled checks at BASELINE.json's full config-2 size.
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+import pytest
+import torch
+
+import smallkv_synth as synth
+from tests import parity
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device (run with -m 'not gpu' on CPU)")
+    from paper_2508_02751_b200 import build
+    build.build()
+    torch.cuda.set_device(0)
+
+
+def _check(p, layers=None, logit_atol=2e-4):
+    step, out_sel, outs = parity.run_gpu_step(p, layers=layers)
+    sel = parity.oracle_select(p)
+    rep = parity.compare_select(p, out_sel, sel, logit_atol=logit_atol)
+    sg = parity.sel_from_gpu(p, out_sel, sel)
+    errs = []
+    for i, slot in enumerate(range(p.llm.num_layers) if layers is None else layers):
+        e, _ = parity.compare_attend(p, slot, outs[i], sg)
+        errs.append(e)
+        assert e <= parity.OUT_TOL, f"layer slot {slot}: row-normwise err {e}"
+    rep["max_out_err"] = max(errs) if errs else 0.0
+    return rep, out_sel, outs
+
+
+def _cfg(llm=(2, 8, 2, 128), slm=(2, 8, 2, 64), n=1500, B=3, budget=(150, 60, 200)):
+    return synth.small_config(llm=llm, slm=slm, seq_len=n, batch=B, budget=budget)
+
+
+# ---------------------------------------------------------------- configs
+
+def test_toy_config_parity():
+    """BASELINE.json configs[0] at full size: 20% critical + 30% marginal."""
+    p = synth.make_problem(synth.CONFIGS["toy"], seed=11).to("cuda")
+    rep, _, _ = _check(p)
+    print("toy", rep)
+
+
+@pytest.mark.parametrize("page_size", [1, 16, 64])
+@pytest.mark.parametrize("map_kind", ["coherent", "random"])
+def test_small_parity_pages_maps(page_size, map_kind):
+    """Several 1024-position chunks, ragged lengths, every page size."""
+    cfg = _cfg(n=2600, B=3)
+    p = synth.make_problem(cfg, seed=5, page_size=page_size, seq_lens=[2600, 1337, 65],
+                           map_kind=map_kind).to("cuda")
+    rep, _, _ = _check(p)
+    print(page_size, map_kind, rep)
+
+
+@pytest.mark.parametrize("dims", [
+    ((1, 28, 4, 128), (2, 14, 2, 64)),   # qwen7b-shaped G=7, G_s=7
+    ((1, 32, 8, 128), (1, 32, 8, 64)),   # llama-shaped G=4, G_s=4
+    ((1, 40, 8, 128), (1, 12, 2, 128)),  # qwen14b-shaped G=5, d_s=128
+    ((1, 64, 8, 128), (1, 14, 2, 64)),   # qwen72b-shaped G=8
+    ((1, 4, 2, 64), (1, 2, 1, 64)),      # toy-shaped d=64
+])
+def test_shapes_parity(dims):
+    llm, slm = dims
+    cfg = _cfg(llm=llm, slm=slm, n=1100, B=2, budget=(110, 55, 110))
+    p = synth.make_problem(cfg, seed=7, page_size=16, seq_lens=[1100, 700],
+                           map_kind="random").to("cuda")
+    rep, _, _ = _check(p)
+    print(dims, rep)
+
+
+# ---------------------------------------------------------------- special cases
+
+def test_full_budget_is_dense_attention():
+    """K'+R' = n, M = 0 => dense attention (pin P1 on the GPU)."""
+    cfg = _cfg(n=1200, B=2, budget=(100000, 33, 0))
+    p = synth.make_problem(cfg, seed=3, page_size=16, seq_lens=[1200, 513]).to("cuda")
+    _check(p)
+
+
+def test_marginal_only_and_empty():
+    for budget in [(0, 0, 100000), (0, 0, 0), (0, 40, 0), (0, 0, 5)]:
+        cfg = _cfg(n=900, B=2, budget=budget)
+        p = synth.make_problem(cfg, seed=4, page_size=16, seq_lens=[900, 301]).to("cuda")
+        rep, _, outs = _check(p)
+        if budget == (0, 0, 0):
+            assert all(torch.count_nonzero(o).item() == 0 for o in outs)
+
+
+def test_clamp_short_sequences():
+    """n below K+R+M and n = 1 (device clamp R5)."""
+    cfg = _cfg(n=300, B=4, budget=(150, 60, 200))
+    p = synth.make_problem(cfg, seed=8, page_size=16, seq_lens=[300, 1, 2, 61]).to("cuda")
+    _check(p)
+
+
+def test_zero_query_all_ties():
+    """q' = 0: every logit ties; lower index wins (R3) — exact lists."""
+    cfg = _cfg(n=1500, B=2)
+    p = synth.make_problem(cfg, seed=9, page_size=16, seq_lens=[1500, 999])
+    p = dataclasses.replace(p, slm_q=torch.zeros_like(p.slm_q)).to("cuda")
+    rep, sel, _ = _check(p)
+    crit, marg, cnt = sel.crit.cpu(), sel.marg.cpu(), sel.counts.cpu()
+    for j in np.unique(p.head_map.cpu().numpy()):
+        for b in range(p.batch):
+            K, M = int(cnt[j, b, 0]), int(cnt[j, b, 1])
+            assert crit[j, b, :K].tolist() == list(range(K))
+            assert marg[j, b, :M].tolist() == list(range(K, K + M))
+
+
+def test_duplicate_keys_exact_ties():
+    """Duplicated K' rows give exactly equal logits; index tie-break decides."""
+    cfg = _cfg(n=1024, B=1, budget=(100, 20, 100))
+    p = synth.make_problem(cfg, seed=10, page_size=64, seq_lens=[1024])
+    k = p.slm.k.clone()
+    k[:, :, :, 1::2] = k[:, :, :, 0::2]      # rows 2i+1 := rows 2i in every page
+    p = dataclasses.replace(p, slm=dataclasses.replace(p.slm, k=k)).to("cuda")
+    _check(p)
+
+
+def test_extreme_logits():
+    """Logits near ±80 (fp32 exp underflow): ranking on logits stays exact."""
+    cfg = _cfg(n=800, B=1, budget=(80, 20, 100))
+    p = synth.make_problem(cfg, seed=12, page_size=16, seq_lens=[800])
+    p = dataclasses.replace(p, slm_q=(p.slm_q.float() * 12).to(torch.bfloat16)).to("cuda")
+    _check(p, logit_atol=5e-3)
+
+
+# ---------------------------------------------------------------- invariants
+
+def test_deterministic_and_page_permutation_invariant():
+    cfg = _cfg(n=2100, B=2)
+    p = synth.make_problem(cfg, seed=13, page_size=16, seq_lens=[2100, 1500],
+                           map_kind="random").to("cuda")
+    _, s1, o1 = parity.run_gpu_step(p)
+    l1 = [s1.crit.clone(), s1.marg.clone(), s1.marg_w.clone(), s1.lse.clone()]
+    _, s2, o2 = parity.run_gpu_step(p)
+    for a, b in zip(l1, [s2.crit, s2.marg, s2.marg_w, s2.lse]):
+        assert torch.equal(a, b)
+    for a, b in zip(o1, o2):
+        assert torch.equal(a, b)
+    # permute the LLM physical pages: same logical cache, different addresses
+    pages = p.llm.k.shape[1]
+    perm = torch.randperm(pages, generator=torch.Generator().manual_seed(3)).cuda()
+    inv = torch.argsort(perm)
+    k2 = p.llm.k[:, inv]
+    v2 = p.llm.v[:, inv]
+    bt2 = perm[p.llm.block_table.long()].to(torch.int32)
+    p2 = dataclasses.replace(p, llm=dataclasses.replace(p.llm, k=k2.contiguous(),
+                                                         v=v2.contiguous(), block_table=bt2))
+    _, _, o3 = parity.run_gpu_step(p2)
+    for a, b in zip(o1, o3):
+        assert torch.equal(a, b)
+
+
+def test_batch_partition_invariant():
+    """A sequence's result does not depend on its batch neighbours (P12)."""
+    cfg = _cfg(n=1500, B=4)
+    p = synth.make_problem(cfg, seed=14, page_size=16, seq_lens=[1500, 900, 1200, 30]).to("cuda")
+    _, _, o_all = parity.run_gpu_step(p)
+    for idx in ([0, 1], [2, 3]):
+        sub = dataclasses.replace(
+            p, seq_lens=p.seq_lens[idx].contiguous(), slm_q=p.slm_q[:, idx].contiguous(),
+            llm_q=p.llm_q[:, idx].contiguous(),
+            slm=dataclasses.replace(p.slm, block_table=p.slm.block_table[idx].contiguous()),
+            llm=dataclasses.replace(p.llm, block_table=p.llm.block_table[idx].contiguous()),
+            k_crit=p.k_crit[idx].contiguous(), n_recent=p.n_recent[idx].contiguous(),
+            k_marg=p.k_marg[idx].contiguous(), max_seq_len=p.max_seq_len)
+        _, _, o_sub = parity.run_gpu_step(sub)
+        for a, b in zip(o_all, o_sub):
+            assert torch.equal(a[idx], b)
+
+
+# ---------------------------------------------------------------- matching
+
+def test_match_heads_vs_oracle():
+    import oracle
+    from paper_2508_02751_b200 import smallkv
+    rng = np.random.default_rng(0)
+    for w, k, n_llm, n_slm in [(150, 30, 784, 336), (200, 40, 96, 50), (100, 16, 20, 7)]:
+        llm_F = rng.integers(0, 50, (n_llm, w)).astype(np.float32) / 7.0  # ties
+        slm_F = rng.random((n_slm, w)).astype(np.float32)
+        slm_F[: min(5, n_slm)] = llm_F[: min(5, n_slm)] * 3.0
+        hm, jac = smallkv.match_heads(torch.from_numpy(llm_F).cuda(),
+                                      torch.from_numpy(slm_F).cuda(), k)
+        ohm, ojac = oracle.match_heads(llm_F.astype(np.float64), slm_F.astype(np.float64), k)
+        assert np.array_equal(hm.cpu().numpy(), ohm)
+        np.testing.assert_allclose(jac.cpu().numpy(), ojac, rtol=1e-6)
+
+
+# ---------------------------------------------------------------- full size (config 2)
+
+@pytest.mark.slow
+def test_qwen7b_full_size_sampled():
+    """BASELINE.json configs[1] at full size (n=4096, B=32, all SLM layers),
+    two resident LLM layers; selection checked on sampled rows/sequences,
+    outputs on every head of the sampled sequences."""
+    cfg = synth.CONFIGS["qwen7b"]
+    p = synth.make_problem(cfg, seed=1, device="cuda", llm_layers=[0, 27])
+    step, sel_gpu, outs = parity.run_gpu_step(p)
+    pc = p.to("cpu")
+    rows = np.unique(pc.head_map.numpy())
+    rng = np.random.default_rng(0)
+    sample_rows = np.sort(rng.choice(rows, 16, replace=False)).astype(np.int32)
+    slm_view, llm_view = parity.views(pc)
+    sel = parity.oracle_select(pc, rows=sample_rows, slm_view=slm_view)
+    sb = sorted(rng.choice(pc.batch, 6, replace=False).tolist())
+    rep = parity.compare_select(pc, sel_gpu, sel, batch_idx=sb)
+    # outputs for sampled sequences: oracle on all rows the layer uses
+    used = np.unique(np.concatenate([pc.head_map.numpy()[l * cfg.llm.q_heads:(l + 1) * cfg.llm.q_heads]
+                                     for l in (0, 27)])).astype(np.int32)
+    sel_used = parity.oracle_select(pc, rows=used, slm_view=slm_view)
+    parity.compare_select(pc, sel_gpu, sel_used, batch_idx=sb)
+    sg = parity.sel_from_gpu(pc, sel_gpu, sel_used)
+    for slot in range(2):
+        e, _ = parity.compare_attend(pc, slot, outs[slot].cpu(), sg, llm_view=llm_view,
+                                     heads=sb)
+        assert e <= parity.OUT_TOL
+    print("qwen7b sampled", rep)
