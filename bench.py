@@ -1,0 +1,417 @@
+#!/usr/bin/env python
+"""Benchmark of the SmallKV decode hot path on B200 (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config qwen7b]
+
+A step = one pass of the whole hot path over one batch: smallkv_select over
+all SLM layers (K1 score + K2 split) and one smallkv_attend per LLM layer
+(K3 gather-attend with the fused combine), captured in one CUDA graph.
+Metric (BASELINE.json): decode-attention layer-steps/s (= L LLM layers per
+step) and achieved HBM GB/s over the algorithmic bytes of DESIGN.md §7.
+Default workload: BASELINE.json configs[1] (Qwen2.5-7B + Qwen2.5-0.5B, ctx 4096,
+batch 32 per GPU).  N > 1 (torchrun, one rank per GPU): batch sharding, every
+rank runs its own batch (weak scaling), no data-path collective; the step time
+is the max over ranks (device clock, CUDA events).
+
+`--impl reference` times the fp64 CPU oracle (oracle/) as the reference arm on
+a bounded sample of the same workload; only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "decode attn layer-steps/s and achieved HBM GB/s vs ~8 TB/s, at 1/2/4/8 B200"
+FALLBACK_HBM_GBS = 6650.0   # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured"
+    return FALLBACK_HBM_GBS, "fallback"
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms while running."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(gpu_index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+                    "samples": 0}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def build_problem(cfg_name: str, rank: int, device):
+    import torch
+    import smallkv_synth as synth
+    cfg = synth.CONFIGS[cfg_name]
+    # resident LLM layers: all when they fit, else a rotating subset (each slice >> L2)
+    per_layer = cfg.batch * cfg.llm.kv_heads * cfg.seq_len * cfg.llm.head_dim * 2 * 2
+    free = torch.cuda.mem_get_info(device)[0]
+    slm_bytes = cfg.slm.layers * cfg.batch * cfg.slm.kv_heads * cfg.seq_len * cfg.slm.head_dim * 2
+    budget = int(0.8 * free) - slm_bytes - (4 << 30)
+    resident = max(1, min(cfg.llm.layers, budget // per_layer))
+    p = synth.make_problem(cfg, seed=rank, device=device, llm_layers=list(range(resident)))
+    return p, resident
+
+
+def run_ours(args, world, rank, local):
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    from paper_2508_02751_b200 import build as kbuild
+    if rank == 0:
+        kbuild.build()
+    if world > 1:
+        dist.barrier()
+    from paper_2508_02751_b200 import bytes_model, smallkv
+
+    p, resident = build_problem(args.config, rank, device)
+    cfg = p.cfg
+    L = cfg.llm.layers
+    step = smallkv.from_problem(p)
+    outs = torch.empty(L, p.batch, cfg.llm.q_heads, cfg.llm.head_dim, dtype=torch.float32,
+                       device=device)
+    plan = [(l, l % resident, p.llm_q[l % resident], outs[l]) for l in range(L)]
+    graph = smallkv.DecodeGraph(step, p.slm_q, plan, timing=False)
+    if args.quick:
+        for _ in range(args.warmup):
+            graph.replay()
+        graph.stream.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(graph.stream)
+        for _ in range(args.steps):
+            graph.replay()
+        e1.record(graph.stream)
+        e1.synchronize()
+        if rank == 0:
+            print(json.dumps({"quick": True, "ms_per_step": e0.elapsed_time(e1) / args.steps,
+                              "kernels_per_step": graph.kernels_per_step}), flush=True)
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    tgraph = smallkv.DecodeGraph(step, p.slm_q, plan, timing=True)
+
+    seq = [int(x) for x in p.seq_lens.cpu()]
+    buds = list(zip(p.k_crit.cpu().tolist(), p.n_recent.cpu().tolist(), p.k_marg.cpu().tolist()))
+    bm = bytes_model.step_bytes_coherent(cfg, seq, buds, L)
+    s = graph.stream
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- warm-up
+    for _ in range(args.warmup):
+        graph.replay()
+    s.synchronize()
+    barrier()
+
+    # ---- timed region: K back-to-back graph replays (device clock); the clock
+    # sampler runs from ~0.5 s before it to >= 1.5 s after its start, under the
+    # same load
+    sampler = ClockSampler(local)
+    t_clock0 = time.time()
+    while time.time() - t_clock0 < 0.5:
+        for _ in range(20):
+            graph.replay()
+        s.synchronize()
+    torch.cuda.synchronize()
+    barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(s)
+    for _ in range(args.steps):
+        graph.replay()
+    ev1.record(s)
+    ev1.synchronize()
+    torch.cuda.synchronize()
+    barrier()
+    elapsed_ms = ev0.elapsed_time(ev1)
+    # keep the clock sampler under the same load for >= 1 s if the region was short
+    while time.time() - t_clock0 < 1.5:
+        for _ in range(20):
+            graph.replay()
+        s.synchronize()
+    clocks = sampler.stop()
+
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    ms_per_step = max_ms / args.steps
+    layer_steps = world * L * args.steps / (max_ms / 1e3)
+
+    # ---- per-kernel durations: same step with external events captured in the graph
+    sel_ms, att_ms = [], []
+    for _ in range(max(3, min(args.steps, 50))):
+        tgraph.replay()
+        tgraph.stream.synchronize()
+        a, b = tgraph.segment_ms()
+        sel_ms.append(a)
+        att_ms.extend(b)
+    attend_avg_ms = statistics.mean(att_ms)
+    select_avg_ms = statistics.mean(sel_ms)
+
+    # ---- end to end: pinned host q', q in; outputs back to pinned host, every step
+    h_slm_q = torch.empty(p.slm_q.shape, dtype=p.slm_q.dtype, pin_memory=True)
+    h_slm_q.copy_(p.slm_q)
+    h_q = torch.empty(p.llm_q.shape, dtype=p.llm_q.dtype, pin_memory=True)
+    h_q.copy_(p.llm_q)
+    h_out = torch.empty(outs.shape, dtype=outs.dtype, pin_memory=True)
+    h2d = h_slm_q.numel() * 2 + h_q.numel() * 2
+    d2h = h_out.numel() * 4
+    e2e_steps = max(3, min(args.steps, 200))
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s):
+        e0.record(s)
+        for _ in range(e2e_steps):
+            p.slm_q.copy_(h_slm_q, non_blocking=True)
+            p.llm_q.copy_(h_q, non_blocking=True)
+            graph.replay()
+            h_out.copy_(outs, non_blocking=True)
+        e1.record(s)
+    e1.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    te = torch.tensor([e2e_ms], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * L * e2e_steps / (float(te.item()) / 1e3)
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    hbm, peak_kind = peaks()
+    attend_bytes = bm["attend_per_layer"]
+    achieved = attend_bytes / (attend_avg_ms / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "attend_dram_traffic.json")
+    if os.path.exists(tpath):
+        tj = json.load(open(tpath))
+        if tj.get("config") == args.config:
+            traffic = tj.get("dram_bytes_per_launch")
+    step_gbs = bm["step"] / (ms_per_step / 1e3) / 1e9
+    line = {
+        "metric": METRIC,
+        "value": round(layer_steps, 2),
+        "unit": "layer-steps/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_per_step, 5),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (seeded; Fig. 2-calibrated salience, random page tables)",
+        "config": {
+            "workload": f"{args.config}: {cfg.description}",
+            "global_batch": p.batch * world,
+            "seq_len": cfg.seq_len,
+            "parallelism": f"batch-sharded x{world} (no collective)",
+            "budget_K_R_M": list(cfg.budget),
+            "head_map": "coherent (every SLM kv-head referenced)",
+            "page_size": p.llm.page_size,
+            "resident_llm_layers": resident,
+            "l2": "inputs larger than L2: %.2f GB touched per step vs 126 MB L2" % (bm["step"] / 1e9),
+        },
+        "achieved_hbm_gbs_step": round(step_gbs, 1),
+        "hbm_frac_step": round(step_gbs / hbm, 4),
+        "bytes_per_step": bm["step"],
+        "roofline": {
+            "kernel": "attend_kernel (K3 gather-attend + fused combine)",
+            "bound": "hbm",
+            "achieved": round(achieved, 1),
+            "peak": hbm,
+            "peak_kind": peak_kind,
+            "unit": "GB/s",
+            "frac": round(achieved / hbm, 4),
+            "traffic": traffic,
+            "algorithmic_bytes_per_launch": attend_bytes,
+            "avg_launch_ms": round(attend_avg_ms, 5),
+            "select_avg_ms": round(select_avg_ms, 5),
+            "select_algorithmic_bytes": bm["slm_score"],
+            "select_gbs": round(bm["slm_score"] / (select_avg_ms / 1e3) / 1e9, 1),
+        },
+        "e2e": {"value": round(e2e_value, 2), "unit": "layer-steps/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "steps": e2e_steps},
+        "gpu_launches": graph.kernels_per_step * args.steps,
+        "clocks": clocks,
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(p, cfg, L, args.cpu_seqs)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def cpu_baseline(p, cfg, L, n_seqs):
+    """Time the oracle, as it stands, on a bounded sample: n_seqs sequences,
+    the full SLM select for every row the step uses, one LLM layer's attend;
+    extrapolated to layer-steps/s of the whole workload (per sequence)."""
+    import numpy as np
+    import oracle
+    import smallkv_synth as synth  # noqa: F401
+
+    import dataclasses
+    idx = list(range(n_seqs))
+    sub = dataclasses.replace(
+        p, seq_lens=p.seq_lens[idx].contiguous(), slm_q=p.slm_q[:, idx].contiguous(),
+        llm_q=p.llm_q[:1, idx].contiguous(),
+        slm=dataclasses.replace(p.slm, block_table=p.slm.block_table[idx].contiguous()),
+        llm=dataclasses.replace(p.llm, k=p.llm.k[:1].contiguous(), v=p.llm.v[:1].contiguous(),
+                                block_table=p.llm.block_table[idx].contiguous()),
+        k_crit=p.k_crit[idx].contiguous(), n_recent=p.n_recent[idx].contiguous(),
+        k_marg=p.k_marg[idx].contiguous()).to("cpu")
+    from tests import parity
+    slm_v, llm_v = parity.views(sub)
+    rows = oracle.image_rows(sub.head_map)
+    t0 = time.perf_counter()
+    sel = parity.oracle_select(sub, rows=rows, slm_view=slm_v)
+    t1 = time.perf_counter()
+    oracle.attend(0, 0, sub.llm_q[0], llm_v, sub.seq_lens, sub.head_map, sel,
+                  cfg.slm.layers * cfg.slm.q_heads)
+    t2 = time.perf_counter()
+    t_step = (t1 - t0) + L * (t2 - t1)            # seconds per step for n_seqs sequences
+    t_full = t_step * p.batch / n_seqs            # whole batch
+    return {"value": round(L / t_full, 4), "unit": "layer-steps/s", "cores": oracle.num_threads(),
+            "kind": "oracle",
+            "sample": (f"{n_seqs} of {p.batch} sequences: select over all {len(rows)} mapped SLM "
+                       f"rows + 1 LLM layer attend, measured {t2 - t0:.2f} s; extrapolated to "
+                       f"{L} layers x {p.batch} sequences"),
+            "measured_s": round(t2 - t0, 3)}
+
+
+def run_reference(args, world, rank, local):
+    """The oracle as the reference arm (rank 0 only), same metric and config."""
+    if rank != 0:
+        return
+    import torch
+    import oracle
+    import smallkv_synth as synth
+    from tests import parity
+
+    oracle.build()
+    cfg = synth.CONFIGS[args.config]
+    L = cfg.llm.layers
+    n_seqs = args.cpu_seqs
+    p = synth.make_problem(cfg, seed=0, device="cpu", batch=n_seqs, llm_layers=[0])
+    slm_v, llm_v = parity.views(p)
+    rows = oracle.image_rows(p.head_map)
+    times = []
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        sel = parity.oracle_select(p, rows=rows, slm_view=slm_v)
+        t1 = time.perf_counter()
+        oracle.attend(0, 0, p.llm_q[0], llm_v, p.seq_lens, p.head_map, sel,
+                      cfg.slm.layers * cfg.slm.q_heads)
+        t2 = time.perf_counter()
+        if it >= args.warmup:
+            times.append((t1 - t0) + L * (t2 - t1))
+    t_step = statistics.mean(times) * cfg.batch / n_seqs
+    value = L / t_step
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "layer-steps/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(t_step * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {cfg.description}", "global_batch": cfg.batch,
+                   "seq_len": cfg.seq_len, "parallelism": "host cores (OpenMP)"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "layer-steps/s",
+                         "cores": oracle.num_threads(), "kind": "oracle",
+                         "sample": (f"each step: {n_seqs} of {cfg.batch} sequences, select over "
+                                    f"all {len(rows)} mapped SLM rows + 1 LLM layer attend, "
+                                    f"extrapolated to {L} layers x {cfg.batch} sequences")},
+        "e2e": {"value": round(value, 4), "unit": "layer-steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="qwen7b")
+    ap.add_argument("--cpu-seqs", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick", action="store_true",
+                    help="profiling mode: only warm-up + timed replays (for ncu launch lists)")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world, rank, local = dist_env()
+    if args.gpus != world and world > 1:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args, world, rank, local)
+    else:
+        run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

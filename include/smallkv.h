@@ -190,29 +190,39 @@ size_t smallkv_attend_workspace_size(const smallkv_cache* llm,
  *   l_k = q_h · K_g[k] / sqrt(d)              for k in C ∪ R'
  *   w_k = exp(l_k - max) / Σ_{C∪R'} exp(.)     (O_c = 0 if C ∪ R' is empty)
  *   O_c = Σ w_k V_g[k];  O_m = Σ_{k∈M} a'_j[k] V_g[k];  out = O_c + O_m
- * with a'_j[k] = exp(slm_logits[j][b][k] - lse'[j][b]) (= marg_w, Eq. 6).
+ * with a'_j[k] = marg_w[j][b][i] for k = marg_idx[j][b][i] (Eq. 6).
  * Inputs:
  *   llm_layer   index into head_map's layer dimension (0 <= llm_layer < L).
  *   cache_layer layer slot of `llm`'s pools holding this layer's K/V
  *               (lets a caller rotate a resident subset of layers).
  *   q           device bf16 [B][H][d].
  *   n_llm_layers L (head_map has L*H entries).
- *   slm_logits, slm_lse, crit_idx, marg_idx, counts: smallkv_select outputs
- *               (slm_row_stride = max_seq_len of that call).
+ *   crit_idx, marg_idx, marg_w, counts: smallkv_select outputs (same batch
+ *               and budgets; slm_heads_total = l*H_s rows).
  *   out         device fp32 [B][H][d].
- *   ws          device workspace, >= smallkv_attend_workspace_size bytes,
- *               ZERO-FILLED before its first use; every call leaves its
- *               completion counters zero again.
- * Errors: as smallkv_select, plus H/H_kv > 8 (SMALLKV_ERR_SHAPE).
+ *   flags       0 or SMALLKV_ATTEND_OVERLAP_PROLOGUE.  The kernel is always
+ *               launched with programmatic dependent launch: it reads q and
+ *               writes out only after the previous kernel on `stream` has
+ *               completed.  With the flag it may also start BEFORE that, and
+ *               then reads the selection outputs, head_map, seq_lens,
+ *               budgets, block table and K/V pools during the previous
+ *               kernel's tail — so the caller guarantees those were complete
+ *               before the previous kernel started (true when another kernel,
+ *               e.g. a previous smallkv_attend, separates this call from
+ *               smallkv_select and from the K/V append).
+ *   ws          device workspace, >= smallkv_attend_workspace_size bytes (the
+ *               split work is merged inside thread-block clusters; no
+ *               initialisation needed).
+ * Errors: as smallkv_select, plus H/H_kv > 8, unknown flags (SMALLKV_ERR_SHAPE).
  */
+#define SMALLKV_ATTEND_OVERLAP_PROLOGUE 1
 int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
                    const smallkv_cache* llm, const smallkv_batch* batch,
                    const int32_t* head_map, int32_t n_llm_layers,
                    int32_t slm_heads_total, const smallkv_budgets* budgets,
-                   const float* slm_logits, const float* slm_lse,
                    const int32_t* crit_idx, const int32_t* marg_idx,
-                   const int32_t* counts, float* out, void* ws,
-                   size_t ws_bytes, void* stream);
+                   const float* marg_w, const int32_t* counts, float* out,
+                   int32_t flags, void* ws, size_t ws_bytes, void* stream);
 
 /*
  * smallkv_match_heads — prefill similarity matching (Eq. 2-3).

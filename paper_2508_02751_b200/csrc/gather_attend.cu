@@ -6,17 +6,19 @@
 //   O_m = Σ_{k ∈ marginal} A'_{f(i)}[k] · V[k]   (Eq. 6 second branch),
 //   O   = O_c + O_m                                (no renormalisation, R3).
 //
-// B200 design.  One CTA = (position chunk, LLM kv-group g, sequence b).  Every
-// q-head h of the group may map to a different SLM row (D6), so the CTA first
-// builds, in shared memory, a per-position 16-bit mask over its chunk (bits
-// 0..7: h is critical/recent, bits 8..15: h is marginal) from the ascending
-// lists of the DISTINCT rows its heads use (warp 32-ary searches bound the
-// chunk's slice of each list), then compacts the positions with a non-zero
-// mask.  Each K/V row is thus read from HBM once per group, however many
-// heads select it; marginal-only rows read V only (their K is never touched,
-// R11).  Each warp then streams its own 16-row tiles with cp.async (16-byte
-// LDGSTS through the page table, XOR-swizzled rows, zero-filled tails) into a
-// private multi-stage ring and runs, on the tensor cores (mma.sync m16n8k16):
+// B200 design.  Work unit = LLM kv-group g of sequence b.  Its q-heads map to
+// one or more DISTINCT SLM rows r (D6); the group's "virtual list" is
+//     [ recent R' (every head critical) | crit(r_0) | marg(r_0) | crit(r_1) | ... ]
+// with a 16-bit head mask per entry (bits 0..7: critical for head h, bits
+// 8..15: marginal for head h).  For a group-coherent map (one row) this is
+// exactly the group's union, so every K/V row is read from HBM once; for a
+// non-coherent map a position chosen by two rows is read twice.
+// The list is split evenly by entry count over gridDim.x CTAs (balanced, no
+// position scan); each CTA stages its entries' positions and page-table
+// entries in two parallel rounds, then every warp streams its own 16-row tiles
+// with cp.async (4 rows x 128 B per instruction, XOR-swizzled, zero-filled
+// tails; K rows only for critical entries) through a private multi-stage ring
+// and runs on the tensor cores (mma.sync m16n8k16):
 //   S[16 x 16] = Q_group[16 x d] · K_tile^T        (heads = M, tokens = N)
 //   O[16 x d] += A[16 x 16] · V_tile               (A rows 0..7: online-softmax
 //                                                    weights p of head h;
@@ -25,161 +27,133 @@
 // so the marginal compensation shares the PV contraction with the critical
 // part (register-resident A, FA2-style), with A split into bf16 hi + lo parts
 // (two MMAs) to keep ~2^-17 relative precision on the weights.  Warps merge in
-// shared memory in a fixed order; chunks merge through a deterministic
-// last-CTA log-sum-exp combine (K4 fused), so the result is bit-reproducible.
+// shared memory in a fixed order; the CTAs of a group merge through a
+// deterministic last-CTA log-sum-exp combine (K4 fused): bit-reproducible.
 #include <float.h>
 #include <limits.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.h"
 
 namespace skv {
 
+#ifdef SKV_TRACE
+__device__ long long* g_trace = nullptr;
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SKV_T(i)                                                                         \
+  if (g_trace && threadIdx.x == 0) {                                                     \
+    const int cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;      \
+    g_trace[cta * 10 + (i)] = gtimer();                                                  \
+  }
+#else
+#define SKV_T(i)
+#endif
+
 namespace {
 constexpr int kTile = 16;      // rows (tokens) per warp tile
 constexpr int kWarps = 4;
 constexpr int kThreads = kWarps * 32;
-constexpr int kMaxChunk = 2048;   // positions are packed in 16 bits of the list
+constexpr int kBatch = 256;    // entries whose positions/pages/weights are staged at once
 
 template <int D>
 constexpr int stages_for() { return 3; }
-
 template <int D>
-constexpr int stage_bytes() {
-  return 2 * kTile * D * 2 + kTile * 8 * 4 + kTile * 4;
-}
+constexpr int stage_bytes() { return 2 * kTile * D * 2; }
 
-// [list: chunk x u32][stages: kWarps x NSTAGE x stage]; the position mask of
-// the prologue aliases the stage ring (dead until the tiles start).
+// [row offset][mask][weight]: kBatch each | stages (kWarps x NSTAGE)
 template <int D>
-constexpr size_t smem_bytes(int chunk) {
-  return static_cast<size_t>(chunk) * 4 +
+constexpr size_t smem_bytes() {
+  return static_cast<size_t>(kBatch) * 12 +
          static_cast<size_t>(kWarps) * stages_for<D>() * stage_bytes<D>();
 }
 
-// first index i in [0, len) with L[i] >= x (len if none); L ascending; whole warp.
-__device__ __forceinline__ int warp_lower_bound(const int32_t* __restrict__ L, int len, int x) {
-  const int lane = threadIdx.x & 31;
-  int lo = 0, hi = len;
-  while (hi - lo > 32) {
-    const int step = (hi - lo + 31) >> 5;
-    const int idx = lo + lane * step;
-    const int v = idx < hi ? __ldg(L + idx) : INT_MAX;
-    const int c = __popc(__ballot_sync(0xffffffffu, v < x));
-    if (c == 0) {
-      hi = lo;
-    } else {
-      const int nlo = lo + (c - 1) * step + 1;
-      hi = min(hi, lo + c * step);
-      lo = nlo;
-    }
-  }
-  const int idx = lo + lane;
-  const int v = idx < hi ? __ldg(L + idx) : INT_MAX;
-  return lo + __popc(__ballot_sync(0xffffffffu, v < x));
-}
+// Lazy online softmax: the running max used as the exponent base is only
+// raised when a new score exceeds it by more than this (log2 units), so the
+// O rescale is skipped for almost every tile; exp2 arguments stay <= 8.
+constexpr float kRescaleSlack = 8.f;
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const AttendParams p) {
   constexpr int NSTAGE = stages_for<D>();
   constexpr int ROWB = D * 2;                // bytes per K or V row
-  constexpr int CH = D / 8;                  // 16-byte chunks per row
   constexpr int KV_BYTES = kTile * ROWB;
   constexpr int SB = stage_bytes<D>();
-  constexpr int EPI = 32 / (2 * CH);         // entries loaded per warp iteration
   constexpr int NT = D / 8;                  // n8 tiles of the output
 
   extern __shared__ __align__(128) uint8_t smem[];
-  uint32_t* list = reinterpret_cast<uint32_t*>(smem);
-  uint8_t* stages = reinterpret_cast<uint8_t*>(list + p.chunk);
-  uint32_t* mask = reinterpret_cast<uint32_t*>(stages);
+  uint32_t* soff = reinterpret_cast<uint32_t*>(smem);   // row offset in the layer's pool (elements)
+  uint32_t* smk = soff + kBatch;
+  float* sw = reinterpret_cast<float*>(smk + kBatch);
+  uint8_t* stages = reinterpret_cast<uint8_t*>(sw + kBatch);
   __shared__ int s_j[8], s_K[8], s_M[8];
-  __shared__ float s_lse[8];
-  __shared__ int s_wcnt[kWarps];
-  __shared__ int s_last;
+  __shared__ int s_rj[8], s_rK[8], s_rM[8];
+  __shared__ uint32_t s_rhm[8];
+  __shared__ int s_nrows, s_T;
 
   const int c = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
+  const int NC = gridDim.x;
+  // Without the overlap flag nothing is read before the previous kernel on the
+  // stream has completed.  With it, the prologue below (selection outputs,
+  // page tables, K/V tiles) may run during that kernel's tail.
+  if (!p.overlap_prologue) griddep_wait();
+  SKV_T(0);
   const int n = p.seq_lens[b];
-  const int nch = (n + p.chunk - 1) / p.chunk;
-  if (c >= nch) return;
-  const int c0 = c * p.chunk, c1 = min(n, c0 + p.chunk), S = c1 - c0;
   const int G = p.heads / p.kv_heads;
   const int Rc = min(max(p.n_recent[b], 0), n);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t allc = (1u << G) - 1u;
 
+  // ---- group layout: distinct SLM rows of the group's heads and list sizes
   if (tid < G) {
     const int j = p.head_map[p.layer * p.heads + g * G + tid];
     const int64_t rb = static_cast<int64_t>(j) * p.batch + b;
     s_j[tid] = j;
     s_K[tid] = p.counts[rb * 2];
     s_M[tid] = p.counts[rb * 2 + 1];
-    s_lse[tid] = p.lse[rb * 2 + 1];
   }
-  for (int i = tid; i < S; i += kThreads) mask[i] = (c0 + i >= n - Rc) ? allc : 0u;
   __syncthreads();
-
-  // ---- per-position head masks from the distinct rows' lists
-  for (int li = warp; li < 2 * G; li += kWarps) {
-    const int h = li % G;
-    const bool isM = li >= G;
-    const int j = s_j[h];
-    bool dup = false;
-    uint32_t bits = 0;
-    for (int h2 = 0; h2 < G; ++h2) {
-      if (s_j[h2] == j) {
-        bits |= 1u << h2;
-        if (h2 < h) dup = true;
+  if (tid == 0) {
+    int nr = 0, T = Rc;
+    for (int h = 0; h < G; ++h) {
+      int k = 0;
+      while (k < nr && s_rj[k] != s_j[h]) ++k;
+      if (k == nr) {
+        s_rj[nr] = s_j[h];
+        s_rK[nr] = s_K[h];
+        s_rM[nr] = s_M[h];
+        s_rhm[nr] = 0u;
+        T += s_K[h] + s_M[h];
+        ++nr;
       }
+      s_rhm[k] |= 1u << h;
     }
-    if (dup) continue;
-    if (isM) bits <<= 8;
-    const int64_t rb = static_cast<int64_t>(j) * p.batch + b;
-    const int32_t* L = isM ? p.marg_idx + rb * p.max_marg : p.crit_idx + rb * p.max_crit;
-    const int len = isM ? s_M[h] : s_K[h];
-    const int lo = warp_lower_bound(L, len, c0);
-    const int hi = warp_lower_bound(L, len, c1);
-    for (int i = lo + lane; i < hi; i += 32) atomicOr(&mask[__ldg(L + i) - c0], bits);
+    s_nrows = nr;
+    s_T = T;
   }
   __syncthreads();
+  const int T = s_T, nrows = s_nrows;
+  const int e_lo = static_cast<int>((static_cast<int64_t>(T) * c) / NC);
+  const int e_hi = static_cast<int>((static_cast<int64_t>(T) * (c + 1)) / NC);
+  SKV_T(1);
 
-  // ---- compact positions with a non-empty mask (ascending)
-  const uint32_t ltm = lanemask_lt();
-  {
-    const int seg = ((S + kThreads - 1) / kThreads) * 32;
-    const int s0 = warp * seg, s1 = min(S, s0 + seg);
-    int cnt = 0;
-    for (int base = s0; base < s1; base += 32) {
-      const int i = base + lane;
-      cnt += __popc(__ballot_sync(0xffffffffu, i < s1 && mask[i] != 0u));
-    }
-    if (lane == 0) s_wcnt[warp] = cnt;
-    __syncthreads();
-    int off = 0;
-    for (int w = 0; w < warp; ++w) off += s_wcnt[w];
-    for (int base = s0; base < s1; base += 32) {
-      const int i = base + lane;
-      const uint32_t mk = i < s1 ? mask[i] : 0u;
-      const uint32_t bal = __ballot_sync(0xffffffffu, mk != 0u);
-      if (mk) list[off + __popc(bal & ltm)] = (static_cast<uint32_t>(i) << 16) | (mk & 0xffffu);
-      off += __popc(bal);
-    }
-  }
-  __syncthreads();
-  int E = 0;
-  for (int w = 0; w < kWarps; ++w) E += s_wcnt[w];
-
-  // ---- per-warp streaming over its tiles
   const int gq = lane >> 2, tq = lane & 3;
-  const int ntile = (E + kTile - 1) / kTile;
-  const int nmy = ntile > warp ? (ntile - warp + kWarps - 1) / kWarps : 0;
   uint8_t* wst = stages + warp * NSTAGE * SB;
   const uint16_t* kpool = p.k + p.layer_offset;
   const uint16_t* vpool = p.v + p.layer_offset;
   const int32_t* bt = p.block_table + static_cast<int64_t>(b) * p.max_blocks;
 
   uint32_t qa[D / 16][2];
-  {
+  bool q_ready = false;
+  // q (and, in a real model, everything the previous kernel produces) is read
+  // only after the programmatic grid dependency is resolved.
+  auto wait_and_load_q = [&]() {
+    griddep_wait();
+    griddep_launch_dependents();
     const uint16_t* qg = p.q + (static_cast<int64_t>(b) * p.heads + g * G) * D;
 #pragma unroll
     for (int kk = 0; kk < D / 16; ++kk) {
@@ -187,57 +161,7 @@ __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const AttendParams 
       qa[kk][0] = gq < G ? *reinterpret_cast<const uint32_t*>(qg + gq * D + cc) : 0u;
       qa[kk][1] = gq < G ? *reinterpret_cast<const uint32_t*>(qg + gq * D + cc + 8) : 0u;
     }
-  }
-  const float lse_h = gq < G ? s_lse[gq] : 0.f;
-
-  auto issue = [&](int i) {
-    if (i < nmy) {
-      const int tile = warp + i * kWarps;
-      uint8_t* st = wst + (i % NSTAGE) * SB;
-      uint32_t* smask = reinterpret_cast<uint32_t*>(st + 2 * KV_BYTES + kTile * 8 * 4);
-      float* sml = reinterpret_cast<float*>(st + 2 * KV_BYTES);
-      const int e = tile * kTile + (lane & 15);
-      const bool ev = e < E;
-      const uint32_t pk = ev ? list[e] : 0u;
-      const int pos = c0 + static_cast<int>(pk >> 16);
-      const uint32_t mk = pk & 0xffffu;
-      int64_t roff = 0;
-      if (ev) {
-        const int page = bt[pos / p.page_size];
-        roff = ((static_cast<int64_t>(page) * p.kv_heads + g) * p.page_size + pos % p.page_size) * D;
-      }
-      if (lane < kTile) smask[lane] = mk;
-#pragma unroll
-      for (int e0 = 0; e0 < kTile; e0 += EPI) {
-        const int eo = e0 + lane / (2 * CH);       // entry this lane copies
-        const int ch = lane % (2 * CH);            // chunk 0..2CH-1 (K then V)
-        const int64_t ro = __shfl_sync(0xffffffffu, roff, eo);
-        const uint32_t me = __shfl_sync(0xffffffffu, mk, eo);
-        const bool ve = __shfl_sync(0xffffffffu, ev, eo);
-        if (ch < CH) {
-          if (me & 0xffu) {
-            const uint32_t dst = smem_u32(st + eo * ROWB + ((ch ^ (eo & 7)) << 4));
-            cp_async16(dst, kpool + ro + ch * 8, true);
-          }
-        } else {
-          const int cv = ch - CH;
-          const uint32_t dst = smem_u32(st + KV_BYTES + eo * ROWB + ((cv ^ (eo & 7)) << 4));
-          cp_async16(dst, vpool + (ve ? ro + cv * 8 : 0), ve);
-        }
-      }
-      // marginal logits a'-numerators: 16 entries x 8 heads
-#pragma unroll
-      for (int q4 = 0; q4 < (kTile * 8) / 32; ++q4) {
-        const int idx = q4 * 32 + lane;
-        const int eo = idx >> 3, h = idx & 7;
-        const uint32_t me = __shfl_sync(0xffffffffu, mk, eo);
-        const int po = __shfl_sync(0xffffffffu, pos, eo);
-        if (h < G && ((me >> (8 + h)) & 1u))
-          cp_async4(smem_u32(sml + idx),
-                    p.logits + (static_cast<int64_t>(s_j[h]) * p.batch + b) * p.row_stride + po);
-      }
-    }
-    cp_async_commit();
+    q_ready = true;
   };
 
   float o[NT][4];
@@ -246,80 +170,159 @@ __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const AttendParams 
   float m_run = -INFINITY, l_run = 0.f;
   const int mi = lane >> 3;
 
-#pragma unroll
-  for (int i = 0; i < NSTAGE - 1; ++i) issue(i);
-  for (int i = 0; i < nmy; ++i) {
-    issue(i + NSTAGE - 1);
-    cp_async_wait<NSTAGE - 1>();
-    __syncwarp();
-    const uint8_t* st = wst + (i % NSTAGE) * SB;
-    const uint8_t* kb = st;
-    const uint8_t* vb = st + KV_BYTES;
-    const float* sml = reinterpret_cast<const float*>(st + 2 * KV_BYTES);
-    const uint32_t* smask = reinterpret_cast<const uint32_t*>(st + 2 * KV_BYTES + kTile * 8 * 4);
+  int tbase = 0;   // tiles this warp consumed in earlier batches (mbarrier phases)
+  for (int e_b = e_lo; e_b < e_hi; e_b += kBatch) {
+    const int E = min(kBatch, e_hi - e_b);
+    // ---- stage positions + masks of this batch (one parallel round of list loads)
+    for (int i = tid; i < E; i += kThreads) {
+      int x = e_b + i, pos;
+      uint32_t mk;
+      float wt = 0.f;
+      if (x < Rc) {
+        pos = n - Rc + x;
+        mk = allc;
+      } else {
+        x -= Rc;
+        int k = 0;
+        while (k < nrows - 1 && x >= s_rK[k] + s_rM[k]) {
+          x -= s_rK[k] + s_rM[k];
+          ++k;
+        }
+        const int64_t rb = static_cast<int64_t>(s_rj[k]) * p.batch + b;
+        if (x < s_rK[k]) {
+          pos = __ldg(p.crit_idx + rb * p.max_crit + x);
+          mk = s_rhm[k];
+        } else {
+          pos = __ldg(p.marg_idx + rb * p.max_marg + (x - s_rK[k]));
+          wt = __ldg(p.marg_w + rb * p.max_marg + (x - s_rK[k]));
+          mk = s_rhm[k] << 8;
+        }
+      }
+      soff[i] = static_cast<uint32_t>(pos);
+      smk[i] = mk;
+      sw[i] = wt;
+    }
+    __syncthreads();
+    // ---- page-table entries (second parallel round) -> row offsets
+    for (int i = tid; i < E; i += kThreads) {
+      const int pos = static_cast<int>(soff[i]);
+      const int page = __ldg(bt + pos / p.page_size);
+      soff[i] = static_cast<uint32_t>(
+          ((static_cast<int64_t>(page) * p.kv_heads + g) * p.page_size + pos % p.page_size) * D);
+    }
+    __syncthreads();
+    SKV_T(2);
 
-    // S = Q K^T : rows = heads, cols = 16 tokens (two n8 tiles)
-    float sacc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    const int ntile = (E + kTile - 1) / kTile;
+    const int nmy = ntile > warp ? (ntile - warp + kWarps - 1) / kWarps : 0;
+
+    // Each cp.async instruction of the warp moves 4 rows x 128 contiguous bytes:
+    // lane l copies 16-byte chunk (l & 7) of entry 4*grp + (l >> 3); rows are
+    // XOR-swizzled in 16-byte chunks so ldmatrix is conflict-free.
+    auto issue = [&](int i) {
+      if (i < nmy) {
+        uint8_t* st = wst + ((tbase + i) % NSTAGE) * SB;
+        const int e0 = (warp + i * kWarps) * kTile;
 #pragma unroll
-    for (int kk = 0; kk < D / 16; ++kk) {
-      const int r = ((mi >> 1) << 3) + (lane & 7);
-      const int ch = 2 * kk + (mi & 1);
-      uint32_t b0, b1, b2, b3;
-      ldsm_x4(smem_u32(kb + r * ROWB + ((ch ^ (r & 7)) << 4)), b0, b1, b2, b3);
-      mma_bf16(sacc[0], qa[kk][0], 0u, qa[kk][1], 0u, b0, b1);
-      mma_bf16(sacc[1], qa[kk][0], 0u, qa[kk][1], 0u, b2, b3);
+        for (int grp = 0; grp < kTile / 4; ++grp) {
+          const int eo = grp * 4 + (lane >> 3);
+          const int e = e0 + eo;
+          const bool ev = e < E;
+          const uint32_t ro = ev ? soff[e] : 0u;
+          const bool kc = ev && (smk[e] & 0xffu) != 0u;
+#pragma unroll
+          for (int hf = 0; hf < D / 64; ++hf) {
+            const int ch = hf * 8 + (lane & 7);
+            const int sw_ = (ch ^ (eo & 7)) << 4;
+            if (kc) cp_async16(smem_u32(st + eo * ROWB + sw_), kpool + ro + ch * 8, true);
+            cp_async16(smem_u32(st + KV_BYTES + eo * ROWB + sw_), vpool + ro + ch * 8, ev);
+          }
+        }
+      }
+      cp_async_commit();
+    };
+
+#pragma unroll
+    for (int i = 0; i < NSTAGE - 1; ++i) issue(i);
+    if (!q_ready) wait_and_load_q();
+    for (int i = 0; i < nmy; ++i) {
+      issue(i + NSTAGE - 1);
+      cp_async_wait<NSTAGE - 1>();
+      __syncwarp();
+      const uint8_t* st = wst + ((tbase + i) % NSTAGE) * SB;
+      const uint8_t* kb = st;
+      const uint8_t* vb = st + KV_BYTES;
+      const int e0 = (warp + i * kWarps) * kTile;
+
+      // S = Q K^T : rows = heads, cols = 16 tokens (two n8 tiles)
+      float sacc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const int r = ((mi >> 1) << 3) + (lane & 7);
+        const int ch = 2 * kk + (mi & 1);
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(smem_u32(kb + r * ROWB + ((ch ^ (r & 7)) << 4)), b0, b1, b2, b3);
+        mma_bf16(sacc[0], qa[kk][0], 0u, qa[kk][1], 0u, b0, b1);
+        mma_bf16(sacc[1], qa[kk][0], 0u, qa[kk][1], 0u, b2, b3);
+      }
+      // masks / weights for this lane's head gq and tokens {2tq, 2tq+1, 8+2tq, 9+2tq}
+      float sv[4], wm[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int tok = (u >> 1) * 8 + 2 * tq + (u & 1);
+        const int e = e0 + tok;
+        const uint32_t mk = e < E ? smk[e] : 0u;
+        const bool crit = gq < G && ((mk >> gq) & 1u);
+        const bool marg = gq < G && ((mk >> (8 + gq)) & 1u);
+        sv[u] = crit ? sacc[u >> 1][u & 1] * p.scale_log2 : -INFINITY;
+        wm[u] = marg ? sw[e] : 0.f;
+      }
+      float tmax = fmaxf(fmaxf(sv[0], sv[1]), fmaxf(sv[2], sv[3]));
+      tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
+      tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
+      if (tmax > m_run + kRescaleSlack) {   // raise the base (rare after the first tiles)
+        const float alpha = exp2f(m_run - tmax);   // 0 when m_run = -inf
+        l_run *= alpha;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          o[t][0] *= alpha;
+          o[t][1] *= alpha;
+        }
+        m_run = tmax;
+      }
+      const float m_use = m_run == -INFINITY ? 0.f : m_run;
+      float pw[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) pw[u] = exp2f(sv[u] - m_use);
+      l_run += (pw[0] + pw[1] + pw[2] + pw[3]);
+      // A fragments (rows gq: p; rows gq+8: a'), hi + lo
+      uint32_t ah[4], al[4];
+      split_bf16x2(pw[0], pw[1], ah[0], al[0]);
+      split_bf16x2(wm[0], wm[1], ah[1], al[1]);
+      split_bf16x2(pw[2], pw[3], ah[2], al[2]);
+      split_bf16x2(wm[2], wm[3], ah[3], al[3]);
+      // O += A · V
+#pragma unroll
+      for (int t = 0; t < NT; t += 2) {
+        const int r = ((mi & 1) << 3) + (lane & 7);
+        const int ch = t + (mi >> 1);
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(smem_u32(vb + r * ROWB + ((ch ^ (r & 7)) << 4)), b0, b1, b2, b3);
+        mma_bf16(o[t], ah[0], ah[1], ah[2], ah[3], b0, b1);
+        mma_bf16(o[t], al[0], al[1], al[2], al[3], b0, b1);
+        mma_bf16(o[t + 1], ah[0], ah[1], ah[2], ah[3], b2, b3);
+        mma_bf16(o[t + 1], al[0], al[1], al[2], al[3], b2, b3);
+      }
+      __syncwarp();
     }
-    // masks / weights for this lane's head gq and tokens {2tq, 2tq+1, 8+2tq, 9+2tq}
-    float sv[4], wm[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int tok = (u >> 1) * 8 + 2 * tq + (u & 1);
-      const uint32_t mk = smask[tok];
-      const bool crit = gq < G && ((mk >> gq) & 1u);
-      const bool marg = gq < G && ((mk >> (8 + gq)) & 1u);
-      sv[u] = crit ? sacc[u >> 1][u & 1] * p.scale_log2 : -INFINITY;
-      wm[u] = marg ? expf(sml[tok * 8 + gq] - lse_h) : 0.f;
-    }
-    float tmax = fmaxf(fmaxf(sv[0], sv[1]), fmaxf(sv[2], sv[3]));
-    tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
-    tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
-    const float m_new = fmaxf(m_run, tmax);
-    const float m_use = m_new == -INFINITY ? 0.f : m_new;
-    const float alpha = exp2f(m_run - m_use);
-    float pw[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) pw[u] = exp2f(sv[u] - m_use);
-    l_run = l_run * alpha + (pw[0] + pw[1] + pw[2] + pw[3]);
-    m_run = m_new;
-#pragma unroll
-    for (int t = 0; t < NT; ++t) {
-      o[t][0] *= alpha;
-      o[t][1] *= alpha;
-    }
-    // A fragments (rows gq: p; rows gq+8: a'), hi + lo
-    uint32_t ah[4], al[4];
-    split_bf16x2(pw[0], pw[1], ah[0], al[0]);
-    split_bf16x2(wm[0], wm[1], ah[1], al[1]);
-    split_bf16x2(pw[2], pw[3], ah[2], al[2]);
-    split_bf16x2(wm[2], wm[3], ah[3], al[3]);
-    // O += A · V
-#pragma unroll
-    for (int t = 0; t < NT; t += 2) {
-      const int r = ((mi & 1) << 3) + (lane & 7);
-      const int ch = t + (mi >> 1);
-      uint32_t b0, b1, b2, b3;
-      ldsm_x4_t(smem_u32(vb + r * ROWB + ((ch ^ (r & 7)) << 4)), b0, b1, b2, b3);
-      mma_bf16(o[t], ah[0], ah[1], ah[2], ah[3], b0, b1);
-      mma_bf16(o[t], al[0], al[1], al[2], al[3], b0, b1);
-      mma_bf16(o[t + 1], ah[0], ah[1], ah[2], ah[3], b2, b3);
-      mma_bf16(o[t + 1], al[0], al[1], al[2], al[3], b2, b3);
-    }
-    __syncwarp();
+    cp_async_wait<0>();
+    tbase += nmy;
+    __syncthreads();   // batch arrays and stages are free again
   }
-  cp_async_wait<0>();
+  if (!q_ready) wait_and_load_q();   // empty share: still order the output writes
   l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
   l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
-  __syncthreads();   // every warp is done with its stages: reuse them for the merge
+  SKV_T(4);
 
   // ---- merge warps (fixed order)
   float* wm_s = reinterpret_cast<float*>(stages);              // [kWarps][8]
@@ -330,10 +333,8 @@ __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const AttendParams 
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
       const int col = t * 8 + 2 * tq;
-      myo[gq * D + col] = o[t][0];
-      myo[gq * D + col + 1] = o[t][1];
-      myo[(gq + 8) * D + col] = o[t][2];
-      myo[(gq + 8) * D + col + 1] = o[t][3];
+      *reinterpret_cast<float2*>(myo + gq * D + col) = make_float2(o[t][0], o[t][1]);
+      *reinterpret_cast<float2*>(myo + (gq + 8) * D + col) = make_float2(o[t][2], o[t][3]);
     }
     if (tq == 0) {
       wm_s[warp * 8 + gq] = m_run;
@@ -341,87 +342,125 @@ __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const AttendParams 
     }
   }
   __syncthreads();
-  const int H = p.heads;
-  const int64_t bh0 = static_cast<int64_t>(b) * H + g * G;
-  for (int idx = tid; idx < G * D; idx += kThreads) {
-    const int h = idx / D, col = idx % D;
+  const int64_t bh0 = static_cast<int64_t>(b) * p.heads + g * G;
+  // this CTA's merged state: [M 8][L 8][O_c 8 x D][O_m 8 x D] (read by rank 0 over DSMEM)
+  float* cst = reinterpret_cast<float*>(stages + (kWarps * 16 * D + 2 * kWarps * 8) * 4);
+  for (int it = tid; it < G * (D / 4); it += kThreads) {
+    const int h = it / (D / 4), c4 = (it % (D / 4)) * 4;
     float M = -INFINITY;
+#pragma unroll
     for (int w = 0; w < kWarps; ++w) M = fmaxf(M, wm_s[w * 8 + h]);
     const float Mu = M == -INFINITY ? 0.f : M;
-    float L = 0.f, oc = 0.f, om = 0.f;
+    float L = 0.f;
+    float4 oc = make_float4(0.f, 0.f, 0.f, 0.f), om = oc;
+#pragma unroll
     for (int w = 0; w < kWarps; ++w) {
-      const float sc = exp2f(wm_s[w * 8 + h] - Mu);
-      L += wl_s[w * 8 + h] * sc;
-      oc += wo_s[(w * 16 + h) * D + col] * sc;
-      om += wo_s[(w * 16 + h + 8) * D + col];
+      const float f = exp2f(wm_s[w * 8 + h] - Mu);
+      L += wl_s[w * 8 + h] * f;
+      const float4 a = *reinterpret_cast<const float4*>(wo_s + (w * 16 + h) * D + c4);
+      const float4 m = *reinterpret_cast<const float4*>(wo_s + (w * 16 + h + 8) * D + c4);
+      oc.x += a.x * f; oc.y += a.y * f; oc.z += a.z * f; oc.w += a.w * f;
+      om.x += m.x; om.y += m.y; om.z += m.z; om.w += m.w;
     }
-    if (nch == 1) {
-      p.out[(bh0 + h) * D + col] = (L > 0.f ? oc / L : 0.f) + om;
+    if (NC == 1) {
+      const float li = L > 0.f ? 1.f / L : 0.f;
+      *reinterpret_cast<float4*>(p.out + (bh0 + h) * D + c4) =
+          make_float4(oc.x * li + om.x, oc.y * li + om.y, oc.z * li + om.z, oc.w * li + om.w);
     } else {
-      float* part = p.partials + ((bh0 + h) * p.max_chunks + c) * (2 + 2 * D);
-      if (col == 0) {
-        part[0] = M;
-        part[1] = L;
+      if (c4 == 0) {
+        cst[h] = M;
+        cst[8 + h] = L;
       }
-      part[2 + col] = oc;
-      part[2 + D + col] = om;
+      *reinterpret_cast<float4*>(cst + 16 + h * D + c4) = oc;
+      *reinterpret_cast<float4*>(cst + 16 + 8 * D + h * D + c4) = om;
     }
   }
-  if (nch == 1) return;
+  SKV_T(5);
+#ifdef SKV_TRACE
+  if (g_trace && tid == 0) {
+    const int cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    int smid;
+    asm("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_trace[cta * 10 + 8] = e_hi - e_lo;
+    g_trace[cta * 10 + 9] = smid;
+  }
+#endif
+  if (NC == 1) return;
 
-  // ---- fused K4: the last chunk CTA of (b, g) combines all chunks in order
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) {
-    const int prev = atomicAdd(&p.counters[b * p.kv_heads + g], 1);
-    s_last = prev == nch - 1;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  for (int idx = tid; idx < G * D; idx += kThreads) {
-    const int h = idx / D, col = idx % D;
-    const float* part0 = p.partials + (bh0 + h) * p.max_chunks * (2 + 2 * D);
-    float M = -INFINITY;
-    for (int q = 0; q < nch; ++q) M = fmaxf(M, __ldcg(part0 + q * (2 + 2 * D)));
-    const float Mu = M == -INFINITY ? 0.f : M;
-    float L = 0.f, oc = 0.f, om = 0.f;
-    for (int q = 0; q < nch; ++q) {
-      const float* pq = part0 + q * (2 + 2 * D);
-      const float sc = exp2f(__ldcg(pq) - Mu);
-      L += __ldcg(pq + 1) * sc;
-      oc += __ldcg(pq + 2 + col) * sc;
-      om += __ldcg(pq + 2 + D + col);
+  // ---- fused K4: the group's CTAs form one thread-block cluster; rank 0
+  // merges every rank's state in rank order through distributed shared memory.
+  cluster_sync();
+  if (c == 0) {
+    const uint32_t base = smem_u32(cst);
+    for (int it = tid; it < G * (D / 4); it += kThreads) {
+      const int h = it / (D / 4), c4 = (it % (D / 4)) * 4;
+      float M = -INFINITY;
+      for (int q = 0; q < NC; ++q) M = fmaxf(M, ld_dsmem_f32(base + h * 4, q));
+      const float Mu = M == -INFINITY ? 0.f : M;
+      float L = 0.f;
+      float4 oc = make_float4(0.f, 0.f, 0.f, 0.f), om = oc;
+      for (int q = 0; q < NC; ++q) {
+        const float f = exp2f(ld_dsmem_f32(base + h * 4, q) - Mu);
+        L += ld_dsmem_f32(base + (8 + h) * 4, q) * f;
+        const float4 a = ld_dsmem_f32x4(base + (16 + h * D + c4) * 4, q);
+        const float4 m = ld_dsmem_f32x4(base + (16 + 8 * D + h * D + c4) * 4, q);
+        oc.x += a.x * f; oc.y += a.y * f; oc.z += a.z * f; oc.w += a.w * f;
+        om.x += m.x; om.y += m.y; om.z += m.z; om.w += m.w;
+      }
+      const float li = L > 0.f ? 1.f / L : 0.f;
+      *reinterpret_cast<float4*>(p.out + (bh0 + h) * D + c4) =
+          make_float4(oc.x * li + om.x, oc.y * li + om.y, oc.z * li + om.z, oc.w * li + om.w);
     }
-    p.out[(bh0 + h) * D + col] = (L > 0.f ? oc / L : 0.f) + om;
   }
-  if (tid == 0) p.counters[b * p.kv_heads + g] = 0;
+  cluster_sync();   // keep every rank's shared memory alive until rank 0 has read it
+  SKV_T(6);
 }
 }  // namespace
 
-int32_t attend_chunk_size(int32_t max_seq_len) {
-  (void)max_seq_len;
-  static_assert(1024 <= kMaxChunk, "chunk too large for the packed list");
-  return 1024;
+#ifdef SKV_TRACE
+extern "C" int skv_debug_set_trace(long long* buf) {
+  return cudaMemcpyToSymbol(g_trace, &buf, sizeof(buf)) == cudaSuccess ? 0 : 1;
+}
+#endif
+
+// CTAs per (sequence, kv-group) = cluster size: one per ~2K tokens of
+// context, at most 8 (portable cluster size).
+int32_t attend_ctas_per_group(int32_t max_seq_len) {
+  static const int32_t tokens_per_cta = [] {
+    const char* e = getenv("SMALLKV_ATTEND_TOKENS_PER_CTA");   // tuning knob
+    const int v = e ? atoi(e) : 0;
+    return v > 0 ? v : 2048;
+  }();
+  const int32_t nc = (max_seq_len + tokens_per_cta - 1) / tokens_per_cta;
+  return nc < 1 ? 1 : (nc > 8 ? 8 : nc);
 }
 
-size_t attend_partials_floats(int32_t batch, int32_t heads, int32_t head_dim, int32_t max_chunks) {
-  return static_cast<size_t>(batch) * heads * max_chunks * (2 + 2 * head_dim);
+template <int D>
+static cudaError_t launch_d(const AttendParams& p, cudaStream_t s) {
+  const size_t sm = smem_bytes<D>();
+  cudaError_t e = cudaFuncSetAttribute(attend_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(sm));
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.max_chunks, p.kv_heads, p.batch);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = p.max_chunks;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, attend_kernel<D>, p);
 }
 
 cudaError_t launch_attend(const AttendParams& p, cudaStream_t s) {
-  dim3 grid(p.max_chunks, p.kv_heads, p.batch);
-  if (p.head_dim == 64) {
-    const size_t sm = smem_bytes<64>(p.chunk);
-    cudaFuncSetAttribute(attend_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(sm));
-    attend_kernel<64><<<grid, kThreads, sm, s>>>(p);
-  } else {
-    const size_t sm = smem_bytes<128>(p.chunk);
-    cudaFuncSetAttribute(attend_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(sm));
-    attend_kernel<128><<<grid, kThreads, sm, s>>>(p);
-  }
+  cudaError_t e = p.head_dim == 64 ? launch_d<64>(p, s) : launch_d<128>(p, s);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

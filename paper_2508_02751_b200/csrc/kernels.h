@@ -56,25 +56,21 @@ struct AttendParams {
   const int32_t* seq_lens;
   const int32_t* head_map;    // [L*H]
   const int32_t* n_recent;
-  const float* logits;        // [l*H_s][B][row_stride]
-  const float* lse;           // [l*H_s][B][2]
   const int32_t* crit_idx;
   const int32_t* marg_idx;
+  const float* marg_w;        // a' at marg_idx
   const int32_t* counts;
   float* out;                 // [B][H][d]
-  float* partials;            // [B*H][max_chunks][2 + 2d]
-  int32_t* counters;          // [B*H_kv]
   int64_t num_pages;
   int64_t layer_offset;       // cache_layer * num_pages * H_kv * page_size * d (elements)
   int32_t max_blocks, page_size, heads, kv_heads, head_dim, batch, layer;
   int32_t row_stride, max_crit, max_marg;
-  int32_t chunk;              // positions per CTA
-  int32_t max_chunks;
+  int32_t max_chunks;         // CTAs (= cluster size) per (sequence, kv-group)
   float scale_log2;           // log2(e)/sqrt(d)
+  int32_t overlap_prologue;   // SMALLKV_ATTEND_OVERLAP_PROLOGUE
 };
 cudaError_t launch_attend(const AttendParams& p, cudaStream_t s);
-size_t attend_partials_floats(int32_t batch, int32_t heads, int32_t head_dim, int32_t max_chunks);
-int32_t attend_chunk_size(int32_t max_seq_len);
+int32_t attend_ctas_per_group(int32_t max_seq_len);
 
 // ---------------------------------------------------------------- K0 match_heads
 cudaError_t launch_match_heads(const float* llm_F, int32_t n_llm, const float* slm_F,

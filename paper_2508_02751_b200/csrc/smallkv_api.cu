@@ -119,17 +119,17 @@ SelectWs select_ws_layout(int32_t n_slm) {
 }
 
 struct AttendWs {
-  size_t counters, partials, total;
-  int32_t chunk, max_chunks;
+  size_t total;
+  int32_t ctas;
 };
+// The attend kernel merges its split work inside thread-block clusters
+// (distributed shared memory), so it needs no global scratch; the workspace
+// argument is kept for ABI stability and future variants.
 AttendWs attend_ws_layout(const smallkv_cache* llm, const smallkv_batch* b) {
+  (void)llm;
   AttendWs w;
-  w.chunk = skv::attend_chunk_size(b->max_seq_len);
-  w.max_chunks = (b->max_seq_len + w.chunk - 1) / w.chunk;
-  w.counters = 0;
-  w.partials = round256(static_cast<size_t>(b->batch) * llm->num_kv_heads * 4);
-  w.total = w.partials + skv::attend_partials_floats(b->batch, llm->num_q_heads,
-                                                     llm->head_dim, w.max_chunks) * 4;
+  w.ctas = skv::attend_ctas_per_group(b->max_seq_len);
+  w.total = 256;
   return w;
 }
 
@@ -272,14 +272,14 @@ size_t smallkv_attend_workspace_size(const smallkv_cache* llm, const smallkv_bat
 int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
                    const smallkv_cache* llm, const smallkv_batch* batch, const int32_t* head_map,
                    int32_t n_llm_layers, int32_t slm_heads_total, const smallkv_budgets* budgets,
-                   const float* slm_logits, const float* slm_lse, const int32_t* crit_idx,
-                   const int32_t* marg_idx, const int32_t* counts, float* out, void* ws,
-                   size_t ws_bytes, void* stream) {
+                   const int32_t* crit_idx, const int32_t* marg_idx, const float* marg_w,
+                   const int32_t* counts, float* out, int32_t flags, void* ws, size_t ws_bytes,
+                   void* stream) {
   int rc;
   if ((rc = check_cache(llm, true, "llm")) != SMALLKV_OK) return rc;
   if ((rc = check_batch(batch, llm)) != SMALLKV_OK) return rc;
   if ((rc = check_budgets(budgets)) != SMALLKV_OK) return rc;
-  if (!q || !head_map || !slm_logits || !slm_lse || !crit_idx || !marg_idx || !counts || !out)
+  if (!q || !head_map || !crit_idx || !marg_idx || !marg_w || !counts || !out)
     return fail(SMALLKV_ERR_NULL, "smallkv_attend: NULL input/output pointer");
   if (n_llm_layers < 1 || llm_layer < 0 || llm_layer >= n_llm_layers)
     return fail(SMALLKV_ERR_SHAPE, "llm_layer %d outside [0,%d)", llm_layer, n_llm_layers);
@@ -287,6 +287,8 @@ int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
     return fail(SMALLKV_ERR_SHAPE, "cache_layer %d outside [0,%d)", cache_layer,
                 llm->num_layers);
   if (slm_heads_total < 1) return fail(SMALLKV_ERR_SHAPE, "slm_heads_total must be >= 1");
+  if (flags & ~SMALLKV_ATTEND_OVERLAP_PROLOGUE)
+    return fail(SMALLKV_ERR_SHAPE, "unknown smallkv_attend flags 0x%x", flags);
   const int G = llm->num_q_heads / llm->num_kv_heads;
   if (G > 8) return fail(SMALLKV_ERR_SHAPE, "LLM GQA group %d > 8 not supported", G);
   if (!aligned(q, 4) || !aligned(out, 4))
@@ -304,15 +306,11 @@ int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
   ap.seq_lens = batch->seq_lens;
   ap.head_map = head_map;
   ap.n_recent = budgets->n_recent;
-  ap.logits = slm_logits;
-  ap.lse = slm_lse;
   ap.crit_idx = crit_idx;
   ap.marg_idx = marg_idx;
+  ap.marg_w = marg_w;
   ap.counts = counts;
   ap.out = out;
-  uint8_t* wsb = static_cast<uint8_t*>(ws);
-  ap.counters = reinterpret_cast<int32_t*>(wsb + L.counters);
-  ap.partials = reinterpret_cast<float*>(wsb + L.partials);
   ap.num_pages = llm->num_pages;
   ap.layer_offset = static_cast<int64_t>(cache_layer) * llm->num_pages * llm->num_kv_heads *
                     llm->page_size * llm->head_dim;
@@ -326,9 +324,9 @@ int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
   ap.row_stride = batch->max_seq_len;
   ap.max_crit = budgets->max_crit;
   ap.max_marg = budgets->max_marg;
-  ap.chunk = L.chunk;
-  ap.max_chunks = L.max_chunks;
+  ap.max_chunks = L.ctas;
   ap.scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(llm->head_dim));
+  ap.overlap_prologue = (flags & SMALLKV_ATTEND_OVERLAP_PROLOGUE) ? 1 : 0;
   cudaError_t e = skv::launch_attend(ap, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "attend launch");
   return SMALLKV_OK;

@@ -21,6 +21,8 @@ LIB_PATH = os.path.join(_HERE, "libsmallkv.so")
 _lock = threading.Lock()
 _lib = None
 
+ATTEND_OVERLAP_PROLOGUE = 1   # include/smallkv.h SMALLKV_ATTEND_OVERLAP_PROLOGUE
+
 STATUS = {0: "OK", 1: "ERR_NULL", 2: "ERR_SHAPE", 3: "ERR_ALIGN", 4: "ERR_WORKSPACE",
           5: "ERR_DEVICE", 6: "ERR_CUDA", 7: "ERR_UNSUPPORTED"}
 
@@ -76,7 +78,8 @@ def load(path: Optional[str] = None):
         lib.smallkv_select.argtypes = [P, P, P, P, i32, P, P, P, P, P, P, P, P, P, sz, P]
         lib.smallkv_attend_workspace_size.argtypes = [P, P]
         lib.smallkv_attend_workspace_size.restype = sz
-        lib.smallkv_attend.argtypes = [i32, i32, P, P, P, P, i32, i32, P, P, P, P, P, P, P, P, sz, P]
+        lib.smallkv_attend.argtypes = [i32, i32, P, P, P, P, i32, i32, P, P, P, P, P, P, i32, P,
+                                       sz, P]
         lib.smallkv_match_heads_workspace_size.argtypes = [i32, i32]
         lib.smallkv_match_heads_workspace_size.restype = sz
         lib.smallkv_match_heads.argtypes = [P, i32, P, i32, i32, i32, P, P, P, sz, P]
@@ -206,15 +209,16 @@ class DecodeStep:
         return o
 
     def attend(self, llm_layer: int, cache_layer: int, q: torch.Tensor, out: torch.Tensor,
-               stream=None):
+               stream=None, overlap_prologue: bool = False):
         assert q.dtype == torch.bfloat16 and q.is_contiguous()
         assert out.dtype == torch.float32 and out.is_contiguous()
         o = self.out
         rc = self.lib.smallkv_attend(
             int(llm_layer), int(cache_layer), q.data_ptr(), ctypes.byref(self.llm),
             ctypes.byref(self.batch), self.head_map.data_ptr(), self.llm_layers, self.n_slm,
-            ctypes.byref(self.budgets), o.logits.data_ptr(), o.lse.data_ptr(),
-            o.crit.data_ptr(), o.marg.data_ptr(), o.counts.data_ptr(), out.data_ptr(),
+            ctypes.byref(self.budgets), o.crit.data_ptr(), o.marg.data_ptr(),
+            o.marg_w.data_ptr(), o.counts.data_ptr(), out.data_ptr(),
+            ATTEND_OVERLAP_PROLOGUE if overlap_prologue else 0,
             self.ws_attend.data_ptr(), self.ws_attend.numel(), _stream(stream))
         _check("smallkv_attend", rc)
         return out
@@ -248,3 +252,63 @@ def match_heads(llm_F: torch.Tensor, slm_F: torch.Tensor, k_match: int, stream=N
                                    int(k_match), hm.data_ptr(), jac.data_ptr(), ws.data_ptr(),
                                    ws.numel(), _stream(stream)))
     return hm, jac
+
+
+class DecodeGraph:
+    """One decode step (smallkv_select + one smallkv_attend per LLM layer)
+    captured in a CUDA graph on static buffers.
+
+    layer_plan: sequence of (llm_layer, cache_layer, q_tensor, out_tensor).
+    With timing=True, external CUDA events are captured between the calls
+    (after select and after every attend) so kernel durations can be read
+    back after a replay with `segment_ms()`.
+    """
+
+    def __init__(self, step: DecodeStep, slm_q: torch.Tensor, layer_plan, timing: bool = False):
+        self.step = step
+        self.slm_q = slm_q
+        self.plan = list(layer_plan)
+        self.timing = timing
+        self.events = []
+        self.stream = torch.cuda.Stream()
+        # eager warm-up on the capture stream (sets kernel attributes, checks args)
+        with torch.cuda.stream(self.stream):
+            self._calls(record=False)
+        self.stream.synchronize()
+        if timing:
+            self.events = [torch.cuda.Event(enable_timing=True, external=True)
+                           for _ in range(len(self.plan) + 2)]
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.stream):
+            self._calls(record=timing)
+
+    def _calls(self, record: bool):
+        if record:
+            self.events[0].record()
+        self.step.select(self.slm_q)
+        if record:
+            self.events[1].record()
+        for i, (layer, slot, q, out) in enumerate(self.plan):
+            # every attend after the first is separated from select by another
+            # attend, so its prologue may overlap the previous kernel's tail
+            self.step.attend(layer, slot, q, out, overlap_prologue=i > 0)
+            if record:
+                self.events[2 + i].record()
+
+    def replay(self):
+        """Launch the graph on this object's stream (CUDAGraph.replay launches on
+        the current stream, so make it ours)."""
+        with torch.cuda.stream(self.stream):
+            self.graph.replay()
+
+    def segment_ms(self):
+        """(select_ms, [attend_ms per layer]) of the last replay (after sync)."""
+        ev = self.events
+        sel = ev[0].elapsed_time(ev[1])
+        att = [ev[1 + i].elapsed_time(ev[2 + i]) for i in range(len(self.plan))]
+        return sel, att
+
+    @property
+    def kernels_per_step(self) -> int:
+        # row_flags + slm_score + select, then one attend kernel per layer
+        return 3 + len(self.plan)

@@ -124,10 +124,11 @@ def run_gpu_step(p, step=None, layers=None):
     step = step or smallkv.from_problem(p)
     sel = step.select(p.slm_q)
     outs = []
-    for slot in (range(p.llm.num_layers) if layers is None else layers):
+    for i, slot in enumerate(range(p.llm.num_layers) if layers is None else layers):
         out = torch.empty(p.batch, p.cfg.llm.q_heads, p.cfg.llm.head_dim, dtype=torch.float32,
                           device=p.seq_lens.device)
-        step.attend(p.llm_layer_ids[slot], slot, p.llm_q[slot], out)
+        # later layers may overlap their prologue with the previous attend (PDL)
+        step.attend(p.llm_layer_ids[slot], slot, p.llm_q[slot], out, overlap_prologue=i > 0)
         outs.append(out)
     torch.cuda.synchronize()
     return step, sel, outs
