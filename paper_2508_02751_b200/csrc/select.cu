@@ -8,14 +8,25 @@
 //   critical = rank < K' (Eq. 6 TopK), marginal = K' <= rank < K'+M' (Top(P-K), R4).
 // Output: ascending compacted crit_idx / marg_idx, marg_w = a'_v, counts (K', M').
 //
-// Exact selection with a deterministic lower-index tie-break: the two rank
-// boundaries are found by a 4-pass MSB radix select (8-bit digits) over
-// order-preserving uint32 keys, with warp-aggregated shared-memory histograms
-// (match_any); ties at a boundary are resolved by index through per-warp
-// ballot prefix counts, then both lists are emitted in ascending order in one
-// pass.  Rows up to kSmemCap tokens are held in shared memory; longer rows are
-// re-read from global memory (they stay L2-resident across the passes).
+// Exact selection with a deterministic lower-index tie-break.  Each rank
+// boundary becomes a lexicographic threshold (T, I) on (key, index), where
+// key is an order-preserving uint32 of the logit (smaller key = larger score):
+// position v is selected iff key_v < T or (key_v == T and v <= I).
+//   Fast path: one pass builds a 256-bin histogram that is LINEAR in the logit
+//   value over [min, max] of the ranked positions (monotone, so bins are
+//   ordered like scores; per-warp private shared-memory histograms), a suffix
+//   scan finds each boundary's bin, one pass collects that bin's (key, index)
+//   pairs, and the boundary is the pair of exact rank among them (rank
+//   counting on <= kCandCap candidates).
+//   Fallback (a boundary bin holds more than kCandCap positions, e.g. massive
+//   ties): a 4-pass 8-bit MSB radix select finds T exactly and a ballot pass
+//   locates I.
+// Both lists are then emitted in ascending order by one counting and one
+// writing pass with per-warp ballot prefix sums.  Rows up to kSmemCap tokens
+// are held in shared memory; longer rows are re-read from global memory (they
+// stay L2-resident across the passes).  All reductions use a fixed order.
 #include <float.h>
+#include <math.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -23,19 +34,31 @@
 namespace skv {
 
 namespace {
-constexpr int kThreads = 512;
+constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+constexpr int kBins = 256;
+constexpr int kCandCap = 1024;
 constexpr int kSmemCap = 40960;  // tokens held in shared memory (160 KB)
 
 __device__ __forceinline__ int iclamp(int x, int lo, int hi) { return x < lo ? lo : (x > hi ? hi : x); }
 
+// deterministic combine of per-thread (max, Σexp) pairs
+__device__ __forceinline__ void lse_combine(float& m, float& s, float m2, float s2) {
+  const float mm = fmaxf(m, m2);
+  s = s * expf(m - mm) + s2 * expf(m2 - mm);
+  m = mm;
+}
+
 template <bool kInSmem>
 __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) {
-  extern __shared__ uint32_t keys[];
-  __shared__ uint32_t hist[2][256];
-  __shared__ float red[kWarps];
-  __shared__ int wcnt[kWarps][4];
-  __shared__ int woff[kWarps][4];
+  extern __shared__ float vals[];
+  __shared__ uint32_t hist[kWarps][kBins];
+  __shared__ unsigned long long cand[2][kCandCap];
+  __shared__ float red[4][kWarps];
+  __shared__ int wcnt[kWarps][2];
+  __shared__ int s_bin[2], s_above[2], s_nc[2], s_fallback;
+  __shared__ uint32_t s_tk[2];
+  __shared__ int s_ti[2];
   __shared__ uint32_t s_pref[2];
   __shared__ int s_rem[2];
 
@@ -51,81 +74,192 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
   const int Mc = min(iclamp(p.k_marg[b], 0, n - Rc - Kc), p.max_marg);
   const int N = n - Rc;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t lt = lanemask_lt();
+  auto VAL = [&](int i) -> float { return kInSmem ? vals[i] : row[i]; };
 
-  // ---- 1. row max (and stage the row in shared memory)
-  float mx = -FLT_MAX;
+  // ---- pass 1: (max, Σexp) over [0, n) (online, per thread), range of [0, N)
+  float mt = -FLT_MAX, st = 0.f, lo = FLT_MAX, hi = -FLT_MAX;
   for (int i = tid; i < n; i += kThreads) {
     const float x = row[i];
-    if (kInSmem) keys[i] = __float_as_uint(x);
-    mx = fmaxf(mx, x);
+    if (kInSmem) vals[i] = x;
+    if (x > mt) {
+      st = st * expf(mt - x) + 1.f;
+      mt = x;
+    } else {
+      st += expf(x - mt);
+    }
+    if (i < N) {
+      lo = fminf(lo, x);
+      hi = fmaxf(hi, x);
+    }
   }
-  mx = warp_max(mx);
-  if (lane == 0) red[warp] = mx;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lse_combine(mt, st, __shfl_xor_sync(0xffffffffu, mt, o), __shfl_xor_sync(0xffffffffu, st, o));
+    lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if (lane == 0) {
+    red[0][warp] = mt;
+    red[1][warp] = st;
+    red[2][warp] = lo;
+    red[3][warp] = hi;
+  }
   __syncthreads();
   if (warp == 0) {
-    float v = lane < kWarps ? red[lane] : -FLT_MAX;
-    v = warp_max(v);
-    if (lane == 0) red[0] = v;
+    float m2 = lane < kWarps ? red[0][lane] : -FLT_MAX;
+    float s2 = lane < kWarps ? red[1][lane] : 0.f;
+    float l2 = lane < kWarps ? red[2][lane] : FLT_MAX;
+    float h2 = lane < kWarps ? red[3][lane] : -FLT_MAX;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lse_combine(m2, s2, __shfl_xor_sync(0xffffffffu, m2, o), __shfl_xor_sync(0xffffffffu, s2, o));
+      l2 = fminf(l2, __shfl_xor_sync(0xffffffffu, l2, o));
+      h2 = fmaxf(h2, __shfl_xor_sync(0xffffffffu, h2, o));
+    }
+    if (lane == 0) {
+      red[0][0] = m2;
+      red[1][0] = s2;
+      red[2][0] = l2;
+      red[3][0] = h2;
+      p.lse[rb * 2] = m2;
+      p.lse[rb * 2 + 1] = m2 + logf(s2);
+      p.counts[rb * 2] = Kc;
+      p.counts[rb * 2 + 1] = Mc;
+    }
   }
   __syncthreads();
-  const float m = red[0];
-  __syncthreads();
-  // ---- 2. Σ exp(s - m) in a fixed order (deterministic)
-  float se = 0.f;
-  for (int i = tid; i < n; i += kThreads) {
-    const float x = kInSmem ? __uint_as_float(keys[i]) : row[i];
-    se += expf(x - m);
-  }
-  se = warp_sum(se);
-  if (lane == 0) red[warp] = se;
-  __syncthreads();
-  if (warp == 0) {
-    float v = lane < kWarps ? red[lane] : 0.f;
-    v = warp_sum(v);
-    if (lane == 0) red[0] = v;
-  }
-  __syncthreads();
-  const float lse = m + logf(red[0]);
-  if (tid == 0) {
-    p.lse[rb * 2] = m;
-    p.lse[rb * 2 + 1] = lse;
-    p.counts[rb * 2] = Kc;
-    p.counts[rb * 2 + 1] = Mc;
-  }
-  if (kInSmem) {
-    for (int i = tid; i < N; i += kThreads) keys[i] = desc_key(__uint_as_float(keys[i]));
-    __syncthreads();
-  }
-  auto KEY = [&](int i) -> uint32_t { return kInSmem ? keys[i] : desc_key(row[i]); };
-
-  // ---- 3. radix select of the rank boundaries rA = K', rB = K'+M'
+  const float lse = red[0][0] + logf(red[1][0]);
+  const float vlo = red[2][0], vhi = red[3][0];
   const int rA = Kc, rB = Kc + Mc;
-  uint32_t pref0 = 0, pref1 = 0;
-  int rem0 = rA, rem1 = rB;
-  const bool act0 = rA > 0, act1 = rB > 0;
-  if (act1) {
+  if (rB == 0) return;
+
+  // per-warp contiguous segments of [0, N) (index order = output order)
+  const int seg = ((N + kThreads - 1) / kThreads) * 32;
+  const int s0 = warp * seg, s1 = min(N, s0 + seg);
+
+  // ---- boundaries as lexicographic thresholds (T, I)
+  const float scale = 255.99f / (vhi - vlo);
+  const bool all_equal = !(vhi > vlo);
+  if (tid == 0) s_fallback = (!all_equal && !isfinite(scale)) ? 1 : 0;
+  __syncthreads();
+  if (all_equal) {
+    // every ranked score ties: the lowest indices win
+    if (tid < 2) {
+      const int rr = tid == 0 ? rA : rB;
+      s_tk[tid] = rr > 0 ? desc_key(vlo) : 0u;
+      s_ti[tid] = rr - 1;
+    }
+  } else if (!s_fallback) {
+    for (int i = tid; i < kWarps * kBins; i += kThreads) (&hist[0][0])[i] = 0u;
+    __syncthreads();
+    for (int base = s0; base < s1; base += 32) {
+      const int i = base + lane;
+      if (i < s1) {
+        const int bin = min(kBins - 1, static_cast<int>((VAL(i) - vlo) * scale));
+        atomicAdd(&hist[warp][bin], 1u);
+      }
+    }
+    __syncthreads();
+    if (warp < 2 && (warp == 0 ? rA > 0 : true)) {
+      // bins from the top: lane covers bins 255-8*lane .. 248-8*lane
+      const int rr = warp == 0 ? rA : rB;
+      int c[8], tot = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int bin = kBins - 1 - (lane * 8 + q);
+        int v = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) v += static_cast<int>(hist[w][bin]);
+        c[q] = v;
+        tot += v;
+      }
+      int incl = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int above = incl - tot;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (above < rr && rr <= above + c[q]) {
+          s_bin[warp] = kBins - 1 - (lane * 8 + q);
+          s_above[warp] = above;
+          s_nc[warp] = c[q];
+          if (c[q] > kCandCap) s_fallback = 1;
+        }
+        above += c[q];
+      }
+    }
+    __syncthreads();
+    if (!s_fallback) {
+      const int binA = rA > 0 ? s_bin[0] : -1, binB = s_bin[1];
+      const bool shared = binA == binB;
+      __shared__ int s_cnt[2];
+      if (tid < 2) s_cnt[tid] = 0;
+      __syncthreads();
+      for (int i = tid; i < N; i += kThreads) {
+        const float x = VAL(i);
+        const int bin = min(kBins - 1, static_cast<int>((x - vlo) * scale));
+        const unsigned long long kv =
+            (static_cast<unsigned long long>(desc_key(x)) << 32) | static_cast<uint32_t>(i);
+        if (bin == binA) cand[0][atomicAdd(&s_cnt[0], 1)] = kv;
+        if (bin == binB && !shared) cand[1][atomicAdd(&s_cnt[1], 1)] = kv;
+      }
+      __syncthreads();
+      // the pair of exact rank (rem - 1) among a bin's candidates (all distinct)
+      for (int t = 0; t < 2; ++t) {
+        const int rr = t == 0 ? rA : rB;
+        if (rr == 0) continue;
+        const int li = (t == 1 && shared) ? 0 : t;
+        const int nc = s_cnt[li];
+        const int want = rr - s_above[t] - 1;
+        for (int c = tid; c < nc; c += kThreads) {
+          const unsigned long long v = cand[li][c];
+          int rank = 0;
+          for (int d = 0; d < nc; ++d) rank += cand[li][d] < v ? 1 : 0;
+          if (rank == want) {
+            s_tk[t] = static_cast<uint32_t>(v >> 32);
+            s_ti[t] = static_cast<int>(v & 0xffffffffu);
+          }
+        }
+      }
+      if (tid == 0 && rA == 0) {
+        s_tk[0] = 0u;
+        s_ti[0] = -1;
+      }
+    }
+  }
+  __syncthreads();
+  if (s_fallback) {
+    // ---- 4-pass 8-bit MSB radix select of the exact keys, then the tie index
+    uint32_t(*rh)[256] = reinterpret_cast<uint32_t(*)[256]>(&hist[0][0]);
+    uint32_t pref0 = 0, pref1 = 0;
+    int rem0 = rA, rem1 = rB;
+    const bool act0 = rA > 0;
 #pragma unroll 1
     for (int pass = 0; pass < 4; ++pass) {
       const int shift = 24 - 8 * pass;
       const uint32_t hmask = pass == 0 ? 0u : (0xffffffffu << (shift + 8));
       const bool same = act0 && pref0 == pref1;
-      hist[tid >> 8][tid & 255] = 0;
+      for (int i = tid; i < 512; i += kThreads) rh[i >> 8][i & 255] = 0;
       __syncthreads();
       for (int base = warp * 32; base < N; base += kThreads) {
         const int i = base + lane;
         const bool valid = i < N;
-        const uint32_t k = valid ? KEY(i) : 0u;
+        const uint32_t k = valid ? desc_key(VAL(i)) : 0u;
         const uint32_t dig = (k >> shift) & 255u;
         const bool in0 = valid && act0 && (k & hmask) == pref0;
         const bool in1 = valid && !same && (k & hmask) == pref1;
         const uint32_t g0 = __match_any_sync(0xffffffffu, in0 ? dig : 0x100u);
-        if (in0 && lane == __ffs(g0) - 1) atomicAdd(&hist[0][dig], __popc(g0));
+        if (in0 && lane == __ffs(g0) - 1) atomicAdd(&rh[0][dig], __popc(g0));
         const uint32_t g1 = __match_any_sync(0xffffffffu, in1 ? dig : 0x100u);
-        if (in1 && lane == __ffs(g1) - 1) atomicAdd(&hist[1][dig], __popc(g1));
+        if (in1 && lane == __ffs(g1) - 1) atomicAdd(&rh[1][dig], __popc(g1));
       }
       __syncthreads();
-      if (warp < 2 && (warp == 0 ? act0 : act1)) {
-        const uint32_t* h = (warp == 1 && same) ? hist[0] : hist[warp];
+      if (warp < 2 && (warp == 0 ? act0 : true)) {
+        const uint32_t* h = (warp == 1 && same) ? rh[0] : rh[warp];
         const int rem = warp == 0 ? rem0 : rem1;
         int c[8], tot = 0;
 #pragma unroll
@@ -140,78 +274,100 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
           if (lane >= o) incl += y;
         }
         int before = incl - tot;
-        int found = -1, newrem = 0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          if (found < 0 && before < rem && rem <= before + c[q]) {
-            found = lane * 8 + q;
-            newrem = rem - before;
+          if (before < rem && rem <= before + c[q]) {
+            s_pref[warp] = (warp == 0 ? pref0 : pref1) | (static_cast<uint32_t>(lane * 8 + q) << shift);
+            s_rem[warp] = rem - before;
           }
           before += c[q];
         }
-        if (found >= 0) {
-          s_pref[warp] = (warp == 0 ? pref0 : pref1) | (static_cast<uint32_t>(found) << shift);
-          s_rem[warp] = newrem;
-        }
       }
       __syncthreads();
-      if (act0) { pref0 = s_pref[0]; rem0 = s_rem[0]; }
+      if (act0) {
+        pref0 = s_pref[0];
+        rem0 = s_rem[0];
+      }
       pref1 = s_pref[1];
       rem1 = s_rem[1];
       __syncthreads();
     }
-  }
-  // thresholds and how many elements equal to them are taken (by lowest index)
-  const uint32_t TA = act0 ? pref0 : 0u, TB = act1 ? pref1 : 0u;
-  const int takeA = act0 ? rem0 : 0, takeB = act1 ? rem1 : 0;
-
-  // ---- 4. per-warp segment counts
-  const int seg = ((N + kThreads - 1) / kThreads) * 32;
-  const int s0 = warp * seg, s1 = min(N, s0 + seg);
-  int ltA = 0, eqA = 0, ltB = 0, eqB = 0;
-  for (int base = s0; base < s1; base += 32) {
-    const int i = base + lane;
-    const bool valid = i < s1;
-    const uint32_t k = valid ? KEY(i) : 0xffffffffu;
-    ltA += __popc(__ballot_sync(0xffffffffu, valid && act0 && k < TA));
-    eqA += __popc(__ballot_sync(0xffffffffu, valid && act0 && k == TA));
-    ltB += __popc(__ballot_sync(0xffffffffu, valid && act1 && k < TB));
-    eqB += __popc(__ballot_sync(0xffffffffu, valid && act1 && k == TB));
-  }
-  if (lane == 0) {
-    wcnt[warp][0] = ltA; wcnt[warp][1] = eqA; wcnt[warp][2] = ltB; wcnt[warp][3] = eqB;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    int tA = 0, tB = 0, oc = 0, om = 0;
-    for (int w = 0; w < kWarps; ++w) {
-      woff[w][0] = tA; woff[w][1] = tB; woff[w][2] = oc; woff[w][3] = om;
-      const int cw = wcnt[w][0] + iclamp(takeA - tA, 0, wcnt[w][1]);
-      const int bw = wcnt[w][2] + iclamp(takeB - tB, 0, wcnt[w][3]);
-      tA += wcnt[w][1];
-      tB += wcnt[w][3];
-      oc += cw;
-      om += bw - cw;
+    // index of the take-th (1-based) position whose key equals T, per target
+    for (int t = 0; t < 2; ++t) {
+      const int rr = t == 0 ? rA : rB;
+      if (rr == 0) {
+        if (tid == 0) {
+          s_tk[0] = 0u;
+          s_ti[0] = -1;
+        }
+        continue;
+      }
+      const uint32_t T = t == 0 ? pref0 : pref1;
+      const int take = t == 0 ? rem0 : rem1;
+      int eq = 0;
+      for (int base = s0; base < s1; base += 32) {
+        const int i = base + lane;
+        eq += __popc(__ballot_sync(0xffffffffu, i < s1 && desc_key(VAL(i)) == T));
+      }
+      if (lane == 0) wcnt[warp][0] = eq;
+      __syncthreads();
+      int before = 0;
+      for (int w = 0; w < warp; ++w) before += wcnt[w][0];
+      if (before < take && take <= before + eq) {
+        for (int base = s0; base < s1; base += 32) {
+          const int i = base + lane;
+          const uint32_t bal = __ballot_sync(0xffffffffu, i < s1 && desc_key(VAL(i)) == T);
+          const int k = take - before;   // 1-based within this warp's remaining ties
+          if (k >= 1 && k <= __popc(bal)) {
+            if (lane == 0) {
+              uint32_t m = bal;
+              for (int q = 1; q < k; ++q) m &= m - 1;
+              s_tk[t] = T;
+              s_ti[t] = base + __ffs(m) - 1;
+            }
+            break;
+          }
+          before += __popc(bal);
+        }
+      }
+      __syncthreads();
     }
   }
   __syncthreads();
 
-  // ---- 5. emit ascending lists
-  int tieA = woff[warp][0], tieB = woff[warp][1], oc = woff[warp][2], om = woff[warp][3];
-  int32_t* crit = p.crit_idx + rb * p.max_crit;
-  int32_t* marg = p.marg_idx + rb * p.max_marg;
-  float* mw = p.marg_w + rb * p.max_marg;
-  const uint32_t lt = lanemask_lt();
+  // ---- emission: count per warp segment, scan, write ascending lists
+  const uint32_t TA = s_tk[0], TB = s_tk[1];
+  const int IA = s_ti[0], IB = s_ti[1];
+  int cc = 0, cb = 0;
   for (int base = s0; base < s1; base += 32) {
     const int i = base + lane;
     const bool valid = i < s1;
-    const uint32_t k = valid ? KEY(i) : 0xffffffffu;
-    const bool eA = valid && act0 && k == TA;
-    const bool eB = valid && act1 && k == TB;
-    const uint32_t bA = __ballot_sync(0xffffffffu, eA);
-    const uint32_t bB = __ballot_sync(0xffffffffu, eB);
-    const bool isC = valid && act0 && (k < TA || (eA && tieA + __popc(bA & lt) < takeA));
-    const bool inB = valid && act1 && (k < TB || (eB && tieB + __popc(bB & lt) < takeB));
+    const uint32_t k = valid ? desc_key(VAL(i)) : 0xffffffffu;
+    const bool isC = valid && (k < TA || (k == TA && i <= IA));
+    const bool inB = valid && (k < TB || (k == TB && i <= IB));
+    cc += __popc(__ballot_sync(0xffffffffu, isC));
+    cb += __popc(__ballot_sync(0xffffffffu, inB));
+  }
+  if (lane == 0) {
+    wcnt[warp][0] = cc;
+    wcnt[warp][1] = cb - cc;
+  }
+  __syncthreads();
+  int oc = 0, om = 0;
+  for (int w = 0; w < warp; ++w) {
+    oc += wcnt[w][0];
+    om += wcnt[w][1];
+  }
+  int32_t* crit = p.crit_idx + rb * p.max_crit;
+  int32_t* marg = p.marg_idx + rb * p.max_marg;
+  float* mw = p.marg_w + rb * p.max_marg;
+  for (int base = s0; base < s1; base += 32) {
+    const int i = base + lane;
+    const bool valid = i < s1;
+    const float x = valid ? VAL(i) : 0.f;
+    const uint32_t k = valid ? desc_key(x) : 0xffffffffu;
+    const bool isC = valid && (k < TA || (k == TA && i <= IA));
+    const bool inB = valid && (k < TB || (k == TB && i <= IB));
     const bool isM = inB && !isC;
     const uint32_t bc = __ballot_sync(0xffffffffu, isC);
     const uint32_t bm = __ballot_sync(0xffffffffu, isM);
@@ -219,10 +375,8 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
     if (isM) {
       const int o = om + __popc(bm & lt);
       marg[o] = i;
-      mw[o] = expf(key_to_float(k) - lse);
+      mw[o] = expf(x - lse);
     }
-    tieA += __popc(bA);
-    tieB += __popc(bB);
     oc += __popc(bc);
     om += __popc(bm);
   }
@@ -234,9 +388,8 @@ cudaError_t launch_select(const SelectParams& p, int32_t max_rows, int32_t max_s
   dim3 grid(max_rows, p.batch);
   if (max_seq_len <= kSmemCap) {
     const size_t sm = static_cast<size_t>(max_seq_len) * 4;
-    if (sm > 48 * 1024)
-      cudaFuncSetAttribute(select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(sm));
+    cudaFuncSetAttribute(select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sm));
     select_kernel<true><<<grid, kThreads, sm, s>>>(p);
   } else {
     select_kernel<false><<<grid, kThreads, 0, s>>>(p);

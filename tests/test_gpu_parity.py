@@ -231,3 +231,15 @@ def test_qwen7b_full_size_sampled():
                                      heads=sb)
         assert e <= parity.OUT_TOL
     print("qwen7b sampled", rep)
+
+
+def test_two_valued_logits_radix_fallback():
+    """Logits taking two values: > 1024 positions share the boundary bin of the
+    histogram path, forcing the radix fallback of K2 (ties by index)."""
+    cfg = _cfg(n=3000, B=2, budget=(500, 100, 700))
+    p = synth.make_problem(cfg, seed=15, page_size=16, seq_lens=[3000, 2500])
+    k = p.slm.k.clone()
+    k[..., 0::2, :] = k[0, 0, 0, 0]       # even rows of every page: one vector
+    k[..., 1::2, :] = k[0, 0, 0, 1]       # odd rows: another
+    p = dataclasses.replace(p, slm=dataclasses.replace(p.slm, k=k)).to("cuda")
+    _check(p)
