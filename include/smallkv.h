@@ -176,6 +176,27 @@ int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm,
                    int32_t* marg_idx, float* marg_w, int32_t* counts,
                    float* acc, void* ws, size_t ws_bytes, void* stream);
 
+/* Bytes of the gather plan of n_llm_layers layers (0 on invalid arguments). */
+size_t smallkv_plan_size(const smallkv_cache* llm, const smallkv_batch* batch,
+                         int32_t n_llm_layers);
+
+/*
+ * smallkv_plan — optional, once per decode step after smallkv_select: stages
+ * for every LLM layer, sequence and kv-group the first gather batch of
+ * smallkv_attend (per entry: row offset in the layer's pool, head mask,
+ * marginal weight) so each attend launch starts streaming after one read.
+ * Same arguments as smallkv_attend's selection inputs; plan is device memory
+ * of >= smallkv_plan_size bytes (16-byte aligned), fully rewritten.  The plan
+ * depends on the page tables, head map and selection of this step only.
+ * Errors: as smallkv_attend.
+ */
+int smallkv_plan(const smallkv_cache* llm, const smallkv_batch* batch,
+                 const int32_t* head_map, int32_t n_llm_layers,
+                 int32_t slm_heads_total, const smallkv_budgets* budgets,
+                 const int32_t* crit_idx, const int32_t* marg_idx,
+                 const float* marg_w, const int32_t* counts, void* plan,
+                 size_t plan_bytes, void* stream);
+
 /* Bytes of workspace smallkv_attend needs (0 on invalid arguments). */
 size_t smallkv_attend_workspace_size(const smallkv_cache* llm,
                                      const smallkv_batch* batch);
@@ -199,6 +220,8 @@ size_t smallkv_attend_workspace_size(const smallkv_cache* llm,
  *   n_llm_layers L (head_map has L*H entries).
  *   crit_idx, marg_idx, marg_w, counts: smallkv_select outputs (same batch
  *               and budgets; slm_heads_total = l*H_s rows).
+ *   plan        NULL, or the smallkv_plan buffer of this step (then the
+ *               kernel skips its own two rounds of list / page-table loads).
  *   out         device fp32 [B][H][d].
  *   flags       0 or SMALLKV_ATTEND_OVERLAP_PROLOGUE.  The kernel is always
  *               launched with programmatic dependent launch: it reads q and
@@ -221,8 +244,9 @@ int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
                    const int32_t* head_map, int32_t n_llm_layers,
                    int32_t slm_heads_total, const smallkv_budgets* budgets,
                    const int32_t* crit_idx, const int32_t* marg_idx,
-                   const float* marg_w, const int32_t* counts, float* out,
-                   int32_t flags, void* ws, size_t ws_bytes, void* stream);
+                   const float* marg_w, const int32_t* counts, const void* plan,
+                   float* out, int32_t flags, void* ws, size_t ws_bytes,
+                   void* stream);
 
 /*
  * smallkv_match_heads — prefill similarity matching (Eq. 2-3).

@@ -58,7 +58,7 @@ namespace {
 constexpr int kTile = 16;      // rows (tokens) per warp tile
 constexpr int kWarps = 4;
 constexpr int kThreads = kWarps * 32;
-constexpr int kBatch = 256;    // entries whose positions/pages/weights are staged at once
+constexpr int kBatch = 1024;   // entries whose positions/pages/weights are staged at once
 
 template <int D>
 constexpr int stages_for() { return 3; }
@@ -77,6 +77,137 @@ constexpr size_t smem_bytes() {
 // O rescale is skipped for almost every tile; exp2 arguments stay <= 8.
 constexpr float kRescaleSlack = 8.f;
 
+// Layout of one (layer, sequence, kv-group) virtual list:
+//   [ recent Rc | crit(r_0) | marg(r_0) | crit(r_1) | marg(r_1) | ... ]
+struct GroupLayout {
+  int T, nrows, Rc, n;
+  int rj[8], rK[8], rM[8];
+  uint32_t rhm[8];
+};
+constexpr int kHdrBytes = 256;
+static_assert(sizeof(GroupLayout) <= kHdrBytes && sizeof(GroupLayout) % 16 == 0, "plan header");
+
+// Plan record of one (layer, sequence, kv-group): header + for each cluster
+// rank the first kBatch staged entries (row offset, head mask, marginal weight).
+__host__ __device__ constexpr int64_t plan_record_bytes(int nc) {
+  return kHdrBytes + static_cast<int64_t>(nc) * kBatch * 12;
+}
+
+// All threads: distinct SLM rows of the group's heads (first occurrence order)
+// and the list sizes.  Two dependent rounds of loads (head map, counts).
+__device__ void build_layout(const AttendParams& p, int layer, int b, int g, GroupLayout& L) {
+  __shared__ int s_j[8], s_K[8], s_M[8];
+  const int G = p.heads / p.kv_heads;
+  const int tid = threadIdx.x;
+  if (tid < G) {
+    const int j = p.head_map[layer * p.heads + g * G + tid];
+    const int64_t rb = static_cast<int64_t>(j) * p.batch + b;
+    s_j[tid] = j;
+    s_K[tid] = p.counts[rb * 2];
+    s_M[tid] = p.counts[rb * 2 + 1];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const int n = p.seq_lens[b];
+    const int Rc = min(max(p.n_recent[b], 0), n);
+    int nr = 0, T = Rc;
+    for (int h = 0; h < G; ++h) {
+      int k = 0;
+      while (k < nr && L.rj[k] != s_j[h]) ++k;
+      if (k == nr) {
+        L.rj[nr] = s_j[h];
+        L.rK[nr] = s_K[h];
+        L.rM[nr] = s_M[h];
+        L.rhm[nr] = 0u;
+        T += s_K[h] + s_M[h];
+        ++nr;
+      }
+      L.rhm[k] |= 1u << h;
+    }
+    L.nrows = nr;
+    L.T = T;
+    L.Rc = Rc;
+    L.n = n;
+  }
+  __syncthreads();
+}
+
+// All threads: stage entries [e_b, e_b + E) of the group's virtual list:
+// row offset in the layer's pool (elements), head mask, marginal weight.
+// Two dependent rounds of loads (list values, page table).
+template <int D>
+__device__ void stage_entries(const AttendParams& p, const GroupLayout& L, int b, int g, int e_b,
+                              int E, uint32_t* soff, uint32_t* smk, float* sw) {
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int G = p.heads / p.kv_heads;
+  const uint32_t allc = (1u << G) - 1u;
+  for (int i = tid; i < E; i += nthr) {
+    int x = e_b + i, pos;
+    uint32_t mk;
+    float wt = 0.f;
+    if (x < L.Rc) {
+      pos = L.n - L.Rc + x;
+      mk = allc;
+    } else {
+      x -= L.Rc;
+      int k = 0;
+      while (k < L.nrows - 1 && x >= L.rK[k] + L.rM[k]) {
+        x -= L.rK[k] + L.rM[k];
+        ++k;
+      }
+      const int64_t rb = static_cast<int64_t>(L.rj[k]) * p.batch + b;
+      if (x < L.rK[k]) {
+        pos = __ldg(p.crit_idx + rb * p.max_crit + x);
+        mk = L.rhm[k];
+      } else {
+        pos = __ldg(p.marg_idx + rb * p.max_marg + (x - L.rK[k]));
+        wt = __ldg(p.marg_w + rb * p.max_marg + (x - L.rK[k]));
+        mk = L.rhm[k] << 8;
+      }
+    }
+    soff[i] = static_cast<uint32_t>(pos);
+    smk[i] = mk;
+    sw[i] = wt;
+  }
+  __syncthreads();
+  const int32_t* bt = p.block_table + static_cast<int64_t>(b) * p.max_blocks;
+  for (int i = tid; i < E; i += nthr) {
+    const int pos = static_cast<int>(soff[i]);
+    const int page = __ldg(bt + pos / p.page_size);
+    soff[i] = static_cast<uint32_t>(
+        ((static_cast<int64_t>(page) * p.kv_heads + g) * p.page_size + pos % p.page_size) * D);
+  }
+  __syncthreads();
+}
+
+// K3a — gather plan for every layer of the step (one launch after select):
+// CTA (c, g, layer*B + b) stages rank c's first batch of the group's list.
+template <int D>
+__global__ void __launch_bounds__(kThreads) plan_kernel(const AttendParams p) {
+  __shared__ GroupLayout L;
+  __shared__ uint32_t soff[kBatch], smk[kBatch];
+  __shared__ float sw[kBatch];
+  const int c = blockIdx.x, g = blockIdx.y;
+  const int layer = blockIdx.z / p.batch, b = blockIdx.z % p.batch;
+  const int NC = gridDim.x;
+  griddep_wait();
+  build_layout(p, layer, b, g, L);
+  const int e_lo = static_cast<int>((static_cast<int64_t>(L.T) * c) / NC);
+  const int e_hi = static_cast<int>((static_cast<int64_t>(L.T) * (c + 1)) / NC);
+  const int E = min(kBatch, e_hi - e_lo);
+  stage_entries<D>(p, L, b, g, e_lo, E, soff, smk, sw);
+  uint8_t* rec = p.plan + ((static_cast<int64_t>(layer) * p.batch + b) * p.kv_heads + g) *
+                              plan_record_bytes(NC);
+  if (c == 0 && threadIdx.x < sizeof(GroupLayout) / 4)
+    reinterpret_cast<int*>(rec)[threadIdx.x] = reinterpret_cast<const int*>(&L)[threadIdx.x];
+  uint32_t* poff = reinterpret_cast<uint32_t*>(rec + kHdrBytes) + static_cast<int64_t>(c) * kBatch * 3;
+  for (int i = threadIdx.x; i < E; i += kThreads) {
+    poff[i] = soff[i];
+    poff[kBatch + i] = smk[i];
+    reinterpret_cast<float*>(poff)[2 * kBatch + i] = sw[i];
+  }
+}
+
 template <int D>
 __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const AttendParams p) {
   constexpr int NSTAGE = stages_for<D>();
@@ -90,53 +221,34 @@ __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const AttendParams 
   uint32_t* smk = soff + kBatch;
   float* sw = reinterpret_cast<float*>(smk + kBatch);
   uint8_t* stages = reinterpret_cast<uint8_t*>(sw + kBatch);
-  __shared__ int s_j[8], s_K[8], s_M[8];
-  __shared__ int s_rj[8], s_rK[8], s_rM[8];
-  __shared__ uint32_t s_rhm[8];
-  __shared__ int s_nrows, s_T;
+  __shared__ __align__(16) GroupLayout L;
 
   const int c = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
   const int NC = gridDim.x;
   // Without the overlap flag nothing is read before the previous kernel on the
-  // stream has completed.  With it, the prologue below (selection outputs,
-  // page tables, K/V tiles) may run during that kernel's tail.
+  // stream has completed.  With it, the prologue below (plan / selection
+  // outputs, page tables, K/V tiles) may run during that kernel's tail.
   if (!p.overlap_prologue) griddep_wait();
   SKV_T(0);
-  const int n = p.seq_lens[b];
-  const int G = p.heads / p.kv_heads;
-  const int Rc = min(max(p.n_recent[b], 0), n);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t allc = (1u << G) - 1u;
-
-  // ---- group layout: distinct SLM rows of the group's heads and list sizes
-  if (tid < G) {
-    const int j = p.head_map[p.layer * p.heads + g * G + tid];
-    const int64_t rb = static_cast<int64_t>(j) * p.batch + b;
-    s_j[tid] = j;
-    s_K[tid] = p.counts[rb * 2];
-    s_M[tid] = p.counts[rb * 2 + 1];
+  const int G = p.heads / p.kv_heads;
+  const uint8_t* rec = p.plan ? p.plan + ((static_cast<int64_t>(p.layer) * p.batch + b) *
+                                              p.kv_heads + g) * plan_record_bytes(NC)
+                              : nullptr;
+  if (rec) {
+    // one round: header + this rank's pre-staged first batch (cp.async, 16 B)
+    for (int i = tid; i < static_cast<int>(sizeof(GroupLayout)) / 16; i += kThreads)
+      cp_async16(smem_u32(reinterpret_cast<uint8_t*>(&L) + 16 * i), rec + 16 * i, true);
+    const uint8_t* slot = rec + kHdrBytes + static_cast<int64_t>(c) * kBatch * 12;
+    for (int i = tid; i < kBatch * 12 / 16; i += kThreads)
+      cp_async16(smem_u32(smem + 16 * i), slot + 16 * i, true);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+  } else {
+    build_layout(p, p.layer, b, g, L);
   }
-  __syncthreads();
-  if (tid == 0) {
-    int nr = 0, T = Rc;
-    for (int h = 0; h < G; ++h) {
-      int k = 0;
-      while (k < nr && s_rj[k] != s_j[h]) ++k;
-      if (k == nr) {
-        s_rj[nr] = s_j[h];
-        s_rK[nr] = s_K[h];
-        s_rM[nr] = s_M[h];
-        s_rhm[nr] = 0u;
-        T += s_K[h] + s_M[h];
-        ++nr;
-      }
-      s_rhm[k] |= 1u << h;
-    }
-    s_nrows = nr;
-    s_T = T;
-  }
-  __syncthreads();
-  const int T = s_T, nrows = s_nrows;
+  const int T = L.T;
   const int e_lo = static_cast<int>((static_cast<int64_t>(T) * c) / NC);
   const int e_hi = static_cast<int>((static_cast<int64_t>(T) * (c + 1)) / NC);
   SKV_T(1);
@@ -145,7 +257,6 @@ __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const AttendParams 
   uint8_t* wst = stages + warp * NSTAGE * SB;
   const uint16_t* kpool = p.k + p.layer_offset;
   const uint16_t* vpool = p.v + p.layer_offset;
-  const int32_t* bt = p.block_table + static_cast<int64_t>(b) * p.max_blocks;
 
   uint32_t qa[D / 16][2];
   bool q_ready = false;
@@ -173,44 +284,8 @@ __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const AttendParams 
   int tbase = 0;   // tiles this warp consumed in earlier batches (mbarrier phases)
   for (int e_b = e_lo; e_b < e_hi; e_b += kBatch) {
     const int E = min(kBatch, e_hi - e_b);
-    // ---- stage positions + masks of this batch (one parallel round of list loads)
-    for (int i = tid; i < E; i += kThreads) {
-      int x = e_b + i, pos;
-      uint32_t mk;
-      float wt = 0.f;
-      if (x < Rc) {
-        pos = n - Rc + x;
-        mk = allc;
-      } else {
-        x -= Rc;
-        int k = 0;
-        while (k < nrows - 1 && x >= s_rK[k] + s_rM[k]) {
-          x -= s_rK[k] + s_rM[k];
-          ++k;
-        }
-        const int64_t rb = static_cast<int64_t>(s_rj[k]) * p.batch + b;
-        if (x < s_rK[k]) {
-          pos = __ldg(p.crit_idx + rb * p.max_crit + x);
-          mk = s_rhm[k];
-        } else {
-          pos = __ldg(p.marg_idx + rb * p.max_marg + (x - s_rK[k]));
-          wt = __ldg(p.marg_w + rb * p.max_marg + (x - s_rK[k]));
-          mk = s_rhm[k] << 8;
-        }
-      }
-      soff[i] = static_cast<uint32_t>(pos);
-      smk[i] = mk;
-      sw[i] = wt;
-    }
-    __syncthreads();
-    // ---- page-table entries (second parallel round) -> row offsets
-    for (int i = tid; i < E; i += kThreads) {
-      const int pos = static_cast<int>(soff[i]);
-      const int page = __ldg(bt + pos / p.page_size);
-      soff[i] = static_cast<uint32_t>(
-          ((static_cast<int64_t>(page) * p.kv_heads + g) * p.page_size + pos % p.page_size) * D);
-    }
-    __syncthreads();
+    // ---- stage this batch (pre-staged by the plan kernel for the first one)
+    if (!(rec && e_b == e_lo)) stage_entries<D>(p, L, b, g, e_b, E, soff, smk, sw);
     SKV_T(2);
 
     const int ntile = (E + kTile - 1) / kTile;
@@ -387,12 +462,13 @@ __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const AttendParams 
 #endif
   if (NC == 1) return;
 
-  // ---- fused K4: the group's CTAs form one thread-block cluster; rank 0
-  // merges every rank's state in rank order through distributed shared memory.
+  // ---- fused K4: the group's CTAs form one thread-block cluster; the ranks
+  // merge every rank's state in rank order through distributed shared memory.
   cluster_sync();
-  if (c == 0) {
+  {
+    // every rank merges its share of the (head, 4-column) items in rank order
     const uint32_t base = smem_u32(cst);
-    for (int it = tid; it < G * (D / 4); it += kThreads) {
+    for (int it = c * kThreads + tid; it < G * (D / 4); it += NC * kThreads) {
       const int h = it / (D / 4), c4 = (it % (D / 4)) * 4;
       float M = -INFINITY;
       for (int q = 0; q < NC; ++q) M = fmaxf(M, ld_dsmem_f32(base + h * 4, q));
@@ -412,7 +488,7 @@ __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const AttendParams 
           make_float4(oc.x * li + om.x, oc.y * li + om.y, oc.z * li + om.z, oc.w * li + om.w);
     }
   }
-  cluster_sync();   // keep every rank's shared memory alive until rank 0 has read it
+  cluster_sync();   // keep every rank's shared memory alive until all reads are done
   SKV_T(6);
 }
 }  // namespace
@@ -456,6 +532,28 @@ static cudaError_t launch_d(const AttendParams& p, cudaStream_t s) {
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, attend_kernel<D>, p);
+}
+
+int64_t plan_bytes(int32_t n_layers, int32_t batch, int32_t kv_heads, int32_t max_seq_len) {
+  return static_cast<int64_t>(n_layers) * batch * kv_heads *
+         plan_record_bytes(attend_ctas_per_group(max_seq_len));
+}
+
+cudaError_t launch_plan(const AttendParams& p, int32_t n_layers, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.max_chunks, p.kv_heads, n_layers * p.batch);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = p.head_dim == 64 ? cudaLaunchKernelEx(&cfg, plan_kernel<64>, p)
+                                   : cudaLaunchKernelEx(&cfg, plan_kernel<128>, p);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_attend(const AttendParams& p, cudaStream_t s) {

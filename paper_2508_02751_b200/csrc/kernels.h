@@ -68,8 +68,11 @@ struct AttendParams {
   int32_t max_chunks;         // CTAs (= cluster size) per (sequence, kv-group)
   float scale_log2;           // log2(e)/sqrt(d)
   int32_t overlap_prologue;   // SMALLKV_ATTEND_OVERLAP_PROLOGUE
+  uint8_t* plan;              // gather plan (smallkv_plan) or nullptr
 };
 cudaError_t launch_attend(const AttendParams& p, cudaStream_t s);
+cudaError_t launch_plan(const AttendParams& p, int32_t n_layers, cudaStream_t s);
+int64_t plan_bytes(int32_t n_layers, int32_t batch, int32_t kv_heads, int32_t max_seq_len);
 int32_t attend_ctas_per_group(int32_t max_seq_len);
 
 // ---------------------------------------------------------------- K0 match_heads

@@ -21,8 +21,9 @@
 //   Fallback (a boundary bin holds more than kCandCap positions, e.g. massive
 //   ties): a 4-pass 8-bit MSB radix select finds T exactly and a ballot pass
 //   locates I.
-// Both lists are then emitted in ascending order by one counting and one
-// writing pass with per-warp ballot prefix sums.  Rows up to kSmemCap tokens
+// Both lists are then emitted in ascending order by one writing pass with
+// per-warp ballot prefix sums (per-warp counts come from the per-warp
+// histograms and the boundary candidates; the fallback adds a counting pass).  Rows up to kSmemCap tokens
 // are held in shared memory; longer rows are re-read from global memory (they
 // stay L2-resident across the passes).  All reductions use a fixed order.
 #include <float.h>
@@ -45,7 +46,7 @@ __device__ __forceinline__ int iclamp(int x, int lo, int hi) { return x < lo ? l
 // deterministic combine of per-thread (max, Σexp) pairs
 __device__ __forceinline__ void lse_combine(float& m, float& s, float m2, float s2) {
   const float mm = fmaxf(m, m2);
-  s = s * expf(m - mm) + s2 * expf(m2 - mm);
+  s = s * __expf(m - mm) + s2 * __expf(m2 - mm);
   m = mm;
 }
 
@@ -56,6 +57,8 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
   __shared__ unsigned long long cand[2][kCandCap];
   __shared__ float red[4][kWarps];
   __shared__ int wcnt[kWarps][2];
+  __shared__ int wsel[kWarps][2];
+  __shared__ int s_have_counts;
   __shared__ int s_bin[2], s_above[2], s_nc[2], s_fallback;
   __shared__ uint32_t s_tk[2];
   __shared__ int s_ti[2];
@@ -83,10 +86,10 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
     const float x = row[i];
     if (kInSmem) vals[i] = x;
     if (x > mt) {
-      st = st * expf(mt - x) + 1.f;
+      st = st * __expf(mt - x) + 1.f;
       mt = x;
     } else {
-      st += expf(x - mt);
+      st += __expf(x - mt);
     }
     if (i < N) {
       lo = fminf(lo, x);
@@ -141,7 +144,10 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
   // ---- boundaries as lexicographic thresholds (T, I)
   const float scale = 255.99f / (vhi - vlo);
   const bool all_equal = !(vhi > vlo);
-  if (tid == 0) s_fallback = (!all_equal && !isfinite(scale)) ? 1 : 0;
+  if (tid == 0) {
+    s_fallback = (!all_equal && !isfinite(scale)) ? 1 : 0;
+    s_have_counts = 0;
+  }
   __syncthreads();
   if (all_equal) {
     // every ranked score ties: the lowest indices win
@@ -228,6 +234,39 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
       if (tid == 0 && rA == 0) {
         s_tk[0] = 0u;
         s_ti[0] = -1;
+      }
+      // per-warp output counts straight from the per-warp histograms plus the
+      // selected candidates of each warp's segment (no counting pass)
+      if (tid < 2 * kWarps) (&wsel[0][0])[tid] = 0;
+      __syncthreads();
+      for (int t = 0; t < 2; ++t) {
+        const int rr = t == 0 ? rA : rB;
+        if (rr == 0) continue;
+        const int li = (t == 1 && shared) ? 0 : t;
+        const unsigned long long thr =
+            (static_cast<unsigned long long>(s_tk[t]) << 32) | static_cast<uint32_t>(s_ti[t]);
+        for (int c = tid; c < s_cnt[li]; c += kThreads) {
+          const unsigned long long v = cand[li][c];
+          if (v <= thr) atomicAdd(&wsel[static_cast<int>(v & 0xffffffffu) / seg][t], 1);
+        }
+      }
+      {
+        int ab[2] = {0, 0};
+        for (int t = 0; t < 2; ++t) {
+          const int bt_ = (t == 0 && rA == 0) ? kBins : s_bin[t];
+          int a = 0;
+          for (int bin = bt_ + 1 + lane; bin < kBins; bin += 32) a += static_cast<int>(hist[warp][bin]);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+          ab[t] = a;
+        }
+        __syncthreads();
+        if (lane == 0) {
+          const int cw = ab[0] + wsel[warp][0];
+          wcnt[warp][0] = cw;
+          wcnt[warp][1] = ab[1] + wsel[warp][1] - cw;
+        }
+        if (tid == 0) s_have_counts = 1;
       }
     }
   }
@@ -338,21 +377,23 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
   // ---- emission: count per warp segment, scan, write ascending lists
   const uint32_t TA = s_tk[0], TB = s_tk[1];
   const int IA = s_ti[0], IB = s_ti[1];
-  int cc = 0, cb = 0;
-  for (int base = s0; base < s1; base += 32) {
-    const int i = base + lane;
-    const bool valid = i < s1;
-    const uint32_t k = valid ? desc_key(VAL(i)) : 0xffffffffu;
-    const bool isC = valid && (k < TA || (k == TA && i <= IA));
-    const bool inB = valid && (k < TB || (k == TB && i <= IB));
-    cc += __popc(__ballot_sync(0xffffffffu, isC));
-    cb += __popc(__ballot_sync(0xffffffffu, inB));
+  if (!s_have_counts) {
+    int cc = 0, cb = 0;
+    for (int base = s0; base < s1; base += 32) {
+      const int i = base + lane;
+      const bool valid = i < s1;
+      const uint32_t k = valid ? desc_key(VAL(i)) : 0xffffffffu;
+      const bool isC = valid && (k < TA || (k == TA && i <= IA));
+      const bool inB = valid && (k < TB || (k == TB && i <= IB));
+      cc += __popc(__ballot_sync(0xffffffffu, isC));
+      cb += __popc(__ballot_sync(0xffffffffu, inB));
+    }
+    if (lane == 0) {
+      wcnt[warp][0] = cc;
+      wcnt[warp][1] = cb - cc;
+    }
+    __syncthreads();
   }
-  if (lane == 0) {
-    wcnt[warp][0] = cc;
-    wcnt[warp][1] = cb - cc;
-  }
-  __syncthreads();
   int oc = 0, om = 0;
   for (int w = 0; w < warp; ++w) {
     oc += wcnt[w][0];

@@ -269,37 +269,33 @@ size_t smallkv_attend_workspace_size(const smallkv_cache* llm, const smallkv_bat
   return attend_ws_layout(llm, batch).total;
 }
 
-int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
-                   const smallkv_cache* llm, const smallkv_batch* batch, const int32_t* head_map,
-                   int32_t n_llm_layers, int32_t slm_heads_total, const smallkv_budgets* budgets,
-                   const int32_t* crit_idx, const int32_t* marg_idx, const float* marg_w,
-                   const int32_t* counts, float* out, int32_t flags, void* ws, size_t ws_bytes,
-                   void* stream) {
+size_t smallkv_plan_size(const smallkv_cache* llm, const smallkv_batch* batch,
+                         int32_t n_llm_layers) {
+  if (!llm || !batch || batch->batch < 1 || batch->max_seq_len < 1 || n_llm_layers < 1) return 0;
+  return static_cast<size_t>(skv::plan_bytes(n_llm_layers, batch->batch, llm->num_kv_heads,
+                                             batch->max_seq_len));
+}
+
+namespace {
+// shared argument checks + parameter block of smallkv_plan / smallkv_attend
+int fill_attend_params(skv::AttendParams& ap, const smallkv_cache* llm, const smallkv_batch* batch,
+                       const int32_t* head_map, int32_t n_llm_layers, int32_t slm_heads_total,
+                       const smallkv_budgets* budgets, const int32_t* crit_idx,
+                       const int32_t* marg_idx, const float* marg_w, const int32_t* counts) {
   int rc;
   if ((rc = check_cache(llm, true, "llm")) != SMALLKV_OK) return rc;
   if ((rc = check_batch(batch, llm)) != SMALLKV_OK) return rc;
   if ((rc = check_budgets(budgets)) != SMALLKV_OK) return rc;
-  if (!q || !head_map || !crit_idx || !marg_idx || !marg_w || !counts || !out)
-    return fail(SMALLKV_ERR_NULL, "smallkv_attend: NULL input/output pointer");
-  if (n_llm_layers < 1 || llm_layer < 0 || llm_layer >= n_llm_layers)
-    return fail(SMALLKV_ERR_SHAPE, "llm_layer %d outside [0,%d)", llm_layer, n_llm_layers);
-  if (cache_layer < 0 || cache_layer >= llm->num_layers)
-    return fail(SMALLKV_ERR_SHAPE, "cache_layer %d outside [0,%d)", cache_layer,
-                llm->num_layers);
+  if (!head_map || !crit_idx || !marg_idx || !marg_w || !counts)
+    return fail(SMALLKV_ERR_NULL, "NULL selection / head-map pointer");
+  if (n_llm_layers < 1) return fail(SMALLKV_ERR_SHAPE, "n_llm_layers must be >= 1");
   if (slm_heads_total < 1) return fail(SMALLKV_ERR_SHAPE, "slm_heads_total must be >= 1");
-  if (flags & ~SMALLKV_ATTEND_OVERLAP_PROLOGUE)
-    return fail(SMALLKV_ERR_SHAPE, "unknown smallkv_attend flags 0x%x", flags);
   const int G = llm->num_q_heads / llm->num_kv_heads;
   if (G > 8) return fail(SMALLKV_ERR_SHAPE, "LLM GQA group %d > 8 not supported", G);
-  if (!aligned(q, 4) || !aligned(out, 4))
-    return fail(SMALLKV_ERR_ALIGN, "q/out must be 4-byte aligned");
-  const AttendWs L = attend_ws_layout(llm, batch);
-  if (!ws || ws_bytes < L.total)
-    return fail(SMALLKV_ERR_WORKSPACE, "attend workspace %zu < %zu bytes", ws_bytes, L.total);
-  if ((rc = check_device()) != SMALLKV_OK) return rc;
-
-  skv::AttendParams ap;
-  ap.q = q;
+  if (static_cast<int64_t>(llm->num_pages) * llm->num_kv_heads * llm->page_size * llm->head_dim >=
+      (int64_t(1) << 32))
+    return fail(SMALLKV_ERR_SHAPE, "one layer of the LLM pool must have < 2^32 elements");
+  ap = skv::AttendParams{};
   ap.k = llm->k;
   ap.v = llm->v;
   ap.block_table = llm->block_table;
@@ -310,23 +306,74 @@ int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
   ap.marg_idx = marg_idx;
   ap.marg_w = marg_w;
   ap.counts = counts;
-  ap.out = out;
   ap.num_pages = llm->num_pages;
-  ap.layer_offset = static_cast<int64_t>(cache_layer) * llm->num_pages * llm->num_kv_heads *
-                    llm->page_size * llm->head_dim;
   ap.max_blocks = llm->max_blocks;
   ap.page_size = llm->page_size;
   ap.heads = llm->num_q_heads;
   ap.kv_heads = llm->num_kv_heads;
   ap.head_dim = llm->head_dim;
   ap.batch = batch->batch;
-  ap.layer = llm_layer;
   ap.row_stride = batch->max_seq_len;
   ap.max_crit = budgets->max_crit;
   ap.max_marg = budgets->max_marg;
-  ap.max_chunks = L.ctas;
+  ap.max_chunks = skv::attend_ctas_per_group(batch->max_seq_len);
   ap.scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(llm->head_dim));
+  return SMALLKV_OK;
+}
+}  // namespace
+
+int smallkv_plan(const smallkv_cache* llm, const smallkv_batch* batch, const int32_t* head_map,
+                 int32_t n_llm_layers, int32_t slm_heads_total, const smallkv_budgets* budgets,
+                 const int32_t* crit_idx, const int32_t* marg_idx, const float* marg_w,
+                 const int32_t* counts, void* plan, size_t plan_bytes, void* stream) {
+  skv::AttendParams ap;
+  int rc = fill_attend_params(ap, llm, batch, head_map, n_llm_layers, slm_heads_total, budgets,
+                              crit_idx, marg_idx, marg_w, counts);
+  if (rc != SMALLKV_OK) return rc;
+  const size_t need = smallkv_plan_size(llm, batch, n_llm_layers);
+  if (!plan || plan_bytes < need)
+    return fail(SMALLKV_ERR_WORKSPACE, "plan buffer %zu < %zu bytes", plan_bytes, need);
+  if (!aligned(plan, 16)) return fail(SMALLKV_ERR_ALIGN, "plan must be 16-byte aligned");
+  if (static_cast<int64_t>(n_llm_layers) * batch->batch > 65535)
+    return fail(SMALLKV_ERR_SHAPE, "L*B > 65535");
+  if ((rc = check_device()) != SMALLKV_OK) return rc;
+  ap.plan = static_cast<uint8_t*>(plan);
+  cudaError_t e = skv::launch_plan(ap, n_llm_layers, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "plan launch");
+  return SMALLKV_OK;
+}
+
+int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
+                   const smallkv_cache* llm, const smallkv_batch* batch, const int32_t* head_map,
+                   int32_t n_llm_layers, int32_t slm_heads_total, const smallkv_budgets* budgets,
+                   const int32_t* crit_idx, const int32_t* marg_idx, const float* marg_w,
+                   const int32_t* counts, const void* plan, float* out, int32_t flags, void* ws,
+                   size_t ws_bytes, void* stream) {
+  skv::AttendParams ap;
+  int rc = fill_attend_params(ap, llm, batch, head_map, n_llm_layers, slm_heads_total, budgets,
+                              crit_idx, marg_idx, marg_w, counts);
+  if (rc != SMALLKV_OK) return rc;
+  if (!q || !out) return fail(SMALLKV_ERR_NULL, "smallkv_attend: NULL q/out");
+  if (llm_layer < 0 || llm_layer >= n_llm_layers)
+    return fail(SMALLKV_ERR_SHAPE, "llm_layer %d outside [0,%d)", llm_layer, n_llm_layers);
+  if (cache_layer < 0 || cache_layer >= llm->num_layers)
+    return fail(SMALLKV_ERR_SHAPE, "cache_layer %d outside [0,%d)", cache_layer,
+                llm->num_layers);
+  if (flags & ~SMALLKV_ATTEND_OVERLAP_PROLOGUE)
+    return fail(SMALLKV_ERR_SHAPE, "unknown smallkv_attend flags 0x%x", flags);
+  if (!aligned(q, 4) || !aligned(out, 16) || (plan && !aligned(plan, 16)))
+    return fail(SMALLKV_ERR_ALIGN, "q must be 4-byte, out and plan 16-byte aligned");
+  const AttendWs L = attend_ws_layout(llm, batch);
+  if (!ws || ws_bytes < L.total)
+    return fail(SMALLKV_ERR_WORKSPACE, "attend workspace %zu < %zu bytes", ws_bytes, L.total);
+  if ((rc = check_device()) != SMALLKV_OK) return rc;
+  ap.q = q;
+  ap.out = out;
+  ap.layer = llm_layer;
+  ap.layer_offset = static_cast<int64_t>(cache_layer) * llm->num_pages * llm->num_kv_heads *
+                    llm->page_size * llm->head_dim;
   ap.overlap_prologue = (flags & SMALLKV_ATTEND_OVERLAP_PROLOGUE) ? 1 : 0;
+  ap.plan = const_cast<uint8_t*>(static_cast<const uint8_t*>(plan));
   cudaError_t e = skv::launch_attend(ap, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "attend launch");
   return SMALLKV_OK;

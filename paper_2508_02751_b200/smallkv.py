@@ -28,8 +28,8 @@ STATUS = {0: "OK", 1: "ERR_NULL", 2: "ERR_SHAPE", 3: "ERR_ALIGN", 4: "ERR_WORKSP
 
 # exported symbols, in the order include/smallkv.h declares them
 EXPORTS = ("smallkv_last_error", "smallkv_version", "smallkv_budget_from_tau",
-           "smallkv_select_workspace_size", "smallkv_select", "smallkv_attend_workspace_size",
-           "smallkv_attend", "smallkv_match_heads_workspace_size", "smallkv_match_heads",
+           "smallkv_select_workspace_size", "smallkv_select", "smallkv_plan_size", "smallkv_plan",
+           "smallkv_attend_workspace_size", "smallkv_attend", "smallkv_match_heads_workspace_size", "smallkv_match_heads",
            "smallkv_workspace_init")
 
 
@@ -78,8 +78,11 @@ def load(path: Optional[str] = None):
         lib.smallkv_select.argtypes = [P, P, P, P, i32, P, P, P, P, P, P, P, P, P, sz, P]
         lib.smallkv_attend_workspace_size.argtypes = [P, P]
         lib.smallkv_attend_workspace_size.restype = sz
-        lib.smallkv_attend.argtypes = [i32, i32, P, P, P, P, i32, i32, P, P, P, P, P, P, i32, P,
-                                       sz, P]
+        lib.smallkv_attend.argtypes = [i32, i32, P, P, P, P, i32, i32, P, P, P, P, P, P, P, i32,
+                                       P, sz, P]
+        lib.smallkv_plan_size.argtypes = [P, P, i32]
+        lib.smallkv_plan_size.restype = sz
+        lib.smallkv_plan.argtypes = [P, P, P, i32, i32, P, P, P, P, P, P, sz, P]
         lib.smallkv_match_heads_workspace_size.argtypes = [i32, i32]
         lib.smallkv_match_heads_workspace_size.restype = sz
         lib.smallkv_match_heads.argtypes = [P, i32, P, i32, i32, i32, P, P, P, sz, P]
@@ -164,7 +167,7 @@ class DecodeStep:
     def __init__(self, *, slm_k, slm_block_table, slm_q_heads: int, llm_k, llm_v,
                  llm_block_table, llm_q_heads: int, llm_layers: int, seq_lens: torch.Tensor,
                  max_seq_len: int, head_map: torch.Tensor, k_crit, n_recent, k_marg,
-                 max_crit: int, max_marg: int):
+                 max_crit: int, max_marg: int, use_plan: bool = True):
         self.lib = load()
         dev = seq_lens.device
         self._keep = (slm_k, slm_block_table, llm_k, llm_v, llm_block_table, seq_lens, head_map,
@@ -195,8 +198,13 @@ class DecodeStep:
             raise SmallKVError("workspace_size", 2, "invalid dimensions")
         self.ws_select = torch.zeros(ws_s, dtype=torch.uint8, device=dev)
         self.ws_attend = torch.zeros(ws_a, dtype=torch.uint8, device=dev)
+        plan_b = self.lib.smallkv_plan_size(ctypes.byref(self.llm), ctypes.byref(self.batch),
+                                            llm_layers)
+        self.plan_buf = torch.empty(max(plan_b, 16), dtype=torch.uint8, device=dev) if use_plan else None
+        self.planned = False
 
     def select(self, slm_q: torch.Tensor, stream=None):
+        """smallkv_select, then (by default) smallkv_plan for every layer."""
         assert slm_q.dtype == torch.bfloat16 and slm_q.is_contiguous()
         o = self.out
         rc = self.lib.smallkv_select(
@@ -206,6 +214,15 @@ class DecodeStep:
             o.marg_w.data_ptr(), o.counts.data_ptr(), None, self.ws_select.data_ptr(),
             self.ws_select.numel(), _stream(stream))
         _check("smallkv_select", rc)
+        self.planned = False
+        if self.plan_buf is not None:
+            rc = self.lib.smallkv_plan(
+                ctypes.byref(self.llm), ctypes.byref(self.batch), self.head_map.data_ptr(),
+                self.llm_layers, self.n_slm, ctypes.byref(self.budgets), o.crit.data_ptr(),
+                o.marg.data_ptr(), o.marg_w.data_ptr(), o.counts.data_ptr(),
+                self.plan_buf.data_ptr(), self.plan_buf.numel(), _stream(stream))
+            _check("smallkv_plan", rc)
+            self.planned = True
         return o
 
     def attend(self, llm_layer: int, cache_layer: int, q: torch.Tensor, out: torch.Tensor,
@@ -217,14 +234,15 @@ class DecodeStep:
             int(llm_layer), int(cache_layer), q.data_ptr(), ctypes.byref(self.llm),
             ctypes.byref(self.batch), self.head_map.data_ptr(), self.llm_layers, self.n_slm,
             ctypes.byref(self.budgets), o.crit.data_ptr(), o.marg.data_ptr(),
-            o.marg_w.data_ptr(), o.counts.data_ptr(), out.data_ptr(),
+            o.marg_w.data_ptr(), o.counts.data_ptr(),
+            self.plan_buf.data_ptr() if self.planned else None, out.data_ptr(),
             ATTEND_OVERLAP_PROLOGUE if overlap_prologue else 0,
             self.ws_attend.data_ptr(), self.ws_attend.numel(), _stream(stream))
         _check("smallkv_attend", rc)
         return out
 
 
-def from_problem(p) -> DecodeStep:
+def from_problem(p, use_plan: bool = True) -> DecodeStep:
     """DecodeStep for a smallkv_synth.Problem already on the GPU."""
     return DecodeStep(slm_k=p.slm.k, slm_block_table=p.slm.block_table,
                       slm_q_heads=p.cfg.slm.q_heads, llm_k=p.llm.k, llm_v=p.llm.v,
@@ -232,7 +250,7 @@ def from_problem(p) -> DecodeStep:
                       llm_layers=p.cfg.llm.layers, seq_lens=p.seq_lens,
                       max_seq_len=p.max_seq_len, head_map=p.head_map, k_crit=p.k_crit,
                       n_recent=p.n_recent, k_marg=p.k_marg, max_crit=p.max_crit,
-                      max_marg=p.max_marg)
+                      max_marg=p.max_marg, use_plan=use_plan)
 
 
 def match_heads(llm_F: torch.Tensor, slm_F: torch.Tensor, k_match: int, stream=None):
@@ -310,5 +328,5 @@ class DecodeGraph:
 
     @property
     def kernels_per_step(self) -> int:
-        # row_flags + slm_score + select, then one attend kernel per layer
-        return 3 + len(self.plan)
+        # row_flags + slm_score + select (+ plan), then one attend kernel per layer
+        return 3 + (1 if self.step.plan_buf is not None else 0) + len(self.plan)

@@ -63,7 +63,7 @@ def test_validation_errors_before_launch(lib):
     b = smallkv.CBatch(0, 1, 16)
     assert lib.smallkv_select_workspace_size(ctypes.byref(c), ctypes.byref(b), 4) > 0
     rc = lib.smallkv_attend(0, 0, None, ctypes.byref(c), ctypes.byref(b), None, 1, 2, None,
-                            None, None, None, None, None, 0, None, 0, None)
+                            None, None, None, None, None, None, 0, None, 0, None)
     assert rc == 1  # ERR_NULL
     assert b"NULL" in lib.smallkv_last_error()
     bad = smallkv.CCache(16, 16, 16, 1, 1, 64, 1, 4, 2, 96)  # head_dim 96
