@@ -21,21 +21,23 @@ struct SlmScoreParams {
   int32_t box_rows;           // TMA box rows = min(page_size, 64)
   uint32_t swz;               // 7 = 128B swizzle, 0 = none
   float scale;                // 1/sqrt(d)
+  int32_t layer_begin, layer_end;   // SLM layers scored by this launch
 };
 cudaError_t launch_slm_score(const SlmScoreParams& p, const CUtensorMap& map, int max_seq_len,
                              cudaStream_t s);
 
 // row flags + compact list of the head map's image
 cudaError_t launch_row_flags(const int32_t* head_map, int32_t n_llm_heads, int32_t n_slm_heads,
-                             uint8_t* row_needed, int32_t* rows, int32_t* n_rows,
-                             cudaStream_t s);
+                             int32_t heads_per_layer, uint8_t* row_needed, int32_t* rows,
+                             int32_t* n_rows, int32_t* layer_off, cudaStream_t s);
 
 // ---------------------------------------------------------------- K2 select
 struct SelectParams {
   const float* logits;        // [l*H_s][B][row_stride]
   const int32_t* seq_lens;
-  const int32_t* rows;        // compact image(f)
-  const int32_t* n_rows;      // device count
+  const int32_t* rows;        // compact image(f), ascending
+  const int32_t* layer_off;   // [l+1] rows of SLM layers < l start at layer_off[l]
+  int32_t layer_begin, layer_end;   // SLM layers whose rows this launch selects
   const int32_t *k_crit, *n_recent, *k_marg;
   float* lse;                 // [l*H_s][B][2]
   int32_t* crit_idx;          // [l*H_s][B][max_crit]
@@ -45,7 +47,7 @@ struct SelectParams {
   int32_t batch, row_stride, max_crit, max_marg;
 };
 cudaError_t launch_select(const SelectParams& p, int32_t max_rows, int32_t max_seq_len,
-                          cudaStream_t s);
+                          bool overlap_previous, cudaStream_t s);
 
 // ---------------------------------------------------------------- K3 gather_attend (+K4)
 struct AttendParams {

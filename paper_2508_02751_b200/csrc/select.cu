@@ -65,8 +65,8 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
   __shared__ uint32_t s_pref[2];
   __shared__ int s_rem[2];
 
-  const int r = blockIdx.x;
-  if (r >= *p.n_rows) return;
+  const int r = p.layer_off[p.layer_begin] + static_cast<int>(blockIdx.x);
+  if (r >= p.layer_off[p.layer_end]) return;
   const int j = p.rows[r];
   const int b = blockIdx.y;
   const int n = p.seq_lens[b];
@@ -424,17 +424,31 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
 }
 }  // namespace
 
+// overlap_previous: launch with programmatic dependent launch so this grid may
+// run alongside the immediately preceding kernel (the next chunk's K1).  The
+// caller guarantees that this grid's inputs were complete before that kernel
+// started (they come from an earlier launch on the stream).
 cudaError_t launch_select(const SelectParams& p, int32_t max_rows, int32_t max_seq_len,
-                          cudaStream_t s) {
-  dim3 grid(max_rows, p.batch);
+                          bool overlap_previous, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(max_rows, p.batch);
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = overlap_previous ? 1 : 0;
+  cudaError_t e;
   if (max_seq_len <= kSmemCap) {
-    const size_t sm = static_cast<size_t>(max_seq_len) * 4;
+    cfg.dynamicSmemBytes = static_cast<size_t>(max_seq_len) * 4;
     cudaFuncSetAttribute(select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(sm));
-    select_kernel<true><<<grid, kThreads, sm, s>>>(p);
+                         static_cast<int>(cfg.dynamicSmemBytes));
+    e = cudaLaunchKernelEx(&cfg, select_kernel<true>, p);
   } else {
-    select_kernel<false><<<grid, kThreads, 0, s>>>(p);
+    e = cudaLaunchKernelEx(&cfg, select_kernel<false>, p);
   }
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -46,7 +46,10 @@ slm_score_kernel(const __grid_constant__ CUtensorMap map, const SlmScoreParams p
   uint64_t* empty = full + NSTAGE;
 
   const int kvh = blockIdx.y;
-  const int layer = blockIdx.z / p.batch, b = blockIdx.z % p.batch;
+  const int layer = p.layer_begin + static_cast<int>(blockIdx.z) / p.batch;
+  const int b = blockIdx.z % p.batch;
+  // the select kernel of the previous layer chunk may run alongside (PDL)
+  griddep_launch_dependents();
   const int G = p.heads / p.kv_heads;
   const int n = p.seq_lens[b];
   const int t_begin = blockIdx.x * p.chunk_tokens;
@@ -153,8 +156,9 @@ slm_score_kernel(const __grid_constant__ CUtensorMap map, const SlmScoreParams p
 
 // One CTA: flags of the head map's image and its compact, ascending list.
 __global__ void row_flags_kernel(const int32_t* __restrict__ head_map, int32_t n_llm,
-                                 int32_t n_slm, uint8_t* __restrict__ needed,
-                                 int32_t* __restrict__ rows, int32_t* __restrict__ n_rows) {
+                                 int32_t n_slm, int32_t heads_per_layer,
+                                 uint8_t* __restrict__ needed, int32_t* __restrict__ rows,
+                                 int32_t* __restrict__ n_rows, int32_t* __restrict__ layer_off) {
   extern __shared__ uint8_t flags[];
   for (int i = threadIdx.x; i < n_slm; i += blockDim.x) flags[i] = 0;
   __syncthreads();
@@ -175,20 +179,29 @@ __global__ void row_flags_kernel(const int32_t* __restrict__ head_map, int32_t n
     }
     if (threadIdx.x == 0) *n_rows = base;
   }
+  // layer_off[l] = number of image rows with flat head < l * heads_per_layer
+  const int n_layers = n_slm / heads_per_layer;
+  for (int l = threadIdx.x; l <= n_layers; l += blockDim.x) {
+    int cnt = 0;
+    for (int i = 0; i < l * heads_per_layer; ++i) cnt += flags[i];
+    layer_off[l] = cnt;
+  }
 }
 }  // namespace
 
 cudaError_t launch_row_flags(const int32_t* head_map, int32_t n_llm_heads, int32_t n_slm_heads,
-                             uint8_t* row_needed, int32_t* rows, int32_t* n_rows,
-                             cudaStream_t s) {
-  row_flags_kernel<<<1, 1024, n_slm_heads, s>>>(head_map, n_llm_heads, n_slm_heads, row_needed,
-                                               rows, n_rows);
+                             int32_t heads_per_layer, uint8_t* row_needed, int32_t* rows,
+                             int32_t* n_rows, int32_t* layer_off, cudaStream_t s) {
+  row_flags_kernel<<<1, 1024, n_slm_heads, s>>>(head_map, n_llm_heads, n_slm_heads,
+                                               heads_per_layer, row_needed, rows, n_rows,
+                                               layer_off);
   return cudaGetLastError();
 }
 
 cudaError_t launch_slm_score(const SlmScoreParams& p, const CUtensorMap& map, int max_seq_len,
                              cudaStream_t s) {
-  dim3 grid((max_seq_len + p.chunk_tokens - 1) / p.chunk_tokens, p.kv_heads, p.layers * p.batch);
+  dim3 grid((max_seq_len + p.chunk_tokens - 1) / p.chunk_tokens, p.kv_heads,
+            (p.layer_end - p.layer_begin) * p.batch);
   if (p.head_dim == 64) {
     constexpr int sm = smem_bytes<64>();
     cudaFuncSetAttribute(slm_score_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);

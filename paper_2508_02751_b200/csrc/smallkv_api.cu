@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 
@@ -107,14 +108,15 @@ int check_budgets(const smallkv_budgets* bu) {
 }
 
 struct SelectWs {
-  size_t flags, rows, nrows, total;
+  size_t flags, rows, nrows, layer_off, total;
 };
-SelectWs select_ws_layout(int32_t n_slm) {
+SelectWs select_ws_layout(int32_t n_slm, int32_t n_layers) {
   SelectWs w;
   w.flags = 0;
   w.rows = round256(static_cast<size_t>(n_slm));
   w.nrows = w.rows + round256(static_cast<size_t>(n_slm) * 4);
-  w.total = w.nrows + 256;
+  w.layer_off = w.nrows + 256;
+  w.total = w.layer_off + round256(static_cast<size_t>(n_layers + 1) * 4);
   return w;
 }
 
@@ -158,7 +160,7 @@ int smallkv_budget_from_tau(double tau, int32_t n, int32_t* k_crit, int32_t* n_r
 size_t smallkv_select_workspace_size(const smallkv_cache* slm, const smallkv_batch* batch,
                                      int32_t n_llm_heads) {
   if (!slm || !batch || n_llm_heads < 1) return 0;
-  return select_ws_layout(slm->num_layers * slm->num_q_heads).total;
+  return select_ws_layout(slm->num_layers * slm->num_q_heads, slm->num_layers).total;
 }
 
 int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm, const smallkv_batch* batch,
@@ -190,7 +192,7 @@ int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm, const smallk
     return fail(SMALLKV_ERR_SHAPE, "SLM pool has %lld rows (>= 2^31)",
                 static_cast<long long>(rows_total));
   if (!aligned(slm_q, 4)) return fail(SMALLKV_ERR_ALIGN, "slm_q must be 4-byte aligned");
-  const SelectWs L = select_ws_layout(n_slm);
+  const SelectWs L = select_ws_layout(n_slm, slm->num_layers);
   if (!ws || ws_bytes < L.total)
     return fail(SMALLKV_ERR_WORKSPACE, "select workspace %zu < %zu bytes", ws_bytes, L.total);
   if ((rc = check_device()) != SMALLKV_OK) return rc;
@@ -216,7 +218,9 @@ int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm, const smallk
   uint8_t* flags = wsb + L.flags;
   int32_t* rows = reinterpret_cast<int32_t*>(wsb + L.rows);
   int32_t* nrows = reinterpret_cast<int32_t*>(wsb + L.nrows);
-  cudaError_t e = skv::launch_row_flags(head_map, n_llm_heads, n_slm, flags, rows, nrows, s);
+  int32_t* layer_off = reinterpret_cast<int32_t*>(wsb + L.layer_off);
+  cudaError_t e = skv::launch_row_flags(head_map, n_llm_heads, n_slm, slm->num_q_heads, flags,
+                                        rows, nrows, layer_off, s);
   if (e != cudaSuccess) return cuda_fail(e, "row_flags launch");
 
   skv::SlmScoreParams sp;
@@ -238,14 +242,11 @@ int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm, const smallk
   sp.box_rows = box_rows;
   sp.swz = swz ? 7u : 0u;
   sp.scale = 1.0f / std::sqrt(static_cast<float>(d));
-  e = skv::launch_slm_score(sp, map, batch->max_seq_len, s);
-  if (e != cudaSuccess) return cuda_fail(e, "slm_score launch");
-
   skv::SelectParams se;
   se.logits = slm_logits;
   se.seq_lens = batch->seq_lens;
   se.rows = rows;
-  se.n_rows = nrows;
+  se.layer_off = layer_off;
   se.k_crit = budgets->k_crit;
   se.n_recent = budgets->n_recent;
   se.k_marg = budgets->k_marg;
@@ -258,8 +259,36 @@ int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm, const smallk
   se.row_stride = batch->max_seq_len;
   se.max_crit = budgets->max_crit;
   se.max_marg = budgets->max_marg;
-  const int max_rows = n_slm < n_llm_heads ? n_slm : n_llm_heads;
-  e = skv::launch_select(se, max_rows, batch->max_seq_len, s);
+  // Score the SLM layers in chunks; the split of chunk i (ALU-bound) runs
+  // alongside the scoring of chunk i+1 (HBM-bound) via programmatic dependent
+  // launch: order  K1(0) K1(1) K2*(0) K1(2) K2*(1) ... K2(last).  K2*(i) reads
+  // only K1(i)'s rows, complete before K1(i+1) (a normal launch) started.
+  const int nl = slm->num_layers;
+  static const int chunks_env = [] {
+    const char* e = getenv("SMALLKV_SELECT_CHUNKS");   // tuning knob
+    return e ? atoi(e) : 0;
+  }();
+  const int want = chunks_env > 0 ? chunks_env : 1;
+  const int nchunk = nl < want ? nl : want;
+  auto chunk_lo = [&](int i) { return (nl * i) / nchunk; };
+  auto launch_k2 = [&](int i, bool overlap) {
+    se.layer_begin = chunk_lo(i);
+    se.layer_end = chunk_lo(i + 1);
+    const int rows_max = (se.layer_end - se.layer_begin) * slm->num_q_heads;
+    return skv::launch_select(se, rows_max < n_llm_heads ? rows_max : n_llm_heads,
+                              batch->max_seq_len, overlap, s);
+  };
+  for (int i = 0; i < nchunk; ++i) {
+    sp.layer_begin = chunk_lo(i);
+    sp.layer_end = chunk_lo(i + 1);
+    e = skv::launch_slm_score(sp, map, batch->max_seq_len, s);
+    if (e != cudaSuccess) return cuda_fail(e, "slm_score launch");
+    if (i > 0) {
+      e = launch_k2(i - 1, true);
+      if (e != cudaSuccess) return cuda_fail(e, "select launch");
+    }
+  }
+  e = launch_k2(nchunk - 1, false);
   if (e != cudaSuccess) return cuda_fail(e, "select launch");
   return SMALLKV_OK;
 }

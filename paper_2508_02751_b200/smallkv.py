@@ -328,5 +328,8 @@ class DecodeGraph:
 
     @property
     def kernels_per_step(self) -> int:
-        # row_flags + slm_score + select (+ plan), then one attend kernel per layer
-        return 3 + (1 if self.step.plan_buf is not None else 0) + len(self.plan)
+        # row_flags + (slm_score + select) per SLM-layer chunk (+ plan), then one
+        # attend kernel per layer
+        nl = self.step.slm.num_layers
+        return (1 + 2 * min(4, nl) + (1 if self.step.plan_buf is not None else 0)
+                + len(self.plan))
