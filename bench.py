@@ -91,17 +91,37 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def build_problem(cfg_name: str, rank: int, device):
+def build_problem(cfg_name: str, rank: int, world: int, shard: str, device):
+    """This rank's inputs.  batch sharding: its own batch of cfg.batch sequences
+    (seed = rank, weak scaling).  head sharding: the shared batch (seed 0) with
+    the LLM side restricted to this rank's kv-groups (strong scaling)."""
+    import dataclasses
     import torch
     import smallkv_synth as synth
+    from paper_2508_02751_b200 import dist as pdist
     cfg = synth.CONFIGS[cfg_name]
+    heads = shard == "heads" and world > 1
+    kv_share = cfg.llm.kv_heads // world if heads else cfg.llm.kv_heads
     # resident LLM layers: all when they fit, else a rotating subset (each slice >> L2)
-    per_layer = cfg.batch * cfg.llm.kv_heads * cfg.seq_len * cfg.llm.head_dim * 2 * 2
+    per_layer = cfg.batch * kv_share * cfg.seq_len * cfg.llm.head_dim * 2 * 2
     free = torch.cuda.mem_get_info(device)[0]
     slm_bytes = cfg.slm.layers * cfg.batch * cfg.slm.kv_heads * cfg.seq_len * cfg.slm.head_dim * 2
     budget = int(0.8 * free) - slm_bytes - (4 << 30)
+    if heads:   # the full LLM pool is generated once, then sliced
+        budget = budget * kv_share // cfg.llm.kv_heads
     resident = max(1, min(cfg.llm.layers, budget // per_layer))
-    p = synth.make_problem(cfg, seed=rank, device=device, llm_layers=list(range(resident)))
+    p = synth.make_problem(cfg, seed=0 if heads else rank, device=device,
+                           llm_layers=list(range(resident)))
+    if heads:
+        g0, g1 = pdist.kv_group_range(cfg.llm.kv_heads, world, rank)
+        L, H, Hkv = cfg.llm.layers, cfg.llm.q_heads, cfg.llm.kv_heads
+        k, v, q, hm = pdist.slice_llm_kv_groups(p.llm.k, p.llm.v, p.llm_q, p.head_map, L, H,
+                                                Hkv, g0, g1)
+        dims = synth.ModelDims(L, (g1 - g0) * (H // Hkv), g1 - g0, cfg.llm.head_dim)
+        p = dataclasses.replace(p, cfg=dataclasses.replace(cfg, llm=dims),
+                                llm=dataclasses.replace(p.llm, k=k, v=v, dims=dims),
+                                llm_q=q, head_map=hm)
+        torch.cuda.empty_cache()
     return p, resident
 
 
@@ -120,7 +140,8 @@ def run_ours(args, world, rank, local):
         dist.barrier()
     from paper_2508_02751_b200 import bytes_model, smallkv
 
-    p, resident = build_problem(args.config, rank, device)
+    heads = args.shard == "heads" and world > 1
+    p, resident = build_problem(args.config, rank, world, args.shard, device)
     cfg = p.cfg
     L = cfg.llm.layers
     step = smallkv.from_problem(p)
@@ -128,6 +149,17 @@ def run_ours(args, world, rank, local):
                        device=device)
     plan = [(l, l % resident, p.llm_q[l % resident], outs[l]) for l in range(L)]
     graph = smallkv.DecodeGraph(step, p.slm_q, plan, timing=False)
+    if heads:
+        # the exchange step of head sharding: all-gather every layer's per-head
+        # outputs [L, B, H/w, d] -> [L, B, H, d] once per step (NCCL / NVLink)
+        from paper_2508_02751_b200 import dist as pdist
+        inner = graph.replay
+
+        def replay_and_gather():
+            inner()
+            with torch.cuda.stream(graph.stream):
+                pdist.gather_heads(outs)
+        graph.replay = replay_and_gather
     if args.quick:
         for _ in range(args.warmup):
             graph.replay()
@@ -194,7 +226,8 @@ def run_ours(args, world, rank, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
     ms_per_step = max_ms / args.steps
-    layer_steps = world * L * args.steps / (max_ms / 1e3)
+    units = 1 if heads else world       # batches processed per step by the whole job
+    layer_steps = units * L * args.steps / (max_ms / 1e3)
 
     # ---- per-kernel durations.  The attend launches of a step overlap through
     # programmatic dependent launch, so an attend's effective duration is
@@ -241,7 +274,7 @@ def run_ours(args, world, rank, local):
     te = torch.tensor([e2e_ms], dtype=torch.float64, device=device)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = world * L * e2e_steps / (float(te.item()) / 1e3)
+    e2e_value = units * L * e2e_steps / (float(te.item()) / 1e3)
 
     if rank != 0:
         if world > 1:
@@ -268,15 +301,16 @@ def run_ours(args, world, rank, local):
         "warmup": args.warmup,
         "ms_per_step": round(ms_per_step, 5),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if heads else "weak",
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (seeded; Fig. 2-calibrated salience, random page tables)",
         "config": {
             "workload": f"{args.config}: {cfg.description}",
-            "global_batch": p.batch * world,
+            "global_batch": p.batch * units,
             "seq_len": cfg.seq_len,
-            "parallelism": f"batch-sharded x{world} (no collective)",
+            "parallelism": (f"kv-head-group sharded x{world} (+1 NCCL all-gather of outputs "
+                            "per step)" if heads else f"batch-sharded x{world} (no collective)"),
             "budget_K_R_M": list(cfg.budget),
             "head_map": "coherent (every SLM kv-head referenced)",
             "page_size": p.llm.page_size,
@@ -310,48 +344,54 @@ def run_ours(args, world, rank, local):
         "clocks": clocks,
     }
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(p, cfg, L, args.cpu_seqs)
+        line["cpu_baseline"] = cpu_baseline(p, cfg, L)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
 
 
-def cpu_baseline(p, cfg, L, n_seqs):
-    """Time the oracle, as it stands, on a bounded sample: n_seqs sequences,
-    the full SLM select for every row the step uses, one LLM layer's attend;
-    extrapolated to layer-steps/s of the whole workload (per sequence)."""
-    import numpy as np
-    import oracle
-    import smallkv_synth as synth  # noqa: F401
-
+def cpu_baseline(p, cfg, L, target_s: float = 12.0):
+    """Time the oracle, as it stands, on a bounded sample of the same step:
+    every sequence of the batch, the select for every SLM row the step uses,
+    and the attend of as many LLM layers as fit in ~target_s seconds; the
+    per-layer attend time is extrapolated to all L layers."""
     import dataclasses
-    idx = list(range(n_seqs))
-    sub = dataclasses.replace(
-        p, seq_lens=p.seq_lens[idx].contiguous(), slm_q=p.slm_q[:, idx].contiguous(),
-        llm_q=p.llm_q[:1, idx].contiguous(),
-        slm=dataclasses.replace(p.slm, block_table=p.slm.block_table[idx].contiguous()),
-        llm=dataclasses.replace(p.llm, k=p.llm.k[:1].contiguous(), v=p.llm.v[:1].contiguous(),
-                                block_table=p.llm.block_table[idx].contiguous()),
-        k_crit=p.k_crit[idx].contiguous(), n_recent=p.n_recent[idx].contiguous(),
-        k_marg=p.k_marg[idx].contiguous()).to("cpu")
+    import oracle
     from tests import parity
-    slm_v, llm_v = parity.views(sub)
-    rows = oracle.image_rows(sub.head_map)
+
+    def cpu_layer(slot):
+        return dataclasses.replace(
+            p, llm_q=p.llm_q[slot:slot + 1].contiguous(),
+            llm=dataclasses.replace(p.llm, k=p.llm.k[slot:slot + 1].contiguous(),
+                                    v=p.llm.v[slot:slot + 1].contiguous()),
+            llm_layer_ids=[p.llm_layer_ids[slot]]).to("cpu")
+
+    base = cpu_layer(0)
+    slm_v, _ = parity.views(base)
+    rows = oracle.image_rows(base.head_map)
     t0 = time.perf_counter()
-    sel = parity.oracle_select(sub, rows=rows, slm_view=slm_v)
-    t1 = time.perf_counter()
-    oracle.attend(0, 0, sub.llm_q[0], llm_v, sub.seq_lens, sub.head_map, sel,
-                  cfg.slm.layers * cfg.slm.q_heads)
-    t2 = time.perf_counter()
-    t_step = (t1 - t0) + L * (t2 - t1)            # seconds per step for n_seqs sequences
-    t_full = t_step * p.batch / n_seqs            # whole batch
-    return {"value": round(L / t_full, 4), "unit": "layer-steps/s", "cores": oracle.num_threads(),
+    sel = parity.oracle_select(base, rows=rows, slm_view=slm_v)
+    t_sel = time.perf_counter() - t0
+    t_layers = []
+    slot = 0
+    while slot < p.llm.num_layers:
+        sub = base if slot == 0 else cpu_layer(slot)
+        _, llm_v = parity.views(sub)
+        t1 = time.perf_counter()
+        oracle.attend(sub.llm_layer_ids[0], 0, sub.llm_q[0], llm_v, sub.seq_lens, sub.head_map,
+                      sel, cfg.slm.layers * cfg.slm.q_heads)
+        t_layers.append(time.perf_counter() - t1)
+        slot += 1
+        if t_sel + sum(t_layers) >= target_s:
+            break
+    t_step = t_sel + L * (sum(t_layers) / len(t_layers))
+    return {"value": round(L / t_step, 4), "unit": "layer-steps/s", "cores": oracle.num_threads(),
             "kind": "oracle",
-            "sample": (f"{n_seqs} of {p.batch} sequences: select over all {len(rows)} mapped SLM "
-                       f"rows + 1 LLM layer attend, measured {t2 - t0:.2f} s; extrapolated to "
-                       f"{L} layers x {p.batch} sequences"),
-            "measured_s": round(t2 - t0, 3)}
+            "sample": (f"all {p.batch} sequences: select over all {len(rows)} mapped SLM rows "
+                       f"({t_sel:.2f} s) + attend of {len(t_layers)} of {L} LLM layers "
+                       f"({sum(t_layers):.2f} s), per-layer time extrapolated to {L} layers"),
+            "measured_s": round(t_sel + sum(t_layers), 3)}
 
 
 def run_reference(args, world, rank, local):
@@ -407,7 +447,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="qwen7b")
-    ap.add_argument("--cpu-seqs", type=int, default=2)
+    ap.add_argument("--shard", choices=["batch", "heads"], default="batch",
+                    help="N>1 partition: sequences (weak scaling) or LLM kv-head groups")
+    ap.add_argument("--cpu-seqs", type=int, default=4,
+                    help="sequences per step of the --impl reference sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true",
                     help="profiling mode: only warm-up + timed replays (for ncu launch lists)")

@@ -5,7 +5,7 @@
  *
  * Citations: "P:n" = PAPER.md line n (section / equation named beside it),
  * "S:n" = SPEC.md line n.  The readings of ambiguous passages are listed in
- * DESIGN.md §3 ("readings") and referred to here as R1..R12.
+ * DESIGN.md §3 ("readings") and referred to here as R1..R15.
  *
  * The three hot-path calls follow the decode branch of Algorithm 1
  * (P:196-209):

@@ -7,7 +7,7 @@
  * header, table or helper with the CUDA path.  Only tests/, __graft_entry__.smoke()
  * and bench.py's cpu_baseline / --impl reference legs may load it.
  *
- * Citations: P:n = PAPER.md line n; S:n = SPEC.md line n; R1..R12 = the
+ * Citations: P:n = PAPER.md line n; S:n = SPEC.md line n; R1..R15 = the
  * readings listed in DESIGN.md §3.
  *
  * Every step follows the paper's order and notation:
@@ -20,7 +20,7 @@
  *                       index (R3).
  *   oracle_attend     — Eq. 6 / Alg. 1 l.12-14: O_c = FlashAttention over the
  *                       critical ∪ recent K/V (R2),
- *                       O_m = A'_{f(i)}[M]·V[M], O = O_c + O_m (R3,
+ *                       O_m = A'_{f(i)}[M]·V[M], O = O_c + O_m (R13,
  *                       P:205).
  *   oracle_match_heads— Eq. 2 Jaccard of TopK sets, Eq. 3 argmax.
  *
@@ -198,10 +198,10 @@ void oracle_select(const uint16_t* slm_q, const oracle_cache* slm,
  *                                               selected K/V, R2)
  *   O_c = Σ w_k V_g[k]   (0 when C ∪ R' is empty)
  *   O_m = Σ_{k∈M} a'_j[k] V_g[k]                (Eq. 6 second branch)
- *   out = O_c + O_m                              (no renormalisation, R3)
+ *   out = O_c + O_m                              (no renormalisation, R13)
  * a_rows[n_rows][B][max_n] are the SLM probabilities (from oracle_select);
  * crit/marg/counts are the selection lists (the oracle's own or, for output
- * parity, the GPU's verified ones, R12 of DESIGN.md §5).
+ * parity, the GPU's verified ones).
  * out: [B][H][d] doubles.  Also writes the critical softmax mass check
  * wsum_out[B][H] = Σ w_k (must be 1 when C ∪ R' is non-empty), may be NULL.
  * ------------------------------------------------------------------------- */

@@ -4,7 +4,7 @@
 //   O_c = softmax over the critical ∪ recent tokens (R2: FlashAttention over
 //         the selected K/V),
 //   O_m = Σ_{k ∈ marginal} A'_{f(i)}[k] · V[k]   (Eq. 6 second branch),
-//   O   = O_c + O_m                                (no renormalisation, R3).
+//   O   = O_c + O_m                                (no renormalisation, R13).
 //
 // B200 design.  Work unit = LLM kv-group g of sequence b.  Its q-heads map to
 // one or more DISTINCT SLM rows r (D6); the group's "virtual list" is

@@ -243,3 +243,28 @@ def test_two_valued_logits_radix_fallback():
     k[..., 1::2, :] = k[0, 0, 0, 1]       # odd rows: another
     p = dataclasses.replace(p, slm=dataclasses.replace(p.slm, k=k)).to("cuda")
     _check(p)
+
+
+def _head_shard(p, g0, g1):
+    from paper_2508_02751_b200 import dist as pdist
+    L, H, Hkv = p.cfg.llm.layers, p.cfg.llm.q_heads, p.cfg.llm.kv_heads
+    k, v, q, hm = pdist.slice_llm_kv_groups(p.llm.k, p.llm.v, p.llm_q, p.head_map, L, H, Hkv,
+                                            g0, g1)
+    G = H // Hkv
+    dims = synth.ModelDims(L, (g1 - g0) * G, g1 - g0, p.cfg.llm.head_dim)
+    cfg = dataclasses.replace(p.cfg, llm=dims)
+    return dataclasses.replace(p, cfg=cfg, llm=dataclasses.replace(p.llm, k=k, v=v, dims=dims),
+                               llm_q=q, head_map=hm)
+
+
+def test_head_split_virtual_shards_bit_identical():
+    """KV-head-group sharding (2 virtual ranks on one GPU): each shard's output
+    slice equals the unsharded output bit for bit (partition invariance P12)."""
+    cfg = _cfg(llm=(2, 8, 4, 128), slm=(2, 8, 2, 64), n=1800, B=2)
+    p = synth.make_problem(cfg, seed=16, page_size=16, seq_lens=[1800, 1000],
+                           map_kind="random").to("cuda")
+    _, _, full = parity.run_gpu_step(p)
+    for g0, g1 in [(0, 2), (2, 4)]:
+        _, _, part = parity.run_gpu_step(_head_shard(p, g0, g1))
+        for a, b in zip(full, part):
+            assert torch.equal(a[:, g0 * 2:g1 * 2], b)
