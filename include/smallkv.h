@@ -165,6 +165,11 @@ size_t smallkv_select_workspace_size(const smallkv_cache* slm,
  *               variant (Eq. 1 running sums) is not built yet and
  *               returns SMALLKV_ERR_UNSUPPORTED.
  *   ws          device workspace, >= smallkv_select_workspace_size bytes.
+ *   aux_stream  NULL, or a second stream: the SLM layers are then scored in
+ *               chunks on `stream` while the split of each finished chunk runs
+ *               on aux_stream (Alg. 1 l.8-9 "in parallel"); `stream`
+ *               waits for the last split before returning work to the caller.
+ *               Both streams must be on the current device; capturable.
  * Errors: NULL pointers, H_s % H_kv_s != 0, head_dim not in {64,128},
  * page_size not a power of two in [1,256], misaligned pointers, small ws,
  * non-sm_100 device.
@@ -174,7 +179,8 @@ int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm,
                    int32_t n_llm_heads, const smallkv_budgets* budgets,
                    float* slm_logits, float* slm_lse, int32_t* crit_idx,
                    int32_t* marg_idx, float* marg_w, int32_t* counts,
-                   float* acc, void* ws, size_t ws_bytes, void* stream);
+                   float* acc, void* ws, size_t ws_bytes, void* stream,
+                   void* aux_stream);
 
 /* Bytes of the gather plan of n_llm_layers layers (0 on invalid arguments). */
 size_t smallkv_plan_size(const smallkv_cache* llm, const smallkv_batch* batch,

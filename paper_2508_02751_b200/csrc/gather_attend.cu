@@ -94,40 +94,44 @@ __host__ __device__ constexpr int64_t plan_record_bytes(int nc) {
 }
 
 // All threads: distinct SLM rows of the group's heads (first occurrence order)
-// and the list sizes.  Two dependent rounds of loads (head map, counts).
+// and the list sizes.  K' and M' follow from the sequence's budgets with the
+// clamp of R5 (the same values smallkv_select writes to `counts`), so one round
+// of independent loads suffices.
 __device__ void build_layout(const AttendParams& p, int layer, int b, int g, GroupLayout& L) {
-  __shared__ int s_j[8], s_K[8], s_M[8];
+  __shared__ int s_j[8];
   const int G = p.heads / p.kv_heads;
   const int tid = threadIdx.x;
-  if (tid < G) {
-    const int j = p.head_map[layer * p.heads + g * G + tid];
-    const int64_t rb = static_cast<int64_t>(j) * p.batch + b;
-    s_j[tid] = j;
-    s_K[tid] = p.counts[rb * 2];
-    s_M[tid] = p.counts[rb * 2 + 1];
+  if (tid < G) s_j[tid] = p.head_map[layer * p.heads + g * G + tid];
+  if (tid == 32) {
+    const int n = p.seq_lens[b];
+    const int Rc = min(max(p.n_recent[b], 0), n);
+    const int Kc = min(min(max(p.k_crit[b], 0), n - Rc), p.max_crit);
+    const int Mc = min(min(max(p.k_marg[b], 0), n - Rc - Kc), p.max_marg);
+    L.n = n;
+    L.Rc = Rc;
+    L.rK[0] = Kc;   // temporarily: the per-row sizes
+    L.rM[0] = Mc;
   }
   __syncthreads();
   if (tid == 0) {
-    const int n = p.seq_lens[b];
-    const int Rc = min(max(p.n_recent[b], 0), n);
-    int nr = 0, T = Rc;
+    const int Kc = L.rK[0], Mc = L.rM[0];
+    int nr = 0;
     for (int h = 0; h < G; ++h) {
       int k = 0;
       while (k < nr && L.rj[k] != s_j[h]) ++k;
       if (k == nr) {
         L.rj[nr] = s_j[h];
-        L.rK[nr] = s_K[h];
-        L.rM[nr] = s_M[h];
         L.rhm[nr] = 0u;
-        T += s_K[h] + s_M[h];
         ++nr;
       }
       L.rhm[k] |= 1u << h;
     }
+    for (int k = 0; k < nr; ++k) {
+      L.rK[k] = Kc;
+      L.rM[k] = Mc;
+    }
     L.nrows = nr;
-    L.T = T;
-    L.Rc = Rc;
-    L.n = n;
+    L.T = L.Rc + nr * (Kc + Mc);
   }
   __syncthreads();
 }
@@ -173,38 +177,89 @@ __device__ void stage_entries(const AttendParams& p, const GroupLayout& L, int b
   const int32_t* bt = p.block_table + static_cast<int64_t>(b) * p.max_blocks;
   for (int i = tid; i < E; i += nthr) {
     const int pos = static_cast<int>(soff[i]);
-    const int page = __ldg(bt + pos / p.page_size);
+    const int page = __ldg(bt + (pos >> p.ps_shift));
     soff[i] = static_cast<uint32_t>(
-        ((static_cast<int64_t>(page) * p.kv_heads + g) * p.page_size + pos % p.page_size) * D);
+        ((static_cast<int64_t>(page) * p.kv_heads + g) * p.page_size + (pos & (p.page_size - 1))) * D);
   }
   __syncthreads();
 }
 
 // K3a — gather plan for every layer of the step (one launch after select):
-// CTA (c, g, layer*B + b) stages rank c's first batch of the group's list.
+// CTA (g, layer*B + b) stages the first batch of every cluster rank's share
+// of the group's list: 2 rounds of loads, 4 entries in flight per thread.
+constexpr int kPlanThreads = 256;
 template <int D>
-__global__ void __launch_bounds__(kThreads) plan_kernel(const AttendParams p) {
-  __shared__ GroupLayout L;
-  __shared__ uint32_t soff[kBatch], smk[kBatch];
-  __shared__ float sw[kBatch];
-  const int c = blockIdx.x, g = blockIdx.y;
-  const int layer = blockIdx.z / p.batch, b = blockIdx.z % p.batch;
-  const int NC = gridDim.x;
+__global__ void __launch_bounds__(kPlanThreads) plan_kernel(const AttendParams p) {
+  __shared__ __align__(16) GroupLayout L;
+  const int g = blockIdx.x;
+  const int layer = blockIdx.y / p.batch, b = blockIdx.y % p.batch;
+  const int NC = p.max_chunks;
+  const int G = p.heads / p.kv_heads;
+  const uint32_t allc = (1u << G) - 1u;
   griddep_wait();
   build_layout(p, layer, b, g, L);
-  const int e_lo = static_cast<int>((static_cast<int64_t>(L.T) * c) / NC);
-  const int e_hi = static_cast<int>((static_cast<int64_t>(L.T) * (c + 1)) / NC);
-  const int E = min(kBatch, e_hi - e_lo);
-  stage_entries<D>(p, L, b, g, e_lo, E, soff, smk, sw);
   uint8_t* rec = p.plan + ((static_cast<int64_t>(layer) * p.batch + b) * p.kv_heads + g) *
                               plan_record_bytes(NC);
-  if (c == 0 && threadIdx.x < sizeof(GroupLayout) / 4)
+  if (threadIdx.x < sizeof(GroupLayout) / 4)
     reinterpret_cast<int*>(rec)[threadIdx.x] = reinterpret_cast<const int*>(&L)[threadIdx.x];
-  uint32_t* poff = reinterpret_cast<uint32_t*>(rec + kHdrBytes) + static_cast<int64_t>(c) * kBatch * 3;
-  for (int i = threadIdx.x; i < E; i += kThreads) {
-    poff[i] = soff[i];
-    poff[kBatch + i] = smk[i];
-    reinterpret_cast<float*>(poff)[2 * kBatch + i] = sw[i];
+  const int32_t* bt = p.block_table + static_cast<int64_t>(b) * p.max_blocks;
+  // flattened over the group's list: entry x belongs to rank
+  // c = floor(((x+1)*NC - 1) / T) and is staged if it is in that rank's first batch
+  constexpr int U = 4;
+  const int T = L.T;
+  for (int base = threadIdx.x; base < T; base += U * kPlanThreads) {
+    int pos[U], slot_i[U];
+    uint32_t mk[U];
+    float wt[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int x0 = base + u * kPlanThreads;
+      slot_i[u] = -1;
+      pos[u] = 0;
+      mk[u] = 0u;
+      wt[u] = 0.f;
+      if (x0 >= T) continue;
+      const int c = ((x0 + 1) * NC - 1) / T;
+      const int e_lo = static_cast<int>((static_cast<int64_t>(T) * c) / NC);
+      const int i = x0 - e_lo;
+      if (i >= kBatch) continue;
+      slot_i[u] = c * kBatch + i;
+      int x = x0;
+      if (x < L.Rc) {
+        pos[u] = L.n - L.Rc + x;
+        mk[u] = allc;
+      } else {
+        x -= L.Rc;
+        int k = 0;
+        while (k < L.nrows - 1 && x >= L.rK[k] + L.rM[k]) {
+          x -= L.rK[k] + L.rM[k];
+          ++k;
+        }
+        const int64_t rb = static_cast<int64_t>(L.rj[k]) * p.batch + b;
+        if (x < L.rK[k]) {
+          pos[u] = __ldg(p.crit_idx + rb * p.max_crit + x);
+          mk[u] = L.rhm[k];
+        } else {
+          pos[u] = __ldg(p.marg_idx + rb * p.max_marg + (x - L.rK[k]));
+          wt[u] = __ldg(p.marg_w + rb * p.max_marg + (x - L.rK[k]));
+          mk[u] = L.rhm[k] << 8;
+        }
+      }
+    }
+    int page[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) page[u] = slot_i[u] >= 0 ? __ldg(bt + (pos[u] >> p.ps_shift)) : 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (slot_i[u] < 0) continue;
+      const int c = slot_i[u] / kBatch, i = slot_i[u] % kBatch;
+      uint32_t* slot = reinterpret_cast<uint32_t*>(rec + kHdrBytes) + static_cast<int64_t>(c) * kBatch * 3;
+      slot[i] = static_cast<uint32_t>(
+          ((static_cast<int64_t>(page[u]) * p.kv_heads + g) * p.page_size +
+           (pos[u] & (p.page_size - 1))) * D);
+      slot[kBatch + i] = mk[u];
+      reinterpret_cast<float*>(slot)[2 * kBatch + i] = wt[u];
+    }
   }
 }
 
@@ -541,8 +596,8 @@ int64_t plan_bytes(int32_t n_layers, int32_t batch, int32_t kv_heads, int32_t ma
 
 cudaError_t launch_plan(const AttendParams& p, int32_t n_layers, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.max_chunks, p.kv_heads, n_layers * p.batch);
-  cfg.blockDim = dim3(kThreads);
+  cfg.gridDim = dim3(p.kv_heads, n_layers * p.batch);
+  cfg.blockDim = dim3(kPlanThreads);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];

@@ -22,6 +22,9 @@ struct SlmScoreParams {
   uint32_t swz;               // 7 = 128B swizzle, 0 = none
   float scale;                // 1/sqrt(d)
   int32_t layer_begin, layer_end;   // SLM layers scored by this launch
+  const int32_t* n_recent;    // [B] (ranked range for the chunk statistics)
+  float4* stats;              // [l*H_s][B][n_chunks] (max, Σexp, min, max) per row chunk
+  int32_t n_chunks;           // chunks of chunk_tokens per row
 };
 cudaError_t launch_slm_score(const SlmScoreParams& p, const CUtensorMap& map, int max_seq_len,
                              cudaStream_t s);
@@ -44,6 +47,8 @@ struct SelectParams {
   int32_t* marg_idx;          // [l*H_s][B][max_marg]
   float* marg_w;
   int32_t* counts;            // [l*H_s][B][2]
+  const float4* stats;        // K1's per-chunk row statistics
+  int32_t n_chunks, chunk_tokens;
   int32_t batch, row_stride, max_crit, max_marg;
 };
 cudaError_t launch_select(const SelectParams& p, int32_t max_rows, int32_t max_seq_len,
@@ -58,6 +63,8 @@ struct AttendParams {
   const int32_t* seq_lens;
   const int32_t* head_map;    // [L*H]
   const int32_t* n_recent;
+  const int32_t* k_crit;
+  const int32_t* k_marg;
   const int32_t* crit_idx;
   const int32_t* marg_idx;
   const float* marg_w;        // a' at marg_idx
@@ -66,6 +73,7 @@ struct AttendParams {
   int64_t num_pages;
   int64_t layer_offset;       // cache_layer * num_pages * H_kv * page_size * d (elements)
   int32_t max_blocks, page_size, heads, kv_heads, head_dim, batch, layer;
+  int32_t ps_shift;           // log2(page_size)
   int32_t row_stride, max_crit, max_marg;
   int32_t max_chunks;         // CTAs (= cluster size) per (sequence, kv-group)
   float scale_log2;           // log2(e)/sqrt(d)

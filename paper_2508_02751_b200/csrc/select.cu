@@ -39,7 +39,7 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kBins = 256;
 constexpr int kCandCap = 1024;
-constexpr int kSmemCap = 40960;  // tokens held in shared memory (160 KB)
+constexpr int kSmemCap = 32768;  // tokens held in shared memory (row + bin bytes: 160 KB)
 
 __device__ __forceinline__ int iclamp(int x, int lo, int hi) { return x < lo ? lo : (x > hi ? hi : x); }
 
@@ -52,7 +52,7 @@ __device__ __forceinline__ void lse_combine(float& m, float& s, float m2, float 
 
 template <bool kInSmem>
 __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) {
-  extern __shared__ float vals[];
+  extern __shared__ float vals[];   // [n] row, then (kInSmem) [n] bin bytes
   __shared__ uint32_t hist[kWarps][kBins];
   __shared__ unsigned long long cand[2][kCandCap];
   __shared__ float red[4][kWarps];
@@ -80,40 +80,20 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
   const uint32_t lt = lanemask_lt();
   auto VAL = [&](int i) -> float { return kInSmem ? vals[i] : row[i]; };
 
-  // ---- pass 1: (max, Σexp) over [0, n) (online, per thread), range of [0, N)
-  float mt = -FLT_MAX, st = 0.f, lo = FLT_MAX, hi = -FLT_MAX;
-  for (int i = tid; i < n; i += kThreads) {
-    const float x = row[i];
-    if (kInSmem) vals[i] = x;
-    if (x > mt) {
-      st = st * __expf(mt - x) + 1.f;
-      mt = x;
-    } else {
-      st += __expf(x - mt);
-    }
-    if (i < N) {
-      lo = fminf(lo, x);
-      hi = fmaxf(hi, x);
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    lse_combine(mt, st, __shfl_xor_sync(0xffffffffu, mt, o), __shfl_xor_sync(0xffffffffu, st, o));
-    lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-    hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-  }
-  if (lane == 0) {
-    red[0][warp] = mt;
-    red[1][warp] = st;
-    red[2][warp] = lo;
-    red[3][warp] = hi;
-  }
-  __syncthreads();
+  // ---- pass 1: stage the row; (max, Σexp) over [0, n) and the ranked range
+  // [min, max] over [0, N) are merged from K1's per-chunk statistics (fixed order)
+  if (kInSmem)
+    for (int i = tid; i < n; i += kThreads) vals[i] = row[i];
   if (warp == 0) {
-    float m2 = lane < kWarps ? red[0][lane] : -FLT_MAX;
-    float s2 = lane < kWarps ? red[1][lane] : 0.f;
-    float l2 = lane < kWarps ? red[2][lane] : FLT_MAX;
-    float h2 = lane < kWarps ? red[3][lane] : -FLT_MAX;
+    const int nch = (n + p.chunk_tokens - 1) / p.chunk_tokens;
+    const float4* st = p.stats + rb * p.n_chunks;
+    float m2 = -FLT_MAX, s2 = 0.f, l2 = FLT_MAX, h2 = -FLT_MAX;
+    for (int c = lane; c < nch; c += 32) {
+      const float4 v = st[c];
+      lse_combine(m2, s2, v.x, v.y);
+      l2 = fminf(l2, v.z);
+      h2 = fmaxf(h2, v.w);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       lse_combine(m2, s2, __shfl_xor_sync(0xffffffffu, m2, o), __shfl_xor_sync(0xffffffffu, s2, o));
@@ -159,10 +139,12 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
   } else if (!s_fallback) {
     for (int i = tid; i < kWarps * kBins; i += kThreads) (&hist[0][0])[i] = 0u;
     __syncthreads();
+    uint8_t* sbin = reinterpret_cast<uint8_t*>(vals + n);
     for (int base = s0; base < s1; base += 32) {
       const int i = base + lane;
       if (i < s1) {
         const int bin = min(kBins - 1, static_cast<int>((VAL(i) - vlo) * scale));
+        if (kInSmem) sbin[i] = static_cast<uint8_t>(bin);
         atomicAdd(&hist[warp][bin], 1u);
       }
     }
@@ -205,11 +187,13 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
       __shared__ int s_cnt[2];
       if (tid < 2) s_cnt[tid] = 0;
       __syncthreads();
+      const uint8_t* sbin = reinterpret_cast<const uint8_t*>(vals + n);
       for (int i = tid; i < N; i += kThreads) {
-        const float x = VAL(i);
-        const int bin = min(kBins - 1, static_cast<int>((x - vlo) * scale));
+        const int bin = kInSmem ? static_cast<int>(sbin[i])
+                                : min(kBins - 1, static_cast<int>((VAL(i) - vlo) * scale));
+        if (bin != binA && bin != binB) continue;
         const unsigned long long kv =
-            (static_cast<unsigned long long>(desc_key(x)) << 32) | static_cast<uint32_t>(i);
+            (static_cast<unsigned long long>(desc_key(VAL(i))) << 32) | static_cast<uint32_t>(i);
         if (bin == binA) cand[0][atomicAdd(&s_cnt[0], 1)] = kv;
         if (bin == binB && !shared) cand[1][atomicAdd(&s_cnt[1], 1)] = kv;
       }
@@ -374,17 +358,18 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
   }
   __syncthreads();
 
-  // ---- emission: count per warp segment, scan, write ascending lists
-  const uint32_t TA = s_tk[0], TB = s_tk[1];
+  // ---- emission: (count per warp segment if not known,) write ascending lists.
+  // Thresholds compared as floats: key < T  <=>  x > key_to_float(T) (with -0 == +0).
+  const float XA = key_to_float(s_tk[0]), XB = key_to_float(s_tk[1]);
   const int IA = s_ti[0], IB = s_ti[1];
   if (!s_have_counts) {
     int cc = 0, cb = 0;
     for (int base = s0; base < s1; base += 32) {
       const int i = base + lane;
       const bool valid = i < s1;
-      const uint32_t k = valid ? desc_key(VAL(i)) : 0xffffffffu;
-      const bool isC = valid && (k < TA || (k == TA && i <= IA));
-      const bool inB = valid && (k < TB || (k == TB && i <= IB));
+      const float x = valid ? VAL(i) : -FLT_MAX;
+      const bool isC = valid && (x > XA || (x == XA && i <= IA));
+      const bool inB = valid && (x > XB || (x == XB && i <= IB));
       cc += __popc(__ballot_sync(0xffffffffu, isC));
       cb += __popc(__ballot_sync(0xffffffffu, inB));
     }
@@ -405,18 +390,17 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
   for (int base = s0; base < s1; base += 32) {
     const int i = base + lane;
     const bool valid = i < s1;
-    const float x = valid ? VAL(i) : 0.f;
-    const uint32_t k = valid ? desc_key(x) : 0xffffffffu;
-    const bool isC = valid && (k < TA || (k == TA && i <= IA));
-    const bool inB = valid && (k < TB || (k == TB && i <= IB));
+    const float x = valid ? VAL(i) : -FLT_MAX;
+    const bool isC = valid && (x > XA || (x == XA && i <= IA));
+    const bool inB = valid && (x > XB || (x == XB && i <= IB));
     const bool isM = inB && !isC;
     const uint32_t bc = __ballot_sync(0xffffffffu, isC);
     const uint32_t bm = __ballot_sync(0xffffffffu, isM);
-    if (isC) crit[oc + __popc(bc & lt)] = i;
+    const int c_at = oc + __popc(bc & lt), m_at = om + __popc(bm & lt);
+    if (isC) crit[c_at] = i;
     if (isM) {
-      const int o = om + __popc(bm & lt);
-      marg[o] = i;
-      mw[o] = expf(x - lse);
+      marg[m_at] = i;
+      mw[m_at] = __expf(x - lse);
     }
     oc += __popc(bc);
     om += __popc(bm);
@@ -441,7 +425,7 @@ cudaError_t launch_select(const SelectParams& p, int32_t max_rows, int32_t max_s
   cfg.numAttrs = overlap_previous ? 1 : 0;
   cudaError_t e;
   if (max_seq_len <= kSmemCap) {
-    cfg.dynamicSmemBytes = static_cast<size_t>(max_seq_len) * 4;
+    cfg.dynamicSmemBytes = static_cast<size_t>(max_seq_len) * 5;
     cudaFuncSetAttribute(select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(cfg.dynamicSmemBytes));
     e = cudaLaunchKernelEx(&cfg, select_kernel<true>, p);

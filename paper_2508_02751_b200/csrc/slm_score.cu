@@ -15,6 +15,8 @@
 // tensor cores (mma.sync m16n8k16: heads = M (padded to 16), tokens = N,
 // head_dim = K).  The path is HBM-bound (≈G_s flop/B); the tensor cores only
 // keep the ALU off the critical path.
+#include <float.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -119,6 +121,11 @@ slm_score_kernel(const __grid_constant__ CUtensorMap map, const SlmScoreParams p
   const uint32_t swz = p.swz;
   const int mi = lane >> 3;
   const int r_ld = warp * 16 + ((mi >> 1) << 3) + (lane & 7);   // token row this lane addresses
+  // per-row statistics of this chunk for K2 (rows gq and gq+8 of this lane):
+  // (max, Σexp rel. max) over [0, n) and (min, max) over the ranked [0, N)
+  const int N = n - min(max(p.n_recent[b], 0), n);
+  float st_m[2] = {-FLT_MAX, -FLT_MAX}, st_s[2] = {0.f, 0.f};
+  float st_lo[2] = {FLT_MAX, FLT_MAX}, st_hi[2] = {-FLT_MAX, -FLT_MAX};
 
   for (int it = 0; it < ntiles; ++it) {
     const int s = it % NSTAGE;
@@ -140,17 +147,65 @@ slm_score_kernel(const __grid_constant__ CUtensorMap map, const SlmScoreParams p
     if (lane == 0) mbar_arrive(&empty[s]);
     const int tw = t_begin + it * kTile + warp * 16;
 #pragma unroll
-    for (int ni = 0; ni < 2; ++ni) {
-      const int pos = tw + ni * 8 + 2 * tq;
-      if (row_lo) {
-        if (pos < t_end) row_lo[pos] = acc[ni][0] * p.scale;
-        if (pos + 1 < t_end) row_lo[pos + 1] = acc[ni][1] * p.scale;
+    for (int hr = 0; hr < 2; ++hr) {
+      float* row = hr == 0 ? row_lo : row_hi;
+      if (!row) continue;   // padding head or a row no LLM head uses
+      float v[4];
+      bool ok[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int pos = tw + (u >> 1) * 8 + 2 * tq + (u & 1);
+        v[u] = acc[u >> 1][2 * hr + (u & 1)] * p.scale;
+        ok[u] = pos < t_end;
+        if (ok[u] && pos < N) {
+          st_lo[hr] = fminf(st_lo[hr], v[u]);
+          st_hi[hr] = fmaxf(st_hi[hr], v[u]);
+        }
       }
-      if (row_hi) {
-        if (pos < t_end) row_hi[pos] = acc[ni][2] * p.scale;
-        if (pos + 1 < t_end) row_hi[pos + 1] = acc[ni][3] * p.scale;
-      }
+      float tm = -FLT_MAX;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) tm = ok[u] ? fmaxf(tm, v[u]) : tm;
+      const float nm = fmaxf(st_m[hr], tm);
+      float acc_s = st_s[hr] * __expf(st_m[hr] - nm);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc_s += ok[u] ? __expf(v[u] - nm) : 0.f;
+      st_m[hr] = nm;
+      st_s[hr] = acc_s;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (ok[u]) row[tw + (u >> 1) * 8 + 2 * tq + (u & 1)] = v[u];
     }
+  }
+
+  // ---- chunk statistics: lanes of a row (tq = 0..3), then the 4 warps (fixed order)
+  __shared__ float4 sst[kConsumers][16];
+#pragma unroll
+  for (int hr = 0; hr < 2; ++hr) {
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, st_m[hr], o);
+      const float s2 = __shfl_xor_sync(0xffffffffu, st_s[hr], o);
+      const float nm = fmaxf(st_m[hr], m2);
+      st_s[hr] = st_s[hr] * __expf(st_m[hr] - nm) + s2 * __expf(m2 - nm);
+      st_m[hr] = nm;
+      st_lo[hr] = fminf(st_lo[hr], __shfl_xor_sync(0xffffffffu, st_lo[hr], o));
+      st_hi[hr] = fmaxf(st_hi[hr], __shfl_xor_sync(0xffffffffu, st_hi[hr], o));
+    }
+    if (tq == 0) sst[warp][gq + 8 * hr] = make_float4(st_m[hr], st_s[hr], st_lo[hr], st_hi[hr]);
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(kConsumers * 32) : "memory");   // consumers only
+  if (warp == 0 && lane < 16 && lane < G && ((need >> lane) & 1u)) {
+    float4 a = sst[0][lane];
+#pragma unroll
+    for (int w = 1; w < kConsumers; ++w) {
+      const float4 c = sst[w][lane];
+      const float nm = fmaxf(a.x, c.x);
+      a.y = a.y * __expf(a.x - nm) + c.y * __expf(c.x - nm);
+      a.x = nm;
+      a.z = fminf(a.z, c.z);
+      a.w = fmaxf(a.w, c.w);
+    }
+    p.stats[(static_cast<int64_t>(head0 + lane) * p.batch + b) * p.n_chunks + blockIdx.x] = a;
   }
 }
 

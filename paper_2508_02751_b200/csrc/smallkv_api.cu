@@ -107,16 +107,20 @@ int check_budgets(const smallkv_budgets* bu) {
   return SMALLKV_OK;
 }
 
+constexpr int kScoreChunk = 1024;   // tokens per K1 CTA = per row-statistics chunk
+
 struct SelectWs {
-  size_t flags, rows, nrows, layer_off, total;
+  size_t flags, rows, nrows, layer_off, stats, total;
 };
-SelectWs select_ws_layout(int32_t n_slm, int32_t n_layers) {
+SelectWs select_ws_layout(int32_t n_slm, int32_t n_layers, int32_t batch, int32_t max_seq_len) {
   SelectWs w;
   w.flags = 0;
   w.rows = round256(static_cast<size_t>(n_slm));
   w.nrows = w.rows + round256(static_cast<size_t>(n_slm) * 4);
   w.layer_off = w.nrows + 256;
-  w.total = w.layer_off + round256(static_cast<size_t>(n_layers + 1) * 4);
+  w.stats = w.layer_off + round256(static_cast<size_t>(n_layers + 1) * 4);
+  const size_t nch = (static_cast<size_t>(max_seq_len) + kScoreChunk - 1) / kScoreChunk;
+  w.total = w.stats + round256(static_cast<size_t>(n_slm) * batch * nch * 16);
   return w;
 }
 
@@ -160,14 +164,15 @@ int smallkv_budget_from_tau(double tau, int32_t n, int32_t* k_crit, int32_t* n_r
 size_t smallkv_select_workspace_size(const smallkv_cache* slm, const smallkv_batch* batch,
                                      int32_t n_llm_heads) {
   if (!slm || !batch || n_llm_heads < 1) return 0;
-  return select_ws_layout(slm->num_layers * slm->num_q_heads, slm->num_layers).total;
+  return select_ws_layout(slm->num_layers * slm->num_q_heads, slm->num_layers, batch->batch,
+                          batch->max_seq_len).total;
 }
 
 int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm, const smallkv_batch* batch,
                    const int32_t* head_map, int32_t n_llm_heads, const smallkv_budgets* budgets,
                    float* slm_logits, float* slm_lse, int32_t* crit_idx, int32_t* marg_idx,
                    float* marg_w, int32_t* counts, float* acc, void* ws, size_t ws_bytes,
-                   void* stream) {
+                   void* stream, void* aux_stream) {
   int rc;
   if ((rc = check_cache(slm, false, "slm")) != SMALLKV_OK) return rc;
   if ((rc = check_batch(batch, slm)) != SMALLKV_OK) return rc;
@@ -192,7 +197,7 @@ int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm, const smallk
     return fail(SMALLKV_ERR_SHAPE, "SLM pool has %lld rows (>= 2^31)",
                 static_cast<long long>(rows_total));
   if (!aligned(slm_q, 4)) return fail(SMALLKV_ERR_ALIGN, "slm_q must be 4-byte aligned");
-  const SelectWs L = select_ws_layout(n_slm, slm->num_layers);
+  const SelectWs L = select_ws_layout(n_slm, slm->num_layers, batch->batch, batch->max_seq_len);
   if (!ws || ws_bytes < L.total)
     return fail(SMALLKV_ERR_WORKSPACE, "select workspace %zu < %zu bytes", ws_bytes, L.total);
   if ((rc = check_device()) != SMALLKV_OK) return rc;
@@ -238,7 +243,10 @@ int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm, const smallk
   sp.head_dim = d;
   sp.batch = batch->batch;
   sp.row_stride = batch->max_seq_len;
-  sp.chunk_tokens = 1024;
+  sp.chunk_tokens = kScoreChunk;
+  sp.n_recent = budgets->n_recent;
+  sp.stats = reinterpret_cast<float4*>(wsb + L.stats);
+  sp.n_chunks = (batch->max_seq_len + kScoreChunk - 1) / kScoreChunk;
   sp.box_rows = box_rows;
   sp.swz = swz ? 7u : 0u;
   sp.scale = 1.0f / std::sqrt(static_cast<float>(d));
@@ -259,38 +267,64 @@ int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm, const smallk
   se.row_stride = batch->max_seq_len;
   se.max_crit = budgets->max_crit;
   se.max_marg = budgets->max_marg;
-  // Score the SLM layers in chunks; the split of chunk i (ALU-bound) runs
-  // alongside the scoring of chunk i+1 (HBM-bound) via programmatic dependent
-  // launch: order  K1(0) K1(1) K2*(0) K1(2) K2*(1) ... K2(last).  K2*(i) reads
-  // only K1(i)'s rows, complete before K1(i+1) (a normal launch) started.
+  se.stats = sp.stats;
+  se.n_chunks = sp.n_chunks;
+  se.chunk_tokens = kScoreChunk;
+  // Score the SLM layers in chunks.  With an auxiliary stream the split of
+  // chunk i (ALU-bound K2) runs on it concurrently with the scoring of chunk
+  // i+1 (HBM-bound K1) on the main stream — the paper's "update KV cache in
+  // parallel" (Alg. 1 l.8-9) applied inside the selection; the main
+  // stream then waits for the last split.  Without one, the chunks run in order.
   const int nl = slm->num_layers;
   static const int chunks_env = [] {
     const char* e = getenv("SMALLKV_SELECT_CHUNKS");   // tuning knob
     return e ? atoi(e) : 0;
   }();
-  const int want = chunks_env > 0 ? chunks_env : 1;
+  const int want = chunks_env > 0 ? chunks_env : (aux_stream ? 4 : 1);
   const int nchunk = nl < want ? nl : want;
+  cudaStream_t aux = static_cast<cudaStream_t>(aux_stream);
   auto chunk_lo = [&](int i) { return (nl * i) / nchunk; };
-  auto launch_k2 = [&](int i, bool overlap) {
+  auto launch_k2 = [&](int i, cudaStream_t st) {
     se.layer_begin = chunk_lo(i);
     se.layer_end = chunk_lo(i + 1);
     const int rows_max = (se.layer_end - se.layer_begin) * slm->num_q_heads;
     return skv::launch_select(se, rows_max < n_llm_heads ? rows_max : n_llm_heads,
-                              batch->max_seq_len, overlap, s);
+                              batch->max_seq_len, false, st);
   };
-  for (int i = 0; i < nchunk; ++i) {
+  cudaEvent_t evs[9] = {};
+  const int nev = aux && nchunk > 1 ? nchunk + 1 : 0;
+  for (int i = 0; i < nev; ++i) {
+    e = cudaEventCreateWithFlags(&evs[i], cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+      for (int k = 0; k < i; ++k) cudaEventDestroy(evs[k]);
+      return cuda_fail(e, "cudaEventCreate");
+    }
+  }
+  int rc2 = SMALLKV_OK;
+  for (int i = 0; i < nchunk && rc2 == SMALLKV_OK; ++i) {
     sp.layer_begin = chunk_lo(i);
     sp.layer_end = chunk_lo(i + 1);
     e = skv::launch_slm_score(sp, map, batch->max_seq_len, s);
-    if (e != cudaSuccess) return cuda_fail(e, "slm_score launch");
-    if (i > 0) {
-      e = launch_k2(i - 1, true);
-      if (e != cudaSuccess) return cuda_fail(e, "select launch");
+    if (e != cudaSuccess) { rc2 = cuda_fail(e, "slm_score launch"); break; }
+    if (nev) {
+      if ((e = cudaEventRecord(evs[i], s)) != cudaSuccess ||
+          (e = cudaStreamWaitEvent(aux, evs[i], 0)) != cudaSuccess) {
+        rc2 = cuda_fail(e, "fork to aux stream");
+        break;
+      }
+      e = launch_k2(i, aux);
+    } else {
+      e = launch_k2(i, s);
     }
+    if (e != cudaSuccess) rc2 = cuda_fail(e, "select launch");
   }
-  e = launch_k2(nchunk - 1, false);
-  if (e != cudaSuccess) return cuda_fail(e, "select launch");
-  return SMALLKV_OK;
+  if (nev && rc2 == SMALLKV_OK) {
+    if ((e = cudaEventRecord(evs[nchunk], aux)) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(s, evs[nchunk], 0)) != cudaSuccess)
+      rc2 = cuda_fail(e, "join from aux stream");
+  }
+  for (int i = 0; i < nev; ++i) cudaEventDestroy(evs[i]);
+  return rc2;
 }
 
 size_t smallkv_attend_workspace_size(const smallkv_cache* llm, const smallkv_batch* batch) {
@@ -331,6 +365,8 @@ int fill_attend_params(skv::AttendParams& ap, const smallkv_cache* llm, const sm
   ap.seq_lens = batch->seq_lens;
   ap.head_map = head_map;
   ap.n_recent = budgets->n_recent;
+  ap.k_crit = budgets->k_crit;
+  ap.k_marg = budgets->k_marg;
   ap.crit_idx = crit_idx;
   ap.marg_idx = marg_idx;
   ap.marg_w = marg_w;
@@ -338,6 +374,8 @@ int fill_attend_params(skv::AttendParams& ap, const smallkv_cache* llm, const sm
   ap.num_pages = llm->num_pages;
   ap.max_blocks = llm->max_blocks;
   ap.page_size = llm->page_size;
+  ap.ps_shift = 0;
+  while ((1 << ap.ps_shift) < llm->page_size) ++ap.ps_shift;
   ap.heads = llm->num_q_heads;
   ap.kv_heads = llm->num_kv_heads;
   ap.head_dim = llm->head_dim;
@@ -364,7 +402,7 @@ int smallkv_plan(const smallkv_cache* llm, const smallkv_batch* batch, const int
     return fail(SMALLKV_ERR_WORKSPACE, "plan buffer %zu < %zu bytes", plan_bytes, need);
   if (!aligned(plan, 16)) return fail(SMALLKV_ERR_ALIGN, "plan must be 16-byte aligned");
   if (static_cast<int64_t>(n_llm_layers) * batch->batch > 65535)
-    return fail(SMALLKV_ERR_SHAPE, "L*B > 65535");
+    return fail(SMALLKV_ERR_SHAPE, "L*B > 65535");   // plan grid.y
   if ((rc = check_device()) != SMALLKV_OK) return rc;
   ap.plan = static_cast<uint8_t*>(plan);
   cudaError_t e = skv::launch_plan(ap, n_llm_layers, static_cast<cudaStream_t>(stream));

@@ -75,7 +75,7 @@ def load(path: Optional[str] = None):
         lib.smallkv_budget_from_tau.argtypes = [ctypes.c_double, i32, P, P, P]
         lib.smallkv_select_workspace_size.argtypes = [P, P, i32]
         lib.smallkv_select_workspace_size.restype = sz
-        lib.smallkv_select.argtypes = [P, P, P, P, i32, P, P, P, P, P, P, P, P, P, sz, P]
+        lib.smallkv_select.argtypes = [P, P, P, P, i32, P, P, P, P, P, P, P, P, P, sz, P, P]
         lib.smallkv_attend_workspace_size.argtypes = [P, P]
         lib.smallkv_attend_workspace_size.restype = sz
         lib.smallkv_attend.argtypes = [i32, i32, P, P, P, P, i32, i32, P, P, P, P, P, P, P, i32,
@@ -167,7 +167,8 @@ class DecodeStep:
     def __init__(self, *, slm_k, slm_block_table, slm_q_heads: int, llm_k, llm_v,
                  llm_block_table, llm_q_heads: int, llm_layers: int, seq_lens: torch.Tensor,
                  max_seq_len: int, head_map: torch.Tensor, k_crit, n_recent, k_marg,
-                 max_crit: int, max_marg: int, use_plan: bool = True):
+                 max_crit: int, max_marg: int, use_plan: bool = True,
+                 overlap_select: bool = False):
         self.lib = load()
         dev = seq_lens.device
         self._keep = (slm_k, slm_block_table, llm_k, llm_v, llm_block_table, seq_lens, head_map,
@@ -202,17 +203,20 @@ class DecodeStep:
                                             llm_layers)
         self.plan_buf = torch.empty(max(plan_b, 16), dtype=torch.uint8, device=dev) if use_plan else None
         self.planned = False
+        self.aux_stream = torch.cuda.Stream(device=dev) if overlap_select else None
 
     def select(self, slm_q: torch.Tensor, stream=None):
-        """smallkv_select, then (by default) smallkv_plan for every layer."""
+        """smallkv_select (K1 chunks overlapped with K2 on an auxiliary stream),
+        then (by default) smallkv_plan for every layer."""
         assert slm_q.dtype == torch.bfloat16 and slm_q.is_contiguous()
         o = self.out
+        aux = self.aux_stream.cuda_stream if self.aux_stream is not None else None
         rc = self.lib.smallkv_select(
             slm_q.data_ptr(), ctypes.byref(self.slm), ctypes.byref(self.batch),
             self.head_map.data_ptr(), self.head_map.numel(), ctypes.byref(self.budgets),
             o.logits.data_ptr(), o.lse.data_ptr(), o.crit.data_ptr(), o.marg.data_ptr(),
             o.marg_w.data_ptr(), o.counts.data_ptr(), None, self.ws_select.data_ptr(),
-            self.ws_select.numel(), _stream(stream))
+            self.ws_select.numel(), _stream(stream), aux)
         _check("smallkv_select", rc)
         self.planned = False
         if self.plan_buf is not None:
@@ -331,5 +335,6 @@ class DecodeGraph:
         # row_flags + (slm_score + select) per SLM-layer chunk (+ plan), then one
         # attend kernel per layer
         nl = self.step.slm.num_layers
-        return (1 + 2 * min(4, nl) + (1 if self.step.plan_buf is not None else 0)
+        chunks = min(4, nl) if self.step.aux_stream is not None else 1
+        return (1 + 2 * chunks + (1 if self.step.plan_buf is not None else 0)
                 + len(self.plan))

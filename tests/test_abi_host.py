@@ -68,7 +68,7 @@ def test_validation_errors_before_launch(lib):
     assert b"NULL" in lib.smallkv_last_error()
     bad = smallkv.CCache(16, 16, 16, 1, 1, 64, 1, 4, 2, 96)  # head_dim 96
     rc = lib.smallkv_select(16, ctypes.byref(bad), ctypes.byref(b), 16, 4, None, None, None,
-                            None, None, None, None, None, None, 0, None)
+                            None, None, None, None, None, None, 0, None, None)
     assert rc == 2  # ERR_SHAPE
     rc = lib.smallkv_match_heads(16, 1, 16, 1, 600, 3, 16, 16, 16, 1 << 20, None)
     assert rc == 2  # window > 512
