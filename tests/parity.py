@@ -14,7 +14,8 @@ import torch
 
 import oracle
 
-SET_BAND = 1e-6
+SET_BAND = 1e-6          # BASELINE.json north_star: score gaps below 1e-6 are exempt
+FLIP_LOGIT_BAND = 2e-5   # stricter internal bar: flips only within fp32 logit rounding
 OUT_TOL = 2e-3
 
 
@@ -47,7 +48,7 @@ def compare_select(p, gpu, sel, rows=None, batch_idx=None, logit_atol=2e-4):
     cnt = gpu.counts.cpu().numpy()
     bs = range(p.batch) if batch_idx is None else batch_idx
     rep = {"max_logit_err": 0.0, "max_lse_err": 0.0, "exempt_tokens": 0, "rows_checked": 0,
-           "max_margw_rel": 0.0}
+           "max_margw_rel": 0.0, "flips": 0, "max_flip_logit_gap": 0.0}
     for r, j in enumerate(rows):
         for b in bs:
             n = int(p.seq_lens[b])
@@ -79,6 +80,16 @@ def compare_select(p, gpu, sel, rows=None, batch_idx=None, logit_atol=2e-4):
             rep["exempt_tokens"] += len(ex)
             assert set(gC.tolist()) - ex == oC - ex, f"critical set mismatch row {j} seq {b}"
             assert set(gM.tolist()) - ex == oM - ex, f"marginal set mismatch row {j} seq {b}"
+            # stricter than the bar: tokens actually classified differently must
+            # sit within fp32 logit rounding (FLIP_LOGIT_BAND) of a boundary logit
+            flipped = (set(gC.tolist()) ^ oC) | (set(gM.tolist()) ^ oM)
+            if flipped:
+                bounds = [o_s[np.argsort(-o_a[: n - Rc], kind="stable")[k - 1]]
+                          for k in (Kc, Kc + Mc) if 0 < k <= n - Rc]
+                gap = max(min(abs(o_s[v] - t) for t in bounds) for v in flipped)
+                rep["flips"] += len(flipped)
+                rep["max_flip_logit_gap"] = max(rep["max_flip_logit_gap"], float(gap))
+                assert gap <= FLIP_LOGIT_BAND, f"flip {gap} away from a boundary, row {j} seq {b}"
             assert not (set(gC.tolist()) & set(gM.tolist()))
             assert np.all(gC < n - Rc) and np.all(gM < n - Rc)
             if Mc:

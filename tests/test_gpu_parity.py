@@ -268,3 +268,72 @@ def test_head_split_virtual_shards_bit_identical():
         _, _, part = parity.run_gpu_step(_head_shard(p, g0, g1))
         for a, b in zip(full, part):
             assert torch.equal(a[:, g0 * 2:g1 * 2], b)
+
+
+def _full_size_sampled(cfg, *, budget=None, n_rows=6, n_seqs=2, seed=2, layers=(0, 1)):
+    """Full BASELINE size on the GPU (all SLM layers, the given LLM layers
+    resident); selection checked on sampled rows x sequences, outputs of the
+    sampled sequences for every head of the resident layers."""
+    p = synth.make_problem(cfg, seed=seed, device="cuda", llm_layers=list(layers),
+                           budget=budget)
+    step, sel_gpu, outs = parity.run_gpu_step(p)
+    rng = np.random.default_rng(seed)
+    sb = sorted(rng.choice(p.batch, n_seqs, replace=False).tolist())
+    # only the sampled sequences go to the CPU: slice batch-indexed inputs
+    sub = dataclasses.replace(
+        p, seq_lens=p.seq_lens[sb].contiguous(), slm_q=p.slm_q[:, sb].contiguous(),
+        llm_q=p.llm_q[:, sb].contiguous(),
+        slm=dataclasses.replace(p.slm, block_table=p.slm.block_table[sb].contiguous()),
+        llm=dataclasses.replace(p.llm, block_table=p.llm.block_table[sb].contiguous()),
+        k_crit=p.k_crit[sb].contiguous(), n_recent=p.n_recent[sb].contiguous(),
+        k_marg=p.k_marg[sb].contiguous()).to("cpu")
+
+    class _SubSel:   # GPU selection outputs restricted to the sampled sequences
+        pass
+    gs = _SubSel()
+    for name in ("logits", "lse", "crit", "marg", "marg_w", "counts"):
+        setattr(gs, name, getattr(sel_gpu, name)[:, sb])
+    H = cfg.llm.q_heads
+    used = np.unique(np.concatenate(
+        [sub.head_map.numpy()[l * H:(l + 1) * H] for l in layers])).astype(np.int32)
+    sample = np.sort(rng.choice(used, min(n_rows, len(used)), replace=False)).astype(np.int32)
+    slm_view, llm_view = parity.views(sub)
+    rep = parity.compare_select(sub, gs, parity.oracle_select(sub, rows=sample,
+                                                              slm_view=slm_view))
+    sel_used = parity.oracle_select(sub, rows=used, slm_view=slm_view)
+    parity.compare_select(sub, gs, sel_used)
+    sg = parity.sel_from_gpu(sub, gs, sel_used)
+    errs = []
+    for slot in range(len(layers)):
+        e, _ = parity.compare_attend(sub, slot, outs[slot][sb].cpu(), sg, llm_view=llm_view)
+        errs.append(e)
+        assert e <= parity.OUT_TOL
+    rep["max_out_err"] = max(errs)
+    return rep
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("tau", [0.05, 0.5])
+def test_llama8b_full_size_sampled(tau):
+    """BASELINE configs[2]: LLaMA-3.1-8B + 3.2-1B, n=32768, B=16, budget
+    sweep end points (tau = 5% and 50%)."""
+    cfg = synth.CONFIGS["llama8b"]
+    print("llama8b", tau, _full_size_sampled(cfg, budget=synth.LLAMA8B_SWEEP[tau]))
+
+
+@pytest.mark.slow
+def test_qwen72b_full_size_sampled():
+    """BASELINE configs[3]: Qwen2.5-72B + 0.5B, n=131072, B=8 (2 resident LLM
+    layers of 80; layers 0 and 79 exercise both ends of the head map)."""
+    cfg = synth.CONFIGS["qwen72b"]
+    print("qwen72b", _full_size_sampled(cfg, layers=(0, 79), n_rows=4))
+
+
+@pytest.mark.slow
+def test_qwen14b_full_size_sampled():
+    """BASELINE configs[4]: Qwen2.5-14B + 1.5B, start of the long generation
+    (n=8193, B=64, d_s=128) and its end (n=16384, per-step tau budgets)."""
+    cfg = synth.CONFIGS["qwen14b"]
+    print("qwen14b n=8193", _full_size_sampled(cfg, n_seqs=3))
+    cfg16 = dataclasses.replace(cfg, seq_len=16384, batch=16)
+    print("qwen14b n=16384", _full_size_sampled(cfg16, budget=(1638, 819, 1638), n_seqs=2))
