@@ -57,6 +57,8 @@ def _load():
             lib.oracle_split.argtypes = [P, i32, i32, i32, i32, P, P, P]
             lib.oracle_select.argtypes = [P, P, P, i32, i32, P, i32, P, P, P, i32, i32,
                                           P, P, P, P, P, P]
+            lib.oracle_select_acc.argtypes = [P, P, P, i32, i32, P, i32, P, P, P, i32, i32,
+                                              P, P, P, P, P, P, P]
             lib.oracle_attend.argtypes = [i32, i32, P, P, P, i32, P, P, P, i32, P, P, P,
                                           i32, i32, P, P]
             lib.oracle_topk.argtypes = [P, i32, i32, P]
@@ -157,6 +159,32 @@ def select(slm_q, slm: CacheView, seq_lens, rows, k_crit, n_recent, k_marg,
                       _ptr(crit), _ptr(marg), _ptr(counts))
     return {"a": a, "s": s, "stats": stats, "crit": crit, "marg": marg,
             "counts": counts, "rows": rows}
+
+
+def select_acc(slm_q, slm: CacheView, seq_lens, rows, k_crit, n_recent, k_marg,
+               max_crit: int, max_marg: int, max_n: int, acc: np.ndarray):
+    """Variant f1: as `select`, ranking by the running column sums acc (fp64
+    [rows][B][max_n], updated in place: acc += a')."""
+    lib = _load()
+    q = _bf16_bits(slm_q)
+    sl = _i32(seq_lens)
+    rows = _i32(rows)
+    B = sl.shape[0]
+    nr = rows.shape[0]
+    assert acc.dtype == np.float64 and acc.shape == (nr, B, max_n) and acc.flags.c_contiguous
+    kc, nrc, km = _i32(k_crit), _i32(n_recent), _i32(k_marg)
+    a = np.zeros((nr, B, max_n), np.float64)
+    s = np.zeros((nr, B, max_n), np.float64)
+    stats = np.zeros((nr, B, 2), np.float64)
+    crit = np.zeros((nr, B, max(max_crit, 1)), np.int32)
+    marg = np.zeros((nr, B, max(max_marg, 1)), np.int32)
+    counts = np.zeros((nr, B, 3), np.int32)
+    lib.oracle_select_acc(_ptr(q), ctypes.byref(slm.struct), _ptr(sl), B, max_n,
+                          _ptr(rows), nr, _ptr(kc), _ptr(nrc), _ptr(km),
+                          crit.shape[2], marg.shape[2], _ptr(acc), _ptr(a), _ptr(s),
+                          _ptr(stats), _ptr(crit), _ptr(marg), _ptr(counts))
+    return {"a": a, "s": s, "stats": stats, "crit": crit, "marg": marg,
+            "counts": counts, "rows": rows, "acc": acc.copy()}
 
 
 def attend(layer: int, cache_layer: int, q, llm: CacheView, seq_lens, head_map,

@@ -190,6 +190,40 @@ void oracle_select(const uint16_t* slm_q, const oracle_cache* slm,
 }
 
 /* ------------------------------------------------------------------------- *
+ * Variant f1: accumulative score selection.  Eq. 1
+ * defines F(A, C) as the column sums s^v = Σ_u A[u, v] of the attention matrix;
+ * in decode each step contributes one more row, so the running score of the
+ * SLM row j is  F_t[v] = F_{t-1}[v] + a'_t[v]  (positions new at step t start
+ * from F_{t-1} = 0, i.e. the caller zero-fills acc once).  The split then ranks
+ * by F_t instead of a'_t (Eq. 6 with F over all rows seen so far); the
+ * marginal weights stay the current row a'_t (Eq. 6: A'_{f(i)}[k]).
+ * acc [n_rows][B][max_n] is read and updated in place; everything else is as
+ * oracle_select.
+ * ------------------------------------------------------------------------- */
+void oracle_select_acc(const uint16_t* slm_q, const oracle_cache* slm,
+                       const int32_t* seq_lens, int32_t batch, int32_t max_n,
+                       const int32_t* rows, int32_t n_rows, const int32_t* k_crit,
+                       const int32_t* n_recent, const int32_t* k_marg,
+                       int32_t max_crit, int32_t max_marg, double* acc, double* a_out,
+                       double* s_out, double* stats, int32_t* crit, int32_t* marg,
+                       int32_t* counts) {
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t rb = 0; rb < (int64_t)n_rows * batch; ++rb) {
+    const int32_t r = (int32_t)(rb / batch), b = (int32_t)(rb % batch);
+    const int32_t n = seq_lens[b];
+    double* a = a_out + rb * max_n;
+    double* f = acc + rb * max_n;
+    double* s = s_out ? s_out + rb * max_n : (double*)malloc(sizeof(double) * n);
+    oracle_slm_row(slm_q, slm, batch, rows[r], b, n, s, a, &stats[rb * 2],
+                   &stats[rb * 2 + 1]);
+    for (int32_t v = 0; v < n; ++v) f[v] += a[v];
+    oracle_split(f, n, k_crit[b], n_recent[b], k_marg[b], crit + rb * max_crit,
+                 marg + rb * max_marg, counts + rb * 3);
+    if (!s_out) free(s);
+  }
+}
+
+/* ------------------------------------------------------------------------- *
  * Step 4: compensated attention of one LLM layer (Alg. 1 l.12-14).
  * For LLM head h of layer `layer` (cache slot `cache_layer`), j = head_map[layer*H+h],
  * kv head g = h / (H/H_kv), and the sets of row r_of_head = row_slot[j]:

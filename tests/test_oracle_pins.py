@@ -328,3 +328,51 @@ def test_match_monotone_in_slm_pool(oracle_mod):
     _, j4 = oracle_mod.match_heads(llm_F, slm_F[:4], 20)
     _, j8 = oracle_mod.match_heads(llm_F, slm_F, 20)
     assert np.all(j8 >= j4)
+
+
+# --------------------------------------------------------------------------- f1 (accumulated score)
+
+def test_P13_accumulated_score_uniform_causal(oracle_mod):
+    """f1: q' = 0 makes every decode row uniform over its n tokens; three steps
+    with n = 1, 2, 3 accumulate the column sums of the uniform causal matrix,
+    (11/6, 5/6, 1/3) (Eq. 1)."""
+    p = _small(seq_lens=(3,), budget=(1, 0, 1))
+    p = dataclasses.replace(p, slm_q=torch.zeros_like(p.slm_q))
+    slm, _ = _views(oracle_mod, p)
+    rows = oracle_mod.image_rows(p.head_map)
+    acc = np.zeros((len(rows), 1, 3), np.float64)
+    for n in (1, 2, 3):
+        sel = oracle_mod.select_acc(p.slm_q, slm, torch.tensor([n], dtype=torch.int32), rows,
+                                    p.k_crit, p.n_recent, p.k_marg, p.max_crit, p.max_marg, 3,
+                                    acc)
+    g = GOLDEN["column_sums_uniform_causal_n3"]["F"]
+    np.testing.assert_allclose(acc[:, 0, :], np.tile(g, (len(rows), 1)), rtol=0, atol=1e-15)
+    # ranked by the running sums: position 0 (11/6) is critical, 1 (5/6) marginal
+    assert sel["crit"][0, 0, 0] == 0 and sel["marg"][0, 0, 0] == 1
+
+
+def test_f1_accumulated_equals_sum_of_rows(oracle_mod):
+    """acc after T steps = Σ_t softmax rows (torch), and the sets = full sort of it."""
+    p = _small(seq_lens=(90, 60), budget=(10, 5, 15))
+    slm, _ = _views(oracle_mod, p)
+    rows = oracle_mod.image_rows(p.head_map)
+    acc = np.zeros((len(rows), 2, 90), np.float64)
+    ref = np.zeros_like(acc)
+    steps = [(80, 50), (85, 55), (90, 60)]
+    for ns in steps:
+        sl = torch.tensor(ns, dtype=torch.int32)
+        sel = oracle_mod.select_acc(p.slm_q, slm, sl, rows, p.k_crit, p.n_recent, p.k_marg,
+                                    p.max_crit, p.max_marg, 90, acc)
+        pp = dataclasses.replace(p, seq_lens=sl)
+        for r, j in enumerate(rows):
+            for b in range(2):
+                _, a = _slm_softmax(pp, j, b)
+                ref[r, b, :ns[b]] += a.numpy()
+    np.testing.assert_allclose(acc, ref, rtol=1e-12, atol=1e-15)
+    for r in range(len(rows)):
+        for b in range(2):
+            n = steps[-1][b]
+            bc, bm, _, _ = brute_split(ref[r, b, :n].tolist(), 10, 5, 15)
+            Kc, Mc, _ = sel["counts"][r, b]
+            assert sel["crit"][r, b, :Kc].tolist() == bc
+            assert sel["marg"][r, b, :Mc].tolist() == bm
