@@ -161,9 +161,12 @@ size_t smallkv_select_workspace_size(const smallkv_cache* slm,
  *   marg_idx    device int32 [l*H_s][B][max_marg]    ascending positions.
  *   marg_w      device fp32 [l*H_s][B][max_marg]     a'_v at marg_idx.
  *   counts      device int32 [l*H_s][B][2]           (K', M') after clamping.
- *   acc         must be NULL (current-row score, R1).  The accumulated-score
- *               variant (Eq. 1 running sums) is not built yet and
- *               returns SMALLKV_ERR_UNSUPPORTED.
+ *   acc         NULL: rank by the current row (R1).  Otherwise variant f1
+ *               (Eq. 1 running column sums): device fp32
+ *               [l*H_s][B][max_seq_len], read and updated in place for the rows
+ *               in image(f): acc[v] += a'_v (v < n), and positions are ranked by
+ *               the updated acc (desc, index asc).  The caller zero-fills it once
+ *               per sequence; marg_w stays the current a' (Eq. 6).
  *   ws          device workspace, >= smallkv_select_workspace_size bytes.
  *   aux_stream  NULL, or a second stream: the SLM layers are then scored in
  *               chunks on `stream` while the split of each finished chunk runs

@@ -48,6 +48,7 @@ struct SelectParams {
   float* marg_w;
   int32_t* counts;            // [l*H_s][B][2]
   const float4* stats;        // K1's per-chunk row statistics
+  float* acc;                 // f1 running column sums [l*H_s][B][row_stride] or nullptr
   int32_t n_chunks, chunk_tokens;
   int32_t batch, row_stride, max_crit, max_marg;
 };

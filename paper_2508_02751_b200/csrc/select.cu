@@ -78,11 +78,15 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
   const int N = n - Rc;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t lt = lanemask_lt();
-  auto VAL = [&](int i) -> float { return kInSmem ? vals[i] : row[i]; };
+  // the ranking score: the logit (R1) or, for variant f1, the running column
+  // sum acc (Eq. 1) updated below
+  float* accrow = p.acc ? p.acc + rb * p.row_stride : nullptr;
+  const float* score = accrow ? accrow : row;
+  auto VAL = [&](int i) -> float { return kInSmem ? vals[i] : score[i]; };
 
   // ---- pass 1: stage the row; (max, Σexp) over [0, n) and the ranked range
   // [min, max] over [0, N) are merged from K1's per-chunk statistics (fixed order)
-  if (kInSmem)
+  if (kInSmem && !accrow)
     for (int i = tid; i < n; i += kThreads) vals[i] = row[i];
   if (warp == 0) {
     const int nch = (n + p.chunk_tokens - 1) / p.chunk_tokens;
@@ -113,7 +117,34 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
   }
   __syncthreads();
   const float lse = red[0][0] + logf(red[1][0]);
-  const float vlo = red[2][0], vhi = red[3][0];
+  float vlo = red[2][0], vhi = red[3][0];
+  if (accrow) {
+    // f1: acc[v] += a'_v for v < n (in place), rank on acc; range over [0, N)
+    float lo = FLT_MAX, hi = -FLT_MAX;
+    for (int i = tid; i < n; i += kThreads) {
+      const float v = accrow[i] + __expf(row[i] - lse);
+      accrow[i] = v;
+      if (kInSmem) vals[i] = v;
+      if (i < N) {
+        lo = fminf(lo, v);
+        hi = fmaxf(hi, v);
+      }
+    }
+    lo = -warp_max(-lo);
+    hi = warp_max(hi);
+    __syncthreads();
+    if (lane == 0) {
+      red[2][warp] = lo;
+      red[3][warp] = hi;
+    }
+    __syncthreads();
+    vlo = FLT_MAX;
+    vhi = -FLT_MAX;
+    for (int w = 0; w < kWarps; ++w) {
+      vlo = fminf(vlo, red[2][w]);
+      vhi = fmaxf(vhi, red[3][w]);
+    }
+  }
   const int rA = Kc, rB = Kc + Mc;
   if (rB == 0) return;
 
@@ -400,7 +431,7 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
     if (isC) crit[c_at] = i;
     if (isM) {
       marg[m_at] = i;
-      mw[m_at] = __expf(x - lse);
+      mw[m_at] = __expf((accrow ? row[i] : x) - lse);   // a' of the current step (Eq. 6)
     }
     oc += __popc(bc);
     om += __popc(bm);

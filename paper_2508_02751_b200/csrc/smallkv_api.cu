@@ -180,9 +180,6 @@ int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm, const smallk
   if (!slm_q || !head_map || !slm_logits || !slm_lse || !crit_idx || !marg_idx || !marg_w ||
       !counts)
     return fail(SMALLKV_ERR_NULL, "smallkv_select: NULL input/output pointer");
-  if (acc)
-    return fail(SMALLKV_ERR_UNSUPPORTED,
-                "accumulated-score selection (acc != NULL) is not built yet; pass NULL");
   if (n_llm_heads < 1) return fail(SMALLKV_ERR_SHAPE, "n_llm_heads must be >= 1");
   const int G_s = slm->num_q_heads / slm->num_kv_heads;
   if (G_s > 16) return fail(SMALLKV_ERR_SHAPE, "SLM GQA group %d > 16", G_s);
@@ -268,6 +265,7 @@ int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm, const smallk
   se.max_crit = budgets->max_crit;
   se.max_marg = budgets->max_marg;
   se.stats = sp.stats;
+  se.acc = acc;
   se.n_chunks = sp.n_chunks;
   se.chunk_tokens = kScoreChunk;
   // Score the SLM layers in chunks.  With an auxiliary stream the split of

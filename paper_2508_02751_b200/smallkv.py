@@ -205,17 +205,21 @@ class DecodeStep:
         self.planned = False
         self.aux_stream = torch.cuda.Stream(device=dev) if overlap_select else None
 
-    def select(self, slm_q: torch.Tensor, stream=None):
-        """smallkv_select (K1 chunks overlapped with K2 on an auxiliary stream),
-        then (by default) smallkv_plan for every layer."""
+    def select(self, slm_q: torch.Tensor, stream=None, acc: Optional[torch.Tensor] = None):
+        """smallkv_select, then (by default) smallkv_plan for every layer.
+        acc: optional fp32 [l*H_s][B][max_seq_len] running column sums (variant
+        f1, zero-filled once by the caller; updated in place)."""
         assert slm_q.dtype == torch.bfloat16 and slm_q.is_contiguous()
+        if acc is not None:
+            assert acc.dtype == torch.float32 and acc.is_contiguous()
+            assert acc.shape == self.out.logits.shape
         o = self.out
         aux = self.aux_stream.cuda_stream if self.aux_stream is not None else None
         rc = self.lib.smallkv_select(
             slm_q.data_ptr(), ctypes.byref(self.slm), ctypes.byref(self.batch),
             self.head_map.data_ptr(), self.head_map.numel(), ctypes.byref(self.budgets),
             o.logits.data_ptr(), o.lse.data_ptr(), o.crit.data_ptr(), o.marg.data_ptr(),
-            o.marg_w.data_ptr(), o.counts.data_ptr(), None, self.ws_select.data_ptr(),
+            o.marg_w.data_ptr(), o.counts.data_ptr(), _ptr(acc), self.ws_select.data_ptr(),
             self.ws_select.numel(), _stream(stream), aux)
         _check("smallkv_select", rc)
         self.planned = False

@@ -36,9 +36,11 @@ def oracle_select(p, rows=None, slm_view=None):
                          p.max_crit, p.max_marg, p.max_seq_len)
 
 
-def compare_select(p, gpu, sel, rows=None, batch_idx=None, logit_atol=2e-4):
+def compare_select(p, gpu, sel, rows=None, batch_idx=None, logit_atol=2e-4, rank_score=None):
     """Check GPU select outputs against oracle dict `sel` for its rows.
-    Returns a report dict; raises AssertionError on a violation."""
+    rank_score: the oracle's ranking score per [row][b][v] when it is not the
+    current-row probability (variant f1: the running sums); flips are then
+    bounded relative to it.  Returns a report dict; raises AssertionError."""
     rows = sel["rows"]
     lg = gpu.logits.cpu().double().numpy()
     lse = gpu.lse.cpu().double().numpy()
@@ -54,6 +56,7 @@ def compare_select(p, gpu, sel, rows=None, batch_idx=None, logit_atol=2e-4):
             n = int(p.seq_lens[b])
             o_s = sel["s"][r, b, :n]
             o_a = sel["a"][r, b, :n]
+            o_r = o_a if rank_score is None else rank_score[r, b, :n]   # ranking score
             Kc, Mc, Rc = (int(x) for x in sel["counts"][r, b])
             err = np.abs(lg[j, b, :n] - o_s).max()
             rep["max_logit_err"] = max(rep["max_logit_err"], float(err))
@@ -69,12 +72,12 @@ def compare_select(p, gpu, sel, rows=None, batch_idx=None, logit_atol=2e-4):
             oC = set(sel["crit"][r, b, :Kc].tolist())
             oM = set(sel["marg"][r, b, :Mc].tolist())
             # exempt band around the oracle's two rank boundaries
-            ranked = np.sort(o_a[: n - Rc])[::-1]
+            ranked = np.sort(o_r[: n - Rc])[::-1]
             exempt = np.zeros(n, bool)
             for k in (Kc, Kc + Mc):
                 if 0 < k <= n - Rc:
                     th = ranked[k - 1]
-                    exempt |= np.abs(o_a - th) < SET_BAND * max(1.0, abs(th))
+                    exempt |= np.abs(o_r - th) < SET_BAND * max(1.0, abs(th))
             exempt[n - Rc:] = False
             ex = set(np.nonzero(exempt)[0].tolist())
             rep["exempt_tokens"] += len(ex)
@@ -84,9 +87,11 @@ def compare_select(p, gpu, sel, rows=None, batch_idx=None, logit_atol=2e-4):
             # sit within fp32 logit rounding (FLIP_LOGIT_BAND) of a boundary logit
             flipped = (set(gC.tolist()) ^ oC) | (set(gM.tolist()) ^ oM)
             if flipped:
-                bounds = [o_s[np.argsort(-o_a[: n - Rc], kind="stable")[k - 1]]
+                sc = o_s if rank_score is None else o_r   # logits, or the f1 sums
+                bounds = [sc[np.argsort(-o_r[: n - Rc], kind="stable")[k - 1]]
                           for k in (Kc, Kc + Mc) if 0 < k <= n - Rc]
-                gap = max(min(abs(o_s[v] - t) for t in bounds) for v in flipped)
+                gap = max(min(abs(sc[v] - t) / max(1.0, abs(t)) for t in bounds)
+                          for v in flipped)
                 rep["flips"] += len(flipped)
                 rep["max_flip_logit_gap"] = max(rep["max_flip_logit_gap"], float(gap))
                 assert gap <= FLIP_LOGIT_BAND, f"flip {gap} away from a boundary, row {j} seq {b}"

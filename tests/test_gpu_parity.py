@@ -337,3 +337,38 @@ def test_qwen14b_full_size_sampled():
     print("qwen14b n=8193", _full_size_sampled(cfg, n_seqs=3))
     cfg16 = dataclasses.replace(cfg, seq_len=16384, batch=16)
     print("qwen14b n=16384", _full_size_sampled(cfg16, budget=(1638, 819, 1638), n_seqs=2))
+
+
+def test_f1_accumulated_score_multistep():
+    """Variant f1 over 4 decode steps (n grows by one each step): the GPU's
+    running sums track the oracle's fp64 chain and the sets match within the
+    A18 band (relative 1e-6 for sums > 1), outputs within 2e-3."""
+    import oracle
+    from paper_2508_02751_b200 import smallkv
+    cfg = _cfg(n=1500, B=2, budget=(120, 40, 160))
+    p = synth.make_problem(cfg, seed=17, page_size=16, seq_lens=[1500, 900]).to("cuda")
+    step = smallkv.from_problem(p)
+    acc = torch.zeros_like(step.out.logits)
+    pc = p.to("cpu")
+    slm_view, llm_view = parity.views(pc)
+    rows = oracle.image_rows(pc.head_map)
+    oacc = np.zeros((len(rows), p.batch, p.max_seq_len), np.float64)
+    for d in (3, 2, 1, 0):
+        sl = torch.tensor([1500 - d, 900 - d], dtype=torch.int32)
+        p.seq_lens.copy_(sl)
+        sel_gpu = step.select(p.slm_q, acc=acc)
+        torch.cuda.synchronize()
+        sel = oracle.select_acc(pc.slm_q, slm_view, sl, rows, pc.k_crit, pc.n_recent,
+                                pc.k_marg, p.max_crit, p.max_marg, p.max_seq_len, oacc)
+    ga = acc.cpu().double().numpy()[rows]
+    for b, n in enumerate([1500, 900]):
+        np.testing.assert_allclose(ga[:, b, :n], oacc[:, b, :n], rtol=2e-5, atol=1e-7)
+    # sets: ranked by the oracle's running sums
+    pcs = dataclasses.replace(pc, seq_lens=sl)
+    rep = parity.compare_select(pcs, sel_gpu, sel, rank_score=oacc)
+    out = torch.empty(p.batch, cfg.llm.q_heads, cfg.llm.head_dim, device="cuda")
+    step.attend(0, 0, p.llm_q[0], out)
+    sg = parity.sel_from_gpu(pcs, sel_gpu, sel)
+    e, _ = parity.compare_attend(pcs, 0, out, sg, llm_view=llm_view)
+    assert e <= parity.OUT_TOL
+    print("f1", rep, e)
