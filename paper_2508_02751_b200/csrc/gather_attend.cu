@@ -56,7 +56,7 @@ __device__ __forceinline__ long long gtimer() {
 
 namespace {
 constexpr int kTile = 16;      // rows (tokens) per warp tile
-constexpr int kWarps = 4;
+constexpr int kWarps = 8;      // one CTA per SM (8 warps x 3-stage rings = 192 KB)
 constexpr int kThreads = kWarps * 32;
 constexpr int kBatch = 1024;   // entries whose positions/pages/weights are staged at once
 
@@ -136,6 +136,35 @@ __device__ void build_layout(const AttendParams& p, int layer, int b, int g, Gro
   __syncthreads();
 }
 
+// First entry of cluster rank c's share of the group's list.  Shares are
+// balanced by BYTES, not entries: a critical/recent entry reads K and V (weight
+// 2), a marginal one only V (weight 1); rank c starts at the first entry whose
+// cumulative weight reaches floor(W * c / NC).
+__device__ __forceinline__ int split_begin(const GroupLayout& L, int c, int NC) {
+  int64_t W = 2 * static_cast<int64_t>(L.Rc);
+  for (int k = 0; k < L.nrows; ++k) W += 2 * static_cast<int64_t>(L.rK[k]) + L.rM[k];
+  const int64_t target = (W * c) / NC;
+  int64_t w = 0;
+  int x = 0;
+  auto seg = [&](int len, int weight, int& out) -> bool {
+    const int64_t sw = static_cast<int64_t>(len) * weight;
+    if (w + sw >= target) {
+      out = x + static_cast<int>((target - w + weight - 1) / weight);
+      return true;
+    }
+    w += sw;
+    x += len;
+    return false;
+  };
+  int out = 0;
+  if (seg(L.Rc, 2, out)) return out;
+  for (int k = 0; k < L.nrows; ++k) {
+    if (seg(L.rK[k], 2, out)) return out;
+    if (seg(L.rM[k], 1, out)) return out;
+  }
+  return x;
+}
+
 // All threads: stage entries [e_b, e_b + E) of the group's virtual list:
 // row offset in the layer's pool (elements), head mask, marginal weight.
 // Two dependent rounds of loads (list values, page table).
@@ -203,8 +232,12 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const AttendParams p
   if (threadIdx.x < sizeof(GroupLayout) / 4)
     reinterpret_cast<int*>(rec)[threadIdx.x] = reinterpret_cast<const int*>(&L)[threadIdx.x];
   const int32_t* bt = p.block_table + static_cast<int64_t>(b) * p.max_blocks;
-  // flattened over the group's list: entry x belongs to rank
-  // c = floor(((x+1)*NC - 1) / T) and is staged if it is in that rank's first batch
+  // flattened over the group's list: entry x belongs to the rank whose
+  // byte-balanced share contains it and is staged if it is in that rank's
+  // first batch
+  __shared__ int s_split[9];
+  if (threadIdx.x <= NC) s_split[threadIdx.x] = split_begin(L, threadIdx.x, NC);
+  __syncthreads();
   constexpr int U = 4;
   const int T = L.T;
   for (int base = threadIdx.x; base < T; base += U * kPlanThreads) {
@@ -219,9 +252,9 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const AttendParams p
       mk[u] = 0u;
       wt[u] = 0.f;
       if (x0 >= T) continue;
-      const int c = ((x0 + 1) * NC - 1) / T;
-      const int e_lo = static_cast<int>((static_cast<int64_t>(T) * c) / NC);
-      const int i = x0 - e_lo;
+      int c = 0;
+      while (c < NC - 1 && x0 >= s_split[c + 1]) ++c;
+      const int i = x0 - s_split[c];
       if (i >= kBatch) continue;
       slot_i[u] = c * kBatch + i;
       int x = x0;
@@ -264,7 +297,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const AttendParams p
 }
 
 template <int D>
-__global__ void __launch_bounds__(kThreads, 2) attend_kernel(const AttendParams p) {
+__global__ void __launch_bounds__(kThreads, 1) attend_kernel(const AttendParams p) {
   constexpr int NSTAGE = stages_for<D>();
   constexpr int ROWB = D * 2;                // bytes per K or V row
   constexpr int KV_BYTES = kTile * ROWB;
@@ -277,6 +310,9 @@ __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const AttendParams 
   float* sw = reinterpret_cast<float*>(smk + kBatch);
   uint8_t* stages = reinterpret_cast<uint8_t*>(sw + kBatch);
   __shared__ __align__(16) GroupLayout L;
+  constexpr int kMaxTiles = kBatch / kTile + 2 * 8 + 2;
+  __shared__ uint32_t s_tiles[kMaxTiles];
+  __shared__ int s_ntile;
 
   const int c = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
   const int NC = gridDim.x;
@@ -304,8 +340,9 @@ __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const AttendParams 
     build_layout(p, p.layer, b, g, L);
   }
   const int T = L.T;
-  const int e_lo = static_cast<int>((static_cast<int64_t>(T) * c) / NC);
-  const int e_hi = static_cast<int>((static_cast<int64_t>(T) * (c + 1)) / NC);
+  const int e_lo = split_begin(L, c, NC);
+  const int e_hi = split_begin(L, c + 1, NC);
+  (void)T;
   SKV_T(1);
 
   const int gq = lane >> 2, tq = lane & 3;
@@ -343,7 +380,28 @@ __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const AttendParams 
     if (!(rec && e_b == e_lo)) stage_entries<D>(p, L, b, g, e_b, E, soff, smk, sw);
     SKV_T(2);
 
-    const int ntile = (E + kTile - 1) / kTile;
+    // ---- tiles of this batch: runs of K+V entries (recent / critical) in
+    // 16-row tiles, runs of V-only (marginal) entries in 32-row tiles — both
+    // fill one 8 KB stage, so the tile count tracks the bytes
+    if (tid == 0) {
+      int nt = 0, x = 0;
+      auto run = [&](int len, bool vonly) {
+        const int a = max(x, e_b), z = min(x + len, e_b + E);
+        const int ts = vonly ? 2 * kTile : kTile;
+        for (int y = a; y < z; y += ts)
+          s_tiles[nt++] = static_cast<uint32_t>(y - e_b) | (static_cast<uint32_t>(min(ts, z - y)) << 16) |
+                          (vonly ? (1u << 24) : 0u);
+        x += len;
+      };
+      run(L.Rc, false);
+      for (int k = 0; k < L.nrows; ++k) {
+        run(L.rK[k], false);
+        run(L.rM[k], true);
+      }
+      s_ntile = nt;
+    }
+    __syncthreads();
+    const int ntile = s_ntile;
     const int nmy = ntile > warp ? (ntile - warp + kWarps - 1) / kWarps : 0;
 
     // Each cp.async instruction of the warp moves 4 rows x 128 contiguous bytes:
@@ -352,20 +410,34 @@ __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const AttendParams 
     auto issue = [&](int i) {
       if (i < nmy) {
         uint8_t* st = wst + ((tbase + i) % NSTAGE) * SB;
-        const int e0 = (warp + i * kWarps) * kTile;
+        const uint32_t td = s_tiles[warp + i * kWarps];
+        const int e0 = static_cast<int>(td & 0xffffu), cnt = static_cast<int>((td >> 16) & 0xffu);
+        if (td >> 24) {
+          // V-only tile: 32 V rows fill the stage
 #pragma unroll
-        for (int grp = 0; grp < kTile / 4; ++grp) {
-          const int eo = grp * 4 + (lane >> 3);
-          const int e = e0 + eo;
-          const bool ev = e < E;
-          const uint32_t ro = ev ? soff[e] : 0u;
-          const bool kc = ev && (smk[e] & 0xffu) != 0u;
+          for (int grp = 0; grp < 2 * kTile / 4; ++grp) {
+            const int eo = grp * 4 + (lane >> 3);
+            const bool ev = eo < cnt;
+            const uint32_t ro = ev ? soff[e0 + eo] : 0u;
 #pragma unroll
-          for (int hf = 0; hf < D / 64; ++hf) {
-            const int ch = hf * 8 + (lane & 7);
-            const int sw_ = (ch ^ (eo & 7)) << 4;
-            if (kc) cp_async16(smem_u32(st + eo * ROWB + sw_), kpool + ro + ch * 8, true);
-            cp_async16(smem_u32(st + KV_BYTES + eo * ROWB + sw_), vpool + ro + ch * 8, ev);
+            for (int hf = 0; hf < D / 64; ++hf) {
+              const int ch = hf * 8 + (lane & 7);
+              cp_async16(smem_u32(st + eo * ROWB + ((ch ^ (eo & 7)) << 4)), vpool + ro + ch * 8, ev);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int grp = 0; grp < kTile / 4; ++grp) {
+            const int eo = grp * 4 + (lane >> 3);
+            const bool ev = eo < cnt;
+            const uint32_t ro = ev ? soff[e0 + eo] : 0u;
+#pragma unroll
+            for (int hf = 0; hf < D / 64; ++hf) {
+              const int ch = hf * 8 + (lane & 7);
+              const int sw_ = (ch ^ (eo & 7)) << 4;
+              if (ev) cp_async16(smem_u32(st + eo * ROWB + sw_), kpool + ro + ch * 8, true);
+              cp_async16(smem_u32(st + KV_BYTES + eo * ROWB + sw_), vpool + ro + ch * 8, ev);
+            }
           }
         }
       }
@@ -382,18 +454,58 @@ __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const AttendParams 
       const uint8_t* st = wst + ((tbase + i) % NSTAGE) * SB;
       const uint8_t* kb = st;
       const uint8_t* vb = st + KV_BYTES;
-      const int e0 = (warp + i * kWarps) * kTile;
+      const uint32_t td = s_tiles[warp + i * kWarps];
+      const int e0 = static_cast<int>(td & 0xffffu), cnt = static_cast<int>((td >> 16) & 0xffu);
+      if (td >> 24) {
+        // ---- V-only tile (marginal entries): O_m += a' · V over 32 rows
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          float wm[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int tok = half * 16 + (u >> 1) * 8 + 2 * tq + (u & 1);
+            const uint32_t mk = tok < cnt ? smk[e0 + tok] : 0u;
+            wm[u] = (gq < G && ((mk >> (8 + gq)) & 1u)) ? sw[e0 + tok] : 0.f;
+          }
+          uint32_t h1, l1, h3, l3;
+          split_bf16x2(wm[0], wm[1], h1, l1);
+          split_bf16x2(wm[2], wm[3], h3, l3);
+#pragma unroll
+          for (int t = 0; t < NT; t += 2) {
+            const int r = half * 16 + ((mi & 1) << 3) + (lane & 7);
+            const int ch = t + (mi >> 1);
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4_t(smem_u32(st + r * ROWB + ((ch ^ (r & 7)) << 4)), b0, b1, b2, b3);
+            mma_bf16(o[t], 0u, h1, 0u, h3, b0, b1);
+            mma_bf16(o[t], 0u, l1, 0u, l3, b0, b1);
+            mma_bf16(o[t + 1], 0u, h1, 0u, h3, b2, b3);
+            mma_bf16(o[t + 1], 0u, l1, 0u, l3, b2, b3);
+          }
+        }
+        __syncwarp();
+        continue;
+      }
 
       // S = Q K^T : rows = heads, cols = 16 tokens (two n8 tiles)
+      // four independent accumulation chains (even / odd k-steps) halve the
+      // dependent HMMA latency of the QK product
       float sacc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      float sod[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk) {
         const int r = ((mi >> 1) << 3) + (lane & 7);
         const int ch = 2 * kk + (mi & 1);
         uint32_t b0, b1, b2, b3;
         ldsm_x4(smem_u32(kb + r * ROWB + ((ch ^ (r & 7)) << 4)), b0, b1, b2, b3);
-        mma_bf16(sacc[0], qa[kk][0], 0u, qa[kk][1], 0u, b0, b1);
-        mma_bf16(sacc[1], qa[kk][0], 0u, qa[kk][1], 0u, b2, b3);
+        float(&a0)[4] = (kk & 1) ? sod[0] : sacc[0];
+        float(&a1)[4] = (kk & 1) ? sod[1] : sacc[1];
+        mma_bf16(a0, qa[kk][0], 0u, qa[kk][1], 0u, b0, b1);
+        mma_bf16(a1, qa[kk][0], 0u, qa[kk][1], 0u, b2, b3);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        sacc[0][u] += sod[0][u];
+        sacc[1][u] += sod[1][u];
       }
       // masks / weights for this lane's head gq and tokens {2tq, 2tq+1, 8+2tq, 9+2tq}
       float sv[4], wm[4];
@@ -401,7 +513,7 @@ __global__ void __launch_bounds__(kThreads, 2) attend_kernel(const AttendParams 
       for (int u = 0; u < 4; ++u) {
         const int tok = (u >> 1) * 8 + 2 * tq + (u & 1);
         const int e = e0 + tok;
-        const uint32_t mk = e < E ? smk[e] : 0u;
+        const uint32_t mk = tok < cnt ? smk[e] : 0u;
         const bool crit = gq < G && ((mk >> gq) & 1u);
         const bool marg = gq < G && ((mk >> (8 + gq)) & 1u);
         sv[u] = crit ? sacc[u >> 1][u & 1] * p.scale_log2 : -INFINITY;
@@ -554,16 +666,27 @@ extern "C" int skv_debug_set_trace(long long* buf) {
 }
 #endif
 
-// CTAs per (sequence, kv-group) = cluster size: one per ~2K tokens of
-// context, at most 8 (portable cluster size).
-int32_t attend_ctas_per_group(int32_t max_seq_len) {
-  static const int32_t tokens_per_cta = [] {
-    const char* e = getenv("SMALLKV_ATTEND_TOKENS_PER_CTA");   // tuning knob
-    const int v = e ? atoi(e) : 0;
-    return v > 0 ? v : 2048;
+// CTAs per (sequence, kv-group) = cluster size: as many as fill the GPU with
+// one 8-warp CTA per SM in a single wave, i.e. floor(#SMs / #groups), 1..8.
+// (Config 2: 128 groups -> 1; config 4 at one GPU: 64 groups -> 2.)
+int32_t attend_ctas_per_group(int32_t batch, int32_t kv_heads) {
+  static const int32_t forced = [] {
+    const char* e = getenv("SMALLKV_ATTEND_CTAS");   // tuning knob
+    return e ? atoi(e) : 0;
   }();
-  const int32_t nc = (max_seq_len + tokens_per_cta - 1) / tokens_per_cta;
-  return nc < 1 ? 1 : (nc > 8 ? 8 : nc);
+  if (forced > 0) return forced > 8 ? 8 : forced;
+  static const int32_t sms = [] {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = 148;   // B200
+    }
+    return n;
+  }();
+  const int64_t groups = static_cast<int64_t>(batch) * kv_heads;
+  const int64_t nc = groups > 0 ? sms / groups : 1;
+  return nc < 1 ? 1 : (nc > 8 ? 8 : static_cast<int32_t>(nc));
 }
 
 template <int D>
@@ -591,7 +714,7 @@ static cudaError_t launch_d(const AttendParams& p, cudaStream_t s) {
 
 int64_t plan_bytes(int32_t n_layers, int32_t batch, int32_t kv_heads, int32_t max_seq_len) {
   return static_cast<int64_t>(n_layers) * batch * kv_heads *
-         plan_record_bytes(attend_ctas_per_group(max_seq_len));
+         plan_record_bytes(attend_ctas_per_group(batch, kv_heads));
 }
 
 cudaError_t launch_plan(const AttendParams& p, int32_t n_layers, cudaStream_t s) {

@@ -84,7 +84,7 @@ struct AttendParams {
 cudaError_t launch_attend(const AttendParams& p, cudaStream_t s);
 cudaError_t launch_plan(const AttendParams& p, int32_t n_layers, cudaStream_t s);
 int64_t plan_bytes(int32_t n_layers, int32_t batch, int32_t kv_heads, int32_t max_seq_len);
-int32_t attend_ctas_per_group(int32_t max_seq_len);
+int32_t attend_ctas_per_group(int32_t batch, int32_t kv_heads);
 
 // ---------------------------------------------------------------- K0 match_heads
 cudaError_t launch_match_heads(const float* llm_F, int32_t n_llm, const float* slm_F,

@@ -74,7 +74,14 @@ slm_score_kernel(const __grid_constant__ CUtensorMap map, const SlmScoreParams p
   __syncthreads();
 
   if (warp == kConsumers) {
-    // ---------------- TMA producer (one elected lane)
+    // ---------------- TMA producer: the warp stages the chunk's page-table
+    // entries (one round), then one elected lane streams the tiles
+    __shared__ int sbt[1024];
+    const int first_blk = t_begin / p.page_size;
+    const int nblk = (t_end - 1) / p.page_size - first_blk + 1;   // <= 1024 (chunk <= 1024 tokens)
+    const int32_t* btb = p.block_table + static_cast<int64_t>(b) * p.max_blocks + first_blk;
+    for (int i = lane; i < nblk; i += 32) sbt[i] = btb[i];
+    __syncwarp();
     if (lane == 0) {
       prefetch_tmap(&map);
       const int boxes_per_tile = kTile / p.box_rows;
@@ -87,7 +94,7 @@ slm_score_kernel(const __grid_constant__ CUtensorMap map, const SlmScoreParams p
         mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(nbox * HALVES * p.box_rows * 128));
         for (int bx = 0; bx < nbox; ++bx) {
           const int t = t0 + bx * p.box_rows;
-          const int page = p.block_table[static_cast<int64_t>(b) * p.max_blocks + t / p.page_size];
+          const int page = sbt[t / p.page_size - first_blk];
           const int64_t row64 =
               ((static_cast<int64_t>(layer) * p.num_pages + page) * p.kv_heads + kvh) * p.page_size +
               t % p.page_size;

@@ -132,9 +132,8 @@ struct AttendWs {
 // (distributed shared memory), so it needs no global scratch; the workspace
 // argument is kept for ABI stability and future variants.
 AttendWs attend_ws_layout(const smallkv_cache* llm, const smallkv_batch* b) {
-  (void)llm;
   AttendWs w;
-  w.ctas = skv::attend_ctas_per_group(b->max_seq_len);
+  w.ctas = skv::attend_ctas_per_group(b->batch, llm->num_kv_heads);
   w.total = 256;
   return w;
 }
@@ -381,7 +380,7 @@ int fill_attend_params(skv::AttendParams& ap, const smallkv_cache* llm, const sm
   ap.row_stride = batch->max_seq_len;
   ap.max_crit = budgets->max_crit;
   ap.max_marg = budgets->max_marg;
-  ap.max_chunks = skv::attend_ctas_per_group(batch->max_seq_len);
+  ap.max_chunks = skv::attend_ctas_per_group(batch->batch, llm->num_kv_heads);
   ap.scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(llm->head_dim));
   return SMALLKV_OK;
 }
