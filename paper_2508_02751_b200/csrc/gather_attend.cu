@@ -13,22 +13,26 @@
 // 8..15: marginal for head h).  For a group-coherent map (one row) this is
 // exactly the group's union, so every K/V row is read from HBM once; for a
 // non-coherent map a position chosen by two rows is read twice.
-// The list is split evenly by entry count over gridDim.x CTAs (balanced, no
-// position scan); each CTA stages its entries' positions and page-table
-// entries in two parallel rounds, then every warp streams its own 16-row tiles
-// with cp.async (4 rows x 128 B per instruction, XOR-swizzled, zero-filled
-// tails; K rows only for critical entries) through a private multi-stage ring
-// and runs on the tensor cores (mma.sync m16n8k16):
-//   S[16 x 16] = Q_group[16 x d] · K_tile^T        (heads = M, tokens = N)
-//   O[16 x d] += A[16 x 16] · V_tile               (A rows 0..7: online-softmax
-//                                                    weights p of head h;
-//                                                    rows 8..15: marginal
-//                                                    weights a' of head h)
-// so the marginal compensation shares the PV contraction with the critical
-// part (register-resident A, FA2-style), with A split into bf16 hi + lo parts
-// (two MMAs) to keep ~2^-17 relative precision on the weights.  Warps merge in
-// shared memory in a fixed order; the CTAs of a group merge through a
-// deterministic last-CTA log-sum-exp combine (K4 fused): bit-reproducible.
+// The list is split over the gridDim.x CTAs of a cluster in byte-balanced
+// shares; the plan kernel (K3a) pre-stages each share's first batch (pool row
+// offsets, head masks, marginal weights), then every warp streams its own
+// 8 KB tiles — 16 K+V rows (recent / critical) or 32 V rows (marginal) — with
+// cp.async (4 rows x 128 B per instruction, XOR-swizzled, zero-filled tails)
+// through a private 3-stage ring
+// and runs on the tensor cores (mma.sync m16n8k16) in the transposed
+// orientation, so no MMA row is spent on absent heads (a kv-group has G <= 8
+// q-heads, the MMA's M is 16):
+//   S^T[16 tok x 8 heads]  = K_tile[16 x d] · Q_group^T      (8 MMAs for d=128)
+//   O_c^T[d x 8 heads]    += V_tile^T · P^T                  (softmax weights p)
+//   O_m^T[d x 8 heads]    += V_tile^T · A'^T                 (marginal weights a')
+// P^T leaves the QK accumulators in (token, head) order; movmatrix transposes
+// its bf16 pairs into the B-operand layout.  Weights are split into bf16
+// hi + lo parts (two MMAs) to keep ~2^-17 relative precision.  The online
+// softmax is lazy: a head's base is raised (with the O rescale) only when a
+// score exceeds it by more than 8 (log2 units) — one warp vote per tile in the
+// common case.  Warps merge in shared memory in a fixed order; the CTAs of a
+// group merge through distributed shared memory in rank order (K4 fused):
+// bit-reproducible.
 #include <float.h>
 #include <limits.h>
 #include <stdlib.h>
@@ -302,7 +306,6 @@ __global__ void __launch_bounds__(kThreads, 1) attend_kernel(const AttendParams 
   constexpr int ROWB = D * 2;                // bytes per K or V row
   constexpr int KV_BYTES = kTile * ROWB;
   constexpr int SB = stage_bytes<D>();
-  constexpr int NT = D / 8;                  // n8 tiles of the output
 
   extern __shared__ __align__(128) uint8_t smem[];
   uint32_t* soff = reinterpret_cast<uint32_t*>(smem);   // row offset in the layer's pool (elements)
@@ -367,11 +370,20 @@ __global__ void __launch_bounds__(kThreads, 1) attend_kernel(const AttendParams 
     q_ready = true;
   };
 
-  float o[NT][4];
+  // O^T accumulators (MMA rows = d, columns = heads): lane holds d = 16*mt +
+  // gq (+8) for heads 2*tq, 2*tq+1.  oc: softmax part (critical ∪ recent),
+  // om: marginal compensation (Eq. 6 second branch).
+  constexpr int MT = D / 16;
+  float oc[MT][4], om[MT][4];
 #pragma unroll
-  for (int t = 0; t < NT; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
-  float m_run = -INFINITY, l_run = 0.f;
+  for (int t = 0; t < MT; ++t) {
+    oc[t][0] = oc[t][1] = oc[t][2] = oc[t][3] = 0.f;
+    om[t][0] = om[t][1] = om[t][2] = om[t][3] = 0.f;
+  }
+  // running max (log2 units) and partial sums of this lane's heads 2tq, 2tq+1
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
   const int mi = lane >> 3;
+  const int h0 = 2 * tq, h1 = 2 * tq + 1;
 
   int tbase = 0;   // tiles this warp consumed in earlier batches (mbarrier phases)
   for (int e_b = e_lo; e_b < e_hi; e_b += kBatch) {
@@ -457,7 +469,8 @@ __global__ void __launch_bounds__(kThreads, 1) attend_kernel(const AttendParams 
       const uint32_t td = s_tiles[warp + i * kWarps];
       const int e0 = static_cast<int>(td & 0xffffu), cnt = static_cast<int>((td >> 16) & 0xffu);
       if (td >> 24) {
-        // ---- V-only tile (marginal entries): O_m += a' · V over 32 rows
+        // ---- V-only tile (marginal entries), 32 rows: O_m^T += V^T · a'^T.
+        // B operand: a' of head gq at tokens 2tq, 2tq+1 (+8), hi + lo bf16.
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
           float wm[4];
@@ -465,95 +478,96 @@ __global__ void __launch_bounds__(kThreads, 1) attend_kernel(const AttendParams 
           for (int u = 0; u < 4; ++u) {
             const int tok = half * 16 + (u >> 1) * 8 + 2 * tq + (u & 1);
             const uint32_t mk = tok < cnt ? smk[e0 + tok] : 0u;
-            wm[u] = (gq < G && ((mk >> (8 + gq)) & 1u)) ? sw[e0 + tok] : 0.f;
+            wm[u] = ((mk >> (8 + gq)) & 1u) ? sw[e0 + tok] : 0.f;
           }
-          uint32_t h1, l1, h3, l3;
-          split_bf16x2(wm[0], wm[1], h1, l1);
-          split_bf16x2(wm[2], wm[3], h3, l3);
+          uint32_t bh0_, bl0_, bh1_, bl1_;
+          split_bf16x2(wm[0], wm[1], bh0_, bl0_);
+          split_bf16x2(wm[2], wm[3], bh1_, bl1_);
 #pragma unroll
-          for (int t = 0; t < NT; t += 2) {
-            const int r = half * 16 + ((mi & 1) << 3) + (lane & 7);
-            const int ch = t + (mi >> 1);
-            uint32_t b0, b1, b2, b3;
-            ldsm_x4_t(smem_u32(st + r * ROWB + ((ch ^ (r & 7)) << 4)), b0, b1, b2, b3);
-            mma_bf16(o[t], 0u, h1, 0u, h3, b0, b1);
-            mma_bf16(o[t], 0u, l1, 0u, l3, b0, b1);
-            mma_bf16(o[t + 1], 0u, h1, 0u, h3, b2, b3);
-            mma_bf16(o[t + 1], 0u, l1, 0u, l3, b2, b3);
+          for (int mt = 0; mt < MT; ++mt) {
+            const int r = half * 16 + ((mi >> 1) << 3) + (lane & 7);
+            const int ch = 2 * mt + (mi & 1);
+            uint32_t a0, a1, a2, a3;
+            ldsm_x4_t(smem_u32(st + r * ROWB + ((ch ^ (r & 7)) << 4)), a0, a1, a2, a3);
+            mma_bf16(om[mt], a0, a1, a2, a3, bh0_, bh1_);
+            mma_bf16(om[mt], a0, a1, a2, a3, bl0_, bl1_);
           }
         }
         __syncwarp();
         continue;
       }
-
-      // S = Q K^T : rows = heads, cols = 16 tokens (two n8 tiles)
-      // four independent accumulation chains (even / odd k-steps) halve the
-      // dependent HMMA latency of the QK product
-      float sacc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-      float sod[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      // S^T = K · Q^T : rows = 16 tokens, columns = 8 heads (one n8 tile);
+      // lane holds tokens gq, gq+8 x heads 2tq, 2tq+1.  Four accumulation chains.
+      float sc[4][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f},
+                        {0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk) {
-        const int r = ((mi >> 1) << 3) + (lane & 7);
-        const int ch = 2 * kk + (mi & 1);
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4(smem_u32(kb + r * ROWB + ((ch ^ (r & 7)) << 4)), b0, b1, b2, b3);
-        float(&a0)[4] = (kk & 1) ? sod[0] : sacc[0];
-        float(&a1)[4] = (kk & 1) ? sod[1] : sacc[1];
-        mma_bf16(a0, qa[kk][0], 0u, qa[kk][1], 0u, b0, b1);
-        mma_bf16(a1, qa[kk][0], 0u, qa[kk][1], 0u, b2, b3);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        sacc[0][u] += sod[0][u];
-        sacc[1][u] += sod[1][u];
-      }
-      // masks / weights for this lane's head gq and tokens {2tq, 2tq+1, 8+2tq, 9+2tq}
-      float sv[4], wm[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int tok = (u >> 1) * 8 + 2 * tq + (u & 1);
-        const int e = e0 + tok;
-        const uint32_t mk = tok < cnt ? smk[e] : 0u;
-        const bool crit = gq < G && ((mk >> gq) & 1u);
-        const bool marg = gq < G && ((mk >> (8 + gq)) & 1u);
-        sv[u] = crit ? sacc[u >> 1][u & 1] * p.scale_log2 : -INFINITY;
-        wm[u] = marg ? sw[e] : 0.f;
-      }
-      float tmax = fmaxf(fmaxf(sv[0], sv[1]), fmaxf(sv[2], sv[3]));
-      tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
-      tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
-      if (tmax > m_run + kRescaleSlack) {   // raise the base (rare after the first tiles)
-        const float alpha = exp2f(m_run - tmax);   // 0 when m_run = -inf
-        l_run *= alpha;
-#pragma unroll
-        for (int t = 0; t < NT; ++t) {
-          o[t][0] *= alpha;
-          o[t][1] *= alpha;
-        }
-        m_run = tmax;
-      }
-      const float m_use = m_run == -INFINITY ? 0.f : m_run;
-      float pw[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) pw[u] = exp2f(sv[u] - m_use);
-      l_run += (pw[0] + pw[1] + pw[2] + pw[3]);
-      // A fragments (rows gq: p; rows gq+8: a'), hi + lo
-      uint32_t ah[4], al[4];
-      split_bf16x2(pw[0], pw[1], ah[0], al[0]);
-      split_bf16x2(wm[0], wm[1], ah[1], al[1]);
-      split_bf16x2(pw[2], pw[3], ah[2], al[2]);
-      split_bf16x2(wm[2], wm[3], ah[3], al[3]);
-      // O += A · V
-#pragma unroll
-      for (int t = 0; t < NT; t += 2) {
         const int r = ((mi & 1) << 3) + (lane & 7);
-        const int ch = t + (mi >> 1);
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(smem_u32(vb + r * ROWB + ((ch ^ (r & 7)) << 4)), b0, b1, b2, b3);
-        mma_bf16(o[t], ah[0], ah[1], ah[2], ah[3], b0, b1);
-        mma_bf16(o[t], al[0], al[1], al[2], al[3], b0, b1);
-        mma_bf16(o[t + 1], ah[0], ah[1], ah[2], ah[3], b2, b3);
-        mma_bf16(o[t + 1], al[0], al[1], al[2], al[3], b2, b3);
+        const int ch = 2 * kk + (mi >> 1);
+        uint32_t a0, a1, a2, a3;
+        ldsm_x4(smem_u32(kb + r * ROWB + ((ch ^ (r & 7)) << 4)), a0, a1, a2, a3);
+        mma_bf16(sc[kk & 3], a0, a1, a2, a3, qa[kk][0], qa[kk][1]);
+      }
+      float s4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) s4[u] = (sc[0][u] + sc[1][u]) + (sc[2][u] + sc[3][u]);
+      const uint32_t mkA = gq < cnt ? smk[e0 + gq] : 0u;
+      const uint32_t mkB = gq + 8 < cnt ? smk[e0 + gq + 8] : 0u;
+      const float sv0 = ((mkA >> h0) & 1u) ? s4[0] * p.scale_log2 : -INFINITY;   // tok gq,   head h0
+      const float sv1 = ((mkA >> h1) & 1u) ? s4[1] * p.scale_log2 : -INFINITY;   // tok gq,   head h1
+      const float sv2 = ((mkB >> h0) & 1u) ? s4[2] * p.scale_log2 : -INFINITY;   // tok gq+8, head h0
+      const float sv3 = ((mkB >> h1) & 1u) ? s4[3] * p.scale_log2 : -INFINITY;   // tok gq+8, head h1
+      float x0 = fmaxf(sv0, sv2), x1 = fmaxf(sv1, sv3);
+      // lazy online softmax: the base of a head is raised (with the O rescale)
+      // only when a score exceeds it by more than kRescaleSlack; one vote in
+      // the common case, the cross-lane max only when some lane needs it
+      if (__any_sync(0xffffffffu, x0 > m0 + kRescaleSlack || x1 > m1 + kRescaleSlack)) {
+#pragma unroll
+        for (int sh = 4; sh < 32; sh <<= 1) {
+          x0 = fmaxf(x0, __shfl_xor_sync(0xffffffffu, x0, sh));
+          x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, sh));
+        }
+        if (x0 > m0 + kRescaleSlack) {
+          const float al = exp2f(m0 - x0);   // 0 when m0 = -inf
+          l0 *= al;
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            oc[mt][0] *= al;
+            oc[mt][2] *= al;
+          }
+          m0 = x0;
+        }
+        if (x1 > m1 + kRescaleSlack) {
+          const float al = exp2f(m1 - x1);
+          l1 *= al;
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            oc[mt][1] *= al;
+            oc[mt][3] *= al;
+          }
+          m1 = x1;
+        }
+      }
+      const float mu0 = m0 == -INFINITY ? 0.f : m0, mu1 = m1 == -INFINITY ? 0.f : m1;
+      const float p0 = exp2f(sv0 - mu0), p1 = exp2f(sv1 - mu1);
+      const float p2 = exp2f(sv2 - mu0), p3 = exp2f(sv3 - mu1);
+      l0 += p0 + p2;
+      l1 += p1 + p3;
+      // P^T fragments (tokens x heads, hi + lo) -> B operand (tokens 2tq.., head gq)
+      uint32_t h01, l01, h23, l23;
+      split_bf16x2(p0, p1, h01, l01);
+      split_bf16x2(p2, p3, h23, l23);
+      const uint32_t bh0_ = movmatrix_t(h01), bh1_ = movmatrix_t(h23);
+      const uint32_t bl0_ = movmatrix_t(l01), bl1_ = movmatrix_t(l23);
+      // O_c^T += V^T · P^T
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int r = ((mi >> 1) << 3) + (lane & 7);
+        const int ch = 2 * mt + (mi & 1);
+        uint32_t a0, a1, a2, a3;
+        ldsm_x4_t(smem_u32(vb + r * ROWB + ((ch ^ (r & 7)) << 4)), a0, a1, a2, a3);
+        mma_bf16(oc[mt], a0, a1, a2, a3, bh0_, bh1_);
+        mma_bf16(oc[mt], a0, a1, a2, a3, bl0_, bl1_);
       }
       __syncwarp();
     }
@@ -562,25 +576,36 @@ __global__ void __launch_bounds__(kThreads, 1) attend_kernel(const AttendParams 
     __syncthreads();   // batch arrays and stages are free again
   }
   if (!q_ready) wait_and_load_q();   // empty share: still order the output writes
-  l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
-  l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
+#pragma unroll
+  for (int sh = 4; sh < 32; sh <<= 1) {
+    l0 += __shfl_xor_sync(0xffffffffu, l0, sh);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, sh);
+  }
   SKV_T(4);
 
   // ---- merge warps (fixed order)
   float* wm_s = reinterpret_cast<float*>(stages);              // [kWarps][8]
   float* wl_s = wm_s + kWarps * 8;                              // [kWarps][8]
-  float* wo_s = wl_s + kWarps * 8;                              // [kWarps][16][D]
+  float* wo_s = wl_s + kWarps * 8;                              // [kWarps][16][D]: O_c rows h, O_m rows 8+h
   {
     float* myo = wo_s + warp * 16 * D;
 #pragma unroll
-    for (int t = 0; t < NT; ++t) {
-      const int col = t * 8 + 2 * tq;
-      *reinterpret_cast<float2*>(myo + gq * D + col) = make_float2(o[t][0], o[t][1]);
-      *reinterpret_cast<float2*>(myo + (gq + 8) * D + col) = make_float2(o[t][2], o[t][3]);
+    for (int mt = 0; mt < MT; ++mt) {
+      const int d0 = 16 * mt + gq;
+      myo[h0 * D + d0] = oc[mt][0];
+      myo[h1 * D + d0] = oc[mt][1];
+      myo[h0 * D + d0 + 8] = oc[mt][2];
+      myo[h1 * D + d0 + 8] = oc[mt][3];
+      myo[(8 + h0) * D + d0] = om[mt][0];
+      myo[(8 + h1) * D + d0] = om[mt][1];
+      myo[(8 + h0) * D + d0 + 8] = om[mt][2];
+      myo[(8 + h1) * D + d0 + 8] = om[mt][3];
     }
-    if (tq == 0) {
-      wm_s[warp * 8 + gq] = m_run;
-      wl_s[warp * 8 + gq] = l_run;
+    if (gq == 0) {
+      wm_s[warp * 8 + h0] = m0;
+      wm_s[warp * 8 + h1] = m1;
+      wl_s[warp * 8 + h0] = l0;
+      wl_s[warp * 8 + h1] = l1;
     }
   }
   __syncthreads();
