@@ -52,7 +52,7 @@ __device__ __forceinline__ void lse_combine(float& m, float& s, float m2, float 
 
 template <bool kInSmem>
 __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) {
-  extern __shared__ float vals[];   // [n] row, then (kInSmem) [n] bin bytes
+  extern __shared__ __align__(16) float vals[];   // [n] row, then (kInSmem) [n] bin bytes (+16)
   __shared__ uint32_t hist[kWarps][kBins];
   __shared__ unsigned long long cand[2][kCandCap];
   __shared__ float red[4][kWarps];
@@ -67,8 +67,9 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
 
   const int r = p.layer_off[p.layer_begin] + static_cast<int>(blockIdx.x);
   if (r >= p.layer_off[p.layer_end]) return;
-  const int j = p.rows[r];
   const int b = blockIdx.y;
+
+  const int j = p.rows[r];
   const int n = p.seq_lens[b];
   const int64_t rb = static_cast<int64_t>(j) * p.batch + b;
   const float* row = p.logits + rb * p.row_stride;
@@ -86,8 +87,17 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
 
   // ---- pass 1: stage the row; (max, Σexp) over [0, n) and the ranked range
   // [min, max] over [0, N) are merged from K1's per-chunk statistics (fixed order)
-  if (kInSmem && !accrow)
-    for (int i = tid; i < n; i += kThreads) vals[i] = row[i];
+  if (kInSmem && !accrow) {
+    // all copies in flight at once (one memory round trip for the row)
+    if ((p.row_stride & 3) == 0) {
+      const int n4 = n >> 2;
+      for (int i = tid; i < n4; i += kThreads) cp_async16(smem_u32(vals + 4 * i), row + 4 * i, true);
+      for (int i = 4 * n4 + tid; i < n; i += kThreads) cp_async4(smem_u32(vals + i), row + i);
+    } else {
+      for (int i = tid; i < n; i += kThreads) cp_async4(smem_u32(vals + i), row + i);
+    }
+    cp_async_commit();
+  }
   if (warp == 0) {
     const int nch = (n + p.chunk_tokens - 1) / p.chunk_tokens;
     const float4* st = p.stats + rb * p.n_chunks;
@@ -115,6 +125,7 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
       p.counts[rb * 2 + 1] = Mc;
     }
   }
+  if (kInSmem && !accrow) cp_async_wait<0>();
   __syncthreads();
   const float lse = red[0][0] + logf(red[1][0]);
   float vlo = red[2][0], vhi = red[3][0];
@@ -149,7 +160,9 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
   if (rB == 0) return;
 
   // per-warp contiguous segments of [0, N) (index order = output order)
-  const int seg = ((N + kThreads - 1) / kThreads) * 32;
+  // (multiples of 128 positions: the shared-memory passes give each lane 4
+  // consecutive positions per step)
+  const int seg = ((N + kWarps * 128 - 1) / (kWarps * 128)) * 128;
   const int s0 = warp * seg, s1 = min(N, s0 + seg);
 
   // ---- boundaries as lexicographic thresholds (T, I)
@@ -171,12 +184,24 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
     for (int i = tid; i < kWarps * kBins; i += kThreads) (&hist[0][0])[i] = 0u;
     __syncthreads();
     uint8_t* sbin = reinterpret_cast<uint8_t*>(vals + n);
-    for (int base = s0; base < s1; base += 32) {
-      const int i = base + lane;
-      if (i < s1) {
-        const int bin = min(kBins - 1, static_cast<int>((VAL(i) - vlo) * scale));
-        if (kInSmem) sbin[i] = static_cast<uint8_t>(bin);
-        atomicAdd(&hist[warp][bin], 1u);
+    if (kInSmem) {
+      // 4 consecutive positions per lane: one 16-B load, one 4-B bin store
+      for (int base = s0 + 4 * lane; base < s1; base += 128) {
+        const float4 v4 = *reinterpret_cast<const float4*>(vals + base);
+        const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+        uint32_t packed = 0u;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int bin = min(kBins - 1, static_cast<int>((vv[k] - vlo) * scale));
+          packed |= static_cast<uint32_t>(bin & 255) << (8 * k);
+          if (base + k < s1) atomicAdd(&hist[warp][bin], 1u);
+        }
+        *reinterpret_cast<uint32_t*>(sbin + base) = packed;
+      }
+    } else {
+      for (int base = s0; base < s1; base += 32) {
+        const int i = base + lane;
+        if (i < s1) atomicAdd(&hist[warp][min(kBins - 1, static_cast<int>((VAL(i) - vlo) * scale))], 1u);
       }
     }
     __syncthreads();
@@ -219,14 +244,30 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
       if (tid < 2) s_cnt[tid] = 0;
       __syncthreads();
       const uint8_t* sbin = reinterpret_cast<const uint8_t*>(vals + n);
-      for (int i = tid; i < N; i += kThreads) {
-        const int bin = kInSmem ? static_cast<int>(sbin[i])
-                                : min(kBins - 1, static_cast<int>((VAL(i) - vlo) * scale));
-        if (bin != binA && bin != binB) continue;
+      auto take = [&](int i, int bin) {
         const unsigned long long kv =
             (static_cast<unsigned long long>(desc_key(VAL(i))) << 32) | static_cast<uint32_t>(i);
         if (bin == binA) cand[0][atomicAdd(&s_cnt[0], 1)] = kv;
         if (bin == binB && !shared) cand[1][atomicAdd(&s_cnt[1], 1)] = kv;
+      };
+      if (kInSmem) {
+        // 4 bin bytes per load; SIMD byte compares skip words without a boundary bin
+        const uint32_t pa = binA >= 0 ? static_cast<uint32_t>(binA) * 0x01010101u : 0u;
+        const uint32_t pb = static_cast<uint32_t>(binB) * 0x01010101u;
+        for (int i4 = 4 * tid; i4 < N; i4 += 4 * kThreads) {
+          const uint32_t w = *reinterpret_cast<const uint32_t*>(sbin + i4);
+          uint32_t hit = __vcmpeq4(w, pb);
+          if (binA >= 0) hit |= __vcmpeq4(w, pa);
+          if (hit == 0u) continue;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (((hit >> (8 * k)) & 0xffu) && i4 + k < N) take(i4 + k, static_cast<int>((w >> (8 * k)) & 0xffu));
+        }
+      } else {
+        for (int i = tid; i < N; i += kThreads) {
+          const int bin = min(kBins - 1, static_cast<int>((VAL(i) - vlo) * scale));
+          if (bin == binA || bin == binB) take(i, bin);
+        }
       }
       __syncthreads();
       // the pair of exact rank (rem - 1) among a bin's candidates (all distinct)
@@ -393,20 +434,55 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
   // Thresholds compared as floats: key < T  <=>  x > key_to_float(T) (with -0 == +0).
   const float XA = key_to_float(s_tk[0]), XB = key_to_float(s_tk[1]);
   const int IA = s_ti[0], IB = s_ti[1];
+  // per-lane classification of positions i..i+3 (shared-memory path)
+  auto classify4 = [&](int i, uint32_t& cm, uint32_t& mm, float (&xs)[4]) {
+    const float4 v4 = i < s1 ? *reinterpret_cast<const float4*>(vals + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    xs[0] = v4.x;
+    xs[1] = v4.y;
+    xs[2] = v4.z;
+    xs[3] = v4.w;
+    cm = 0u;
+    mm = 0u;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int ik = i + k;
+      const bool valid = ik < s1;
+      const bool isC = valid && (xs[k] > XA || (xs[k] == XA && ik <= IA));
+      const bool inB = valid && (xs[k] > XB || (xs[k] == XB && ik <= IB));
+      cm |= static_cast<uint32_t>(isC) << k;
+      mm |= static_cast<uint32_t>(inB && !isC) << k;
+    }
+  };
   if (!s_have_counts) {
     int cc = 0, cb = 0;
-    for (int base = s0; base < s1; base += 32) {
-      const int i = base + lane;
-      const bool valid = i < s1;
-      const float x = valid ? VAL(i) : -FLT_MAX;
-      const bool isC = valid && (x > XA || (x == XA && i <= IA));
-      const bool inB = valid && (x > XB || (x == XB && i <= IB));
-      cc += __popc(__ballot_sync(0xffffffffu, isC));
-      cb += __popc(__ballot_sync(0xffffffffu, inB));
-    }
-    if (lane == 0) {
-      wcnt[warp][0] = cc;
-      wcnt[warp][1] = cb - cc;
+    if (kInSmem) {
+      for (int base = s0 + 4 * lane; base < s1; base += 128) {
+        uint32_t cm, mm;
+        float xs[4];
+        classify4(base, cm, mm, xs);
+        cc += __popc(cm);
+        cb += __popc(mm);
+      }
+      cc = warp_sum_i(cc);
+      cb = warp_sum_i(cb);
+      if (lane == 0) {
+        wcnt[warp][0] = cc;
+        wcnt[warp][1] = cb;
+      }
+    } else {
+      for (int base = s0; base < s1; base += 32) {
+        const int i = base + lane;
+        const bool valid = i < s1;
+        const float x = valid ? VAL(i) : -FLT_MAX;
+        const bool isC = valid && (x > XA || (x == XA && i <= IA));
+        const bool inB = valid && (x > XB || (x == XB && i <= IB));
+        cc += __popc(__ballot_sync(0xffffffffu, isC));
+        cb += __popc(__ballot_sync(0xffffffffu, inB));
+      }
+      if (lane == 0) {
+        wcnt[warp][0] = cc;
+        wcnt[warp][1] = cb - cc;
+      }
     }
     __syncthreads();
   }
@@ -418,25 +494,57 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
   int32_t* crit = p.crit_idx + rb * p.max_crit;
   int32_t* marg = p.marg_idx + rb * p.max_marg;
   float* mw = p.marg_w + rb * p.max_marg;
-  for (int base = s0; base < s1; base += 32) {
-    const int i = base + lane;
-    const bool valid = i < s1;
-    const float x = valid ? VAL(i) : -FLT_MAX;
-    const bool isC = valid && (x > XA || (x == XA && i <= IA));
-    const bool inB = valid && (x > XB || (x == XB && i <= IB));
-    const bool isM = inB && !isC;
-    const uint32_t bc = __ballot_sync(0xffffffffu, isC);
-    const uint32_t bm = __ballot_sync(0xffffffffu, isM);
-    const int c_at = oc + __popc(bc & lt), m_at = om + __popc(bm & lt);
-    if (isC) crit[c_at] = i;
-    if (isM) {
-      marg[m_at] = i;
-      mw[m_at] = __expf((accrow ? row[i] : x) - lse);   // a' of the current step (Eq. 6)
+  if (kInSmem) {
+    // 128 positions per warp step: per-lane masks, one packed warp scan
+    for (int base0 = s0; base0 < s1; base0 += 128) {
+      const int base = base0 + 4 * lane;
+      uint32_t cm, mm;
+      float xs[4];
+      classify4(base, cm, mm, xs);
+      const int own = __popc(cm) | (__popc(mm) << 16);
+      int incl = own;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int ac = oc + ((incl - own) & 0xffff), am = om + ((incl - own) >> 16);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if ((cm >> k) & 1u) crit[ac++] = base + k;
+        if ((mm >> k) & 1u) {
+          marg[am] = base + k;
+          mw[am] = __expf((accrow ? row[base + k] : xs[k]) - lse);   // a' of the current step (Eq. 6)
+          ++am;
+        }
+      }
+      const int tot = __shfl_sync(0xffffffffu, incl, 31);
+      oc += tot & 0xffff;
+      om += tot >> 16;
     }
-    oc += __popc(bc);
-    om += __popc(bm);
+  } else {
+    for (int base = s0; base < s1; base += 32) {
+      const int i = base + lane;
+      const bool valid = i < s1;
+      const float x = valid ? VAL(i) : -FLT_MAX;
+      const bool isC = valid && (x > XA || (x == XA && i <= IA));
+      const bool inB = valid && (x > XB || (x == XB && i <= IB));
+      const bool isM = inB && !isC;
+      const uint32_t bc = __ballot_sync(0xffffffffu, isC);
+      const uint32_t bm = __ballot_sync(0xffffffffu, isM);
+      const int c_at = oc + __popc(bc & lt), m_at = om + __popc(bm & lt);
+      if (isC) crit[c_at] = i;
+      if (isM) {
+        marg[m_at] = i;
+        mw[m_at] = __expf((accrow ? row[i] : x) - lse);   // a' of the current step (Eq. 6)
+      }
+      oc += __popc(bc);
+      om += __popc(bm);
+    }
   }
 }
+
+
 }  // namespace
 
 // overlap_previous: launch with programmatic dependent launch so this grid may
@@ -456,7 +564,7 @@ cudaError_t launch_select(const SelectParams& p, int32_t max_rows, int32_t max_s
   cfg.numAttrs = overlap_previous ? 1 : 0;
   cudaError_t e;
   if (max_seq_len <= kSmemCap) {
-    cfg.dynamicSmemBytes = static_cast<size_t>(max_seq_len) * 5;
+    cfg.dynamicSmemBytes = static_cast<size_t>(max_seq_len) * 5 + 16;
     cudaFuncSetAttribute(select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(cfg.dynamicSmemBytes));
     e = cudaLaunchKernelEx(&cfg, select_kernel<true>, p);
