@@ -61,6 +61,9 @@ def _load():
                                               P, P, P, P, P, P, P]
             lib.oracle_attend.argtypes = [i32, i32, P, P, P, i32, P, P, P, i32, P, P, P,
                                           i32, i32, P, P]
+            lib.oracle_select_group.argtypes = [i32, i32, i32, P, P, P, i32, P, i32, P, P, P,
+                                                i32, i32, P, P, P, P]
+            lib.oracle_attend_group.argtypes = lib.oracle_attend.argtypes
             lib.oracle_topk.argtypes = [P, i32, i32, P]
             lib.oracle_match_heads.argtypes = [P, i32, P, i32, i32, i32, P, P]
             lib.oracle_accumulate_scores.argtypes = [P, i32, P]
@@ -210,6 +213,57 @@ def attend(layer: int, cache_layer: int, q, llm: CacheView, seq_lens, head_map,
                       _ptr(hm), _ptr(row_slot), _ptr(a), a.shape[2], _ptr(crit),
                       _ptr(marg), _ptr(counts), crit.shape[2], marg.shape[2],
                       _ptr(out), _ptr(wsum))
+    return out, wsum
+
+
+def select_group(layer: int, H: int, H_kv: int, head_map, sel: dict, seq_lens, k_crit,
+                 n_recent, k_marg, max_crit: int, max_marg: int, n_slm_heads: int):
+    """Variant f2: per-kv-group shared split of F_g = Σ_{h in group} a'_{f(layer,h)}
+    (sel from `select` over the image of the head map).  Returns a dict indexed
+    [g][b]... with "score", "crit", "marg", "counts"."""
+    lib = _load()
+    hm = _i32(head_map)
+    sl = _i32(seq_lens)
+    B = sl.shape[0]
+    row_slot = np.full(n_slm_heads, -1, np.int32)
+    for slot, j in enumerate(sel["rows"]):
+        row_slot[j] = slot
+    a = _c(sel["a"], np.float64)
+    max_n = a.shape[2]
+    kc, nrc, km = _i32(k_crit), _i32(n_recent), _i32(k_marg)
+    score = np.zeros((H_kv, B, max_n), np.float64)
+    crit = np.zeros((H_kv, B, max(max_crit, 1)), np.int32)
+    marg = np.zeros((H_kv, B, max(max_marg, 1)), np.int32)
+    counts = np.zeros((H_kv, B, 3), np.int32)
+    lib.oracle_select_group(layer, H, H_kv, _ptr(hm), _ptr(row_slot), _ptr(a), max_n, _ptr(sl),
+                            B, _ptr(kc), _ptr(nrc), _ptr(km), crit.shape[2], marg.shape[2],
+                            _ptr(score), _ptr(crit), _ptr(marg), _ptr(counts))
+    return {"score": score, "crit": crit, "marg": marg, "counts": counts}
+
+
+def attend_group(layer: int, cache_layer: int, q, llm: CacheView, seq_lens, head_map,
+                 sel: dict, gsel: dict, n_slm_heads: int):
+    """Variant f2 step 4: head h uses its group's shared sets (gsel) and its own
+    SLM row's weights (sel["a"]).  Returns (out[B,H,d], wsum[B,H])."""
+    lib = _load()
+    qq = _bf16_bits(q)
+    sl = _i32(seq_lens)
+    hm = _i32(head_map)
+    B = sl.shape[0]
+    H, d = llm.struct.num_q_heads, llm.struct.head_dim
+    row_slot = np.full(n_slm_heads, -1, np.int32)
+    for slot, j in enumerate(sel["rows"]):
+        row_slot[j] = slot
+    a = _c(sel["a"], np.float64)
+    crit = _c(gsel["crit"], np.int32)
+    marg = _c(gsel["marg"], np.int32)
+    counts = _c(gsel["counts"], np.int32)
+    out = np.zeros((B, H, d), np.float64)
+    wsum = np.zeros((B, H), np.float64)
+    lib.oracle_attend_group(layer, cache_layer, _ptr(qq), ctypes.byref(llm.struct), _ptr(sl), B,
+                            _ptr(hm), _ptr(row_slot), _ptr(a), a.shape[2], _ptr(crit),
+                            _ptr(marg), _ptr(counts), crit.shape[2], marg.shape[2],
+                            _ptr(out), _ptr(wsum))
     return out, wsum
 
 

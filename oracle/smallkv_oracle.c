@@ -23,6 +23,10 @@
  *                       O_m = A'_{f(i)}[M]·V[M], O = O_c + O_m (R13,
  *                       P:205).
  *   oracle_match_heads— Eq. 2 Jaccard of TopK sets, Eq. 3 argmax.
+ *   oracle_select_acc — variant f1: Eq. 1 running column sums.
+ *   oracle_select_group / oracle_attend_group — variant f2: one split per LLM
+ *                       KV head of the summed proxy rows (R16), per-head
+ *                       marginal weights.
  *
  * Precision: bf16 inputs are widened exactly to double; all arithmetic is
  * double.  Sorting uses the C library qsort (a library primitive).
@@ -239,6 +243,55 @@ void oracle_select_acc(const uint16_t* slm_q, const oracle_cache* slm,
  * out: [B][H][d] doubles.  Also writes the critical softmax mass check
  * wsum_out[B][H] = Σ w_k (must be 1 when C ∪ R' is non-empty), may be NULL.
  * ------------------------------------------------------------------------- */
+/* One head's compensated output: sets (crit / marg / counts) of selection row
+ * `rb_set`, marginal weights a' of SLM row `rb_w` (both [slot][b] indices). */
+static void attend_head(const oracle_cache* llm, int32_t cache_layer, const uint16_t* qh, int b,
+                        int n, int g, int64_t rb_set, int64_t rb_w, const double* a_rows,
+                        int32_t max_n, const int32_t* crit, const int32_t* marg,
+                        const int32_t* counts, int32_t max_crit, int32_t max_marg, double* o,
+                        double* wsum_out) {
+  const int d = llm->head_dim;
+  const double scale = 1.0 / sqrt((double)d);
+  const int32_t Kc = counts[rb_set * 3], Mc = counts[rb_set * 3 + 1], Rc = counts[rb_set * 3 + 2];
+  const int32_t* C = crit + rb_set * max_crit;
+  const int32_t* Mset = marg + rb_set * max_marg;
+  const double* a = a_rows + rb_w * max_n;
+  for (int t = 0; t < d; ++t) o[t] = 0.0;
+
+  /* critical ∪ recent positions */
+  const int nsel = Kc + Rc;
+  int32_t* sel = (int32_t*)malloc(sizeof(int32_t) * (nsel > 0 ? nsel : 1));
+  for (int i = 0; i < Kc; ++i) sel[i] = C[i];
+  for (int i = 0; i < Rc; ++i) sel[Kc + i] = n - Rc + i;
+  double* logit = (double*)malloc(sizeof(double) * (nsel > 0 ? nsel : 1));
+  double mx = -INFINITY;
+  for (int i = 0; i < nsel; ++i) {
+    const uint16_t* kr = cache_row(llm, llm->k, cache_layer, b, sel[i], g);
+    double dot = 0.0;
+    for (int t = 0; t < d; ++t) dot += bf16_to_double(qh[t]) * bf16_to_double(kr[t]);
+    logit[i] = dot * scale;
+    if (logit[i] > mx) mx = logit[i];
+  }
+  double z = 0.0;
+  for (int i = 0; i < nsel; ++i) z += exp(logit[i] - mx);
+  double wsum = 0.0;
+  for (int i = 0; i < nsel; ++i) {
+    const double w = exp(logit[i] - mx) / z;
+    wsum += w;
+    const uint16_t* vr = cache_row(llm, llm->v, cache_layer, b, sel[i], g);
+    for (int t = 0; t < d; ++t) o[t] += w * bf16_to_double(vr[t]);
+  }
+  /* marginal compensation: SLM weights times LLM V */
+  for (int i = 0; i < Mc; ++i) {
+    const int k = Mset[i];
+    const uint16_t* vr = cache_row(llm, llm->v, cache_layer, b, k, g);
+    for (int t = 0; t < d; ++t) o[t] += a[k] * bf16_to_double(vr[t]);
+  }
+  if (wsum_out) *wsum_out = wsum;
+  free(sel);
+  free(logit);
+}
+
 void oracle_attend(int32_t layer, int32_t cache_layer, const uint16_t* q, /* [B][H][d] */
                    const oracle_cache* llm, const int32_t* seq_lens, int32_t batch,
                    const int32_t* head_map, const int32_t* row_slot,
@@ -247,54 +300,73 @@ void oracle_attend(int32_t layer, int32_t cache_layer, const uint16_t* q, /* [B]
                    int32_t max_marg, double* out, double* wsum_out) {
   const int H = llm->num_q_heads, d = llm->head_dim;
   const int G = H / llm->num_kv_heads;
-  const double scale = 1.0 / sqrt((double)d);
 #pragma omp parallel for schedule(dynamic, 1)
   for (int64_t bh = 0; bh < (int64_t)batch * H; ++bh) {
     const int b = (int)(bh / H), h = (int)(bh % H);
-    const int n = seq_lens[b];
-    const int g = h / G;
     const int j = head_map[layer * H + h];
     const int64_t rb = (int64_t)row_slot[j] * batch + b;
-    const int32_t Kc = counts[rb * 3], Mc = counts[rb * 3 + 1], Rc = counts[rb * 3 + 2];
-    const int32_t* C = crit + rb * max_crit;
-    const int32_t* Mset = marg + rb * max_marg;
-    const double* a = a_rows + rb * max_n;
-    const uint16_t* qh = q + ((int64_t)b * H + h) * d;
-    double* o = out + bh * d;
-    for (int t = 0; t < d; ++t) o[t] = 0.0;
+    attend_head(llm, cache_layer, q + ((int64_t)b * H + h) * d, b, seq_lens[b], h / G, rb, rb,
+                a_rows, max_n, crit, marg, counts, max_crit, max_marg, out + bh * d,
+                wsum_out ? wsum_out + bh : NULL);
+  }
+}
 
-    /* critical ∪ recent positions */
-    const int nsel = Kc + Rc;
-    int32_t* sel = (int32_t*)malloc(sizeof(int32_t) * (nsel > 0 ? nsel : 1));
-    for (int i = 0; i < Kc; ++i) sel[i] = C[i];
-    for (int i = 0; i < Rc; ++i) sel[Kc + i] = n - Rc + i;
-    double* logit = (double*)malloc(sizeof(double) * (nsel > 0 ? nsel : 1));
-    double mx = -INFINITY;
-    for (int i = 0; i < nsel; ++i) {
-      const uint16_t* kr = cache_row(llm, llm->k, cache_layer, b, sel[i], g);
-      double dot = 0.0;
-      for (int t = 0; t < d; ++t) dot += bf16_to_double(qh[t]) * bf16_to_double(kr[t]);
-      logit[i] = dot * scale;
-      if (logit[i] > mx) mx = logit[i];
+/* ------------------------------------------------------------------------- *
+ * Variant f2: per-kv-group shared selection (R16).
+ * For LLM layer `layer`, kv group g (q heads g·G .. g·G+G-1) and sequence b,
+ * the group score sums the SLM proxy rows of the group's heads,
+ *     F_g[v] = Σ_{h in group g} a'_{f(layer,h)}[v]
+ * (Eq. 6's F(A'_{f(i)}) of each head i, summed over the heads that share one
+ * LLM KV head; App. A counts budgets per KV head), and ONE three-way
+ * split of F_g (oracle_split: Eq. 4 / Eq. 6, R3-R5, R7, R10) is shared by all
+ * heads of the group.  a_rows / row_slot come from oracle_select over the
+ * image of the head map.  Outputs per (g, b), gb = g·B + b:
+ *   score [H_kv][B][max_n], crit [H_kv][B][max_crit], marg [H_kv][B][max_marg],
+ *   counts [H_kv][B][3] = (K', M', R').
+ * ------------------------------------------------------------------------- */
+void oracle_select_group(int32_t layer, int32_t H, int32_t H_kv, const int32_t* head_map,
+                         const int32_t* row_slot, const double* a_rows, int32_t max_n,
+                         const int32_t* seq_lens, int32_t batch, const int32_t* k_crit,
+                         const int32_t* n_recent, const int32_t* k_marg, int32_t max_crit,
+                         int32_t max_marg, double* score, int32_t* crit, int32_t* marg,
+                         int32_t* counts) {
+  const int G = H / H_kv;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t gb = 0; gb < (int64_t)H_kv * batch; ++gb) {
+    const int g = (int)(gb / batch), b = (int)(gb % batch);
+    const int n = seq_lens[b];
+    double* F = score + gb * max_n;
+    for (int v = 0; v < n; ++v) F[v] = 0.0;
+    for (int h = 0; h < G; ++h) {
+      const int j = head_map[layer * H + g * G + h];
+      const double* a = a_rows + ((int64_t)row_slot[j] * batch + b) * max_n;
+      for (int v = 0; v < n; ++v) F[v] += a[v];
     }
-    double z = 0.0;
-    for (int i = 0; i < nsel; ++i) z += exp(logit[i] - mx);
-    double wsum = 0.0;
-    for (int i = 0; i < nsel; ++i) {
-      const double w = exp(logit[i] - mx) / z;
-      wsum += w;
-      const uint16_t* vr = cache_row(llm, llm->v, cache_layer, b, sel[i], g);
-      for (int t = 0; t < d; ++t) o[t] += w * bf16_to_double(vr[t]);
-    }
-    /* marginal compensation: SLM weights times LLM V */
-    for (int i = 0; i < Mc; ++i) {
-      const int k = Mset[i];
-      const uint16_t* vr = cache_row(llm, llm->v, cache_layer, b, k, g);
-      for (int t = 0; t < d; ++t) o[t] += a[k] * bf16_to_double(vr[t]);
-    }
-    if (wsum_out) wsum_out[bh] = wsum;
-    free(sel);
-    free(logit);
+    oracle_split(F, n, k_crit[b], n_recent[b], k_marg[b], crit + gb * max_crit,
+                 marg + gb * max_marg, counts + gb * 3);
+  }
+}
+
+/* Step 4 for variant f2: head h of group g attends over its group's shared
+ * sets (crit / marg / counts of (g, b)); its marginal weights stay its own SLM
+ * row a'_{f(layer,h)} (Eq. 6 second branch). */
+void oracle_attend_group(int32_t layer, int32_t cache_layer, const uint16_t* q, /* [B][H][d] */
+                         const oracle_cache* llm, const int32_t* seq_lens, int32_t batch,
+                         const int32_t* head_map, const int32_t* row_slot,
+                         const double* a_rows, int32_t max_n, const int32_t* crit,
+                         const int32_t* marg, const int32_t* counts, int32_t max_crit,
+                         int32_t max_marg, double* out, double* wsum_out) {
+  const int H = llm->num_q_heads, d = llm->head_dim;
+  const int G = H / llm->num_kv_heads;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t bh = 0; bh < (int64_t)batch * H; ++bh) {
+    const int b = (int)(bh / H), h = (int)(bh % H);
+    const int j = head_map[layer * H + h];
+    const int64_t rb_w = (int64_t)row_slot[j] * batch + b;
+    const int64_t rb_set = (int64_t)(h / G) * batch + b;
+    attend_head(llm, cache_layer, q + ((int64_t)b * H + h) * d, b, seq_lens[b], h / G, rb_set,
+                rb_w, a_rows, max_n, crit, marg, counts, max_crit, max_marg, out + bh * d,
+                wsum_out ? wsum_out + bh : NULL);
   }
 }
 

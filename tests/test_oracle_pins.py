@@ -376,3 +376,93 @@ def test_f1_accumulated_equals_sum_of_rows(oracle_mod):
             Kc, Mc, _ = sel["counts"][r, b]
             assert sel["crit"][r, b, :Kc].tolist() == bc
             assert sel["marg"][r, b, :Mc].tolist() == bm
+
+
+# --------------------------------------------------------------------------- variant f2
+def _group_map(p, kind):
+    """Head map for f2 pins: "uniform" = every head of an LLM kv group maps to
+    one SLM row; else the problem's own (random) map."""
+    if kind != "uniform":
+        return p
+    H, H_kv = p.cfg.llm.q_heads, p.cfg.llm.kv_heads
+    G = H // H_kv
+    n_slm = p.cfg.slm.layers * p.cfg.slm.q_heads
+    rng = random.Random(7)
+    hm = torch.empty(p.cfg.llm.layers * H, dtype=torch.int32)
+    for lg in range(p.cfg.llm.layers * H_kv):
+        hm[lg * G:(lg + 1) * G] = rng.randrange(n_slm)
+    return dataclasses.replace(p, head_map=hm)
+
+
+def _run_group(oracle, p, layer_slot=0):
+    slm, llm = _views(oracle, p)
+    rows = oracle.image_rows(p.head_map)
+    n_slm = p.cfg.slm.layers * p.cfg.slm.q_heads
+    sel = oracle.select(p.slm_q, slm, p.seq_lens, rows, p.k_crit, p.n_recent, p.k_marg,
+                        p.max_crit, p.max_marg, p.max_seq_len)
+    layer = p.llm_layer_ids[layer_slot]
+    gsel = oracle.select_group(layer, p.cfg.llm.q_heads, p.cfg.llm.kv_heads, p.head_map, sel,
+                               p.seq_lens, p.k_crit, p.n_recent, p.k_marg, p.max_crit,
+                               p.max_marg, n_slm)
+    out, wsum = oracle.attend_group(layer, layer_slot, p.llm_q[layer_slot], llm, p.seq_lens,
+                                    p.head_map, sel, gsel, n_slm)
+    return sel, gsel, out, wsum
+
+
+def test_P16_f2_uniform_group_reduces_to_default(oracle_mod):
+    """f2 with every head of a group on one SLM row: F_g = G·a' (an exact
+    power-of-two scale for G=4) ranks like a' => the default method."""
+    p = _group_map(_small(seq_lens=(150, 97, 1), budget=(30, 10, 40)), "uniform")
+    sel, gsel, out_g, wsum_g = _run_group(oracle_mod, p)
+    _, out, wsum = _run(oracle_mod, p)
+    np.testing.assert_array_equal(out_g, out)
+    np.testing.assert_array_equal(wsum_g, wsum)
+
+
+def test_P17_f2_group_split_bruteforce(oracle_mod):
+    """f2 split = Python sort of the torch-softmax rows summed over the group's
+    heads (R16: F_g = Σ_h a'_{f(h)})."""
+    p = _small(seq_lens=(150, 97, 5), budget=(30, 10, 40))
+    _, gsel, _, _ = _run_group(oracle_mod, p)
+    H, H_kv = p.cfg.llm.q_heads, p.cfg.llm.kv_heads
+    G = H // H_kv
+    layer = p.llm_layer_ids[0]
+    for g in range(H_kv):
+        for b in range(p.batch):
+            F = sum(_slm_softmax(p, int(p.head_map[layer * H + g * G + h]), b)[1] for h in range(G))
+            bc, bm, br, _ = brute_split(F.tolist(), 30, 10, 40)
+            Kc, Mc, Rc = (int(x) for x in gsel["counts"][g, b])
+            assert (Kc, Mc, Rc) == (len(bc), len(bm), len(br))
+            assert gsel["crit"][g, b, :Kc].tolist() == bc
+            assert gsel["marg"][g, b, :Mc].tolist() == bm
+
+
+def test_P18_f2_attend_shared_sets_own_weights(oracle_mod):
+    """f2 attention: M = 0 => SDPA over the group's shared C ∪ R (mask from the
+    brute-force split of F_g); K = R = 0 => Σ_{k∈M_g} a'_{f(h)}[k] V[k] with the
+    head's OWN row weights (Eq. 6 second branch)."""
+    H, H_kv = 8, 2
+    G = H // H_kv
+    for budget in ((30, 10, 0), (0, 0, 60)):
+        p = _small(seq_lens=(150, 97, 5), budget=budget)
+        _, _, out, _ = _run_group(oracle_mod, p)
+        layer = p.llm_layer_ids[0]
+        for b in range(p.batch):
+            n = int(p.seq_lens[b])
+            for g in range(H_kv):
+                F = sum(_slm_softmax(p, int(p.head_map[layer * H + g * G + h]), b)[1]
+                        for h in range(G))
+                bc, bm, br, _ = brute_split(F.tolist(), *budget)
+                K = dense_rows(p.llm, 0, b, n, g, "k")
+                V = dense_rows(p.llm, 0, b, n, g, "v")
+                for h in range(g * G, (g + 1) * G):
+                    if budget[2] == 0:
+                        mask = torch.zeros(n, dtype=torch.bool)
+                        mask[bc + br] = True
+                        ref = sdpa_fp64(p.llm_q[0, b, h], K, V, mask)
+                    else:
+                        _, a = _slm_softmax(p, int(p.head_map[layer * H + h]), b)
+                        w = torch.zeros(n, dtype=torch.float64)
+                        w[bm] = a[bm]
+                        ref = w @ V
+                    np.testing.assert_allclose(out[b, h], ref.numpy(), rtol=1e-12, atol=1e-13)
