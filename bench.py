@@ -144,7 +144,7 @@ def run_ours(args, world, rank, local):
     p, resident = build_problem(args.config, rank, world, args.shard, device)
     cfg = p.cfg
     L = cfg.llm.layers
-    step = smallkv.from_problem(p)
+    step = smallkv.from_problem(p, variant=args.variant)
     outs = torch.empty(L, p.batch, cfg.llm.q_heads, cfg.llm.head_dim, dtype=torch.float32,
                        device=device)
     plan = [(l, l % resident, p.llm_q[l % resident], outs[l]) for l in range(L)]
@@ -313,6 +313,9 @@ def run_ours(args, world, rank, local):
                             "per step)" if heads else f"batch-sharded x{world} (no collective)"),
             "budget_K_R_M": list(cfg.budget),
             "head_map": "coherent (every SLM kv-head referenced)",
+            "selection": ("f2: one split per LLM (layer, kv-group) of the summed proxy rows "
+                          "(SURVEY §8(f) f2, DESIGN.md R16)" if args.variant == "f2"
+                          else "per SLM row (Eq. 6, R1/R14)"),
             "page_size": p.llm.page_size,
             "resident_llm_layers": resident,
             "l2": "inputs larger than L2: %.2f GB touched per step vs 126 MB L2" % (bm["step"] / 1e9),
@@ -344,14 +347,14 @@ def run_ours(args, world, rank, local):
         "clocks": clocks,
     }
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(p, cfg, L)
+        line["cpu_baseline"] = cpu_baseline(p, cfg, L, variant=args.variant)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
 
 
-def cpu_baseline(p, cfg, L, target_s: float = 12.0):
+def cpu_baseline(p, cfg, L, target_s: float = 12.0, variant: str = "default"):
     """Time the oracle, as it stands, on a bounded sample of the same step:
     every sequence of the batch, the select for every SLM row the step uses,
     and the attend of as many LLM layers as fit in ~target_s seconds; the
@@ -379,8 +382,16 @@ def cpu_baseline(p, cfg, L, target_s: float = 12.0):
         sub = base if slot == 0 else cpu_layer(slot)
         _, llm_v = parity.views(sub)
         t1 = time.perf_counter()
-        oracle.attend(sub.llm_layer_ids[0], 0, sub.llm_q[0], llm_v, sub.seq_lens, sub.head_map,
-                      sel, cfg.slm.layers * cfg.slm.q_heads)
+        n_slm = cfg.slm.layers * cfg.slm.q_heads
+        if variant == "f2":
+            gsel = oracle.select_group(sub.llm_layer_ids[0], cfg.llm.q_heads, cfg.llm.kv_heads,
+                                       sub.head_map, sel, sub.seq_lens, sub.k_crit, sub.n_recent,
+                                       sub.k_marg, sub.max_crit, sub.max_marg, n_slm)
+            oracle.attend_group(sub.llm_layer_ids[0], 0, sub.llm_q[0], llm_v, sub.seq_lens,
+                                sub.head_map, sel, gsel, n_slm)
+        else:
+            oracle.attend(sub.llm_layer_ids[0], 0, sub.llm_q[0], llm_v, sub.seq_lens,
+                          sub.head_map, sel, n_slm)
         t_layers.append(time.perf_counter() - t1)
         slot += 1
         if t_sel + sum(t_layers) >= target_s:
@@ -447,6 +458,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="qwen7b")
+    ap.add_argument("--variant", choices=["default", "f2"], default="default",
+                    help="f2: per-KV-group shared selection (SURVEY §8(f) f2, DESIGN.md R16)")
     ap.add_argument("--shard", choices=["batch", "heads"], default="batch",
                     help="N>1 partition: sequences (weak scaling) or LLM kv-head groups")
     ap.add_argument("--cpu-seqs", type=int, default=4,

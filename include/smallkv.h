@@ -185,6 +185,45 @@ int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm,
                    float* acc, void* ws, size_t ws_bytes, void* stream,
                    void* aux_stream);
 
+/*
+ * Variant f2 (R16): per-LLM-KV-head shared selection.
+ * For LLM layer l, kv group g (q heads g*G .. g*G+G-1, G = H/H_kv) and
+ * sequence b, the group score sums the SLM proxy rows of the group's heads
+ * (App. A counts budgets per KV head):
+ *   F_g[v] = Σ_{h in group g} a'_{f(l,h)}[v],   a' as in smallkv_select
+ * and ONE three-way split of F_g (same clamps, recent window and
+ * lower-index tie-break as smallkv_select) is shared by all heads of the
+ * group.  The marginal weight of head h at a shared marginal position k stays
+ * its own row a'_{f(l,h)}[k] (Eq. 6 second branch).
+ * Inputs: as smallkv_select; n_llm_layers = L, llm_q_heads = H,
+ *   llm_kv_heads = H_kv (head_map has L*H entries; H % H_kv == 0, G <= 8).
+ * Outputs, indexed by group row r = l*H_kv + g:
+ *   slm_logits, slm_lse  as smallkv_select (rows in image(f)).
+ *   group_score device fp32 [L*H_kv][B][max_seq_len]   F_g[v] for v < n (fp32
+ *               sum over the group's heads in head order).
+ *   crit_idx    device int32 [L*H_kv][B][max_crit]     ascending positions.
+ *   marg_idx    device int32 [L*H_kv][B][max_marg]     ascending positions.
+ *   marg_w      device fp32 [L*H_kv][B][max_marg][8]   per-head a'_{f(l,h)}
+ *               at marg_idx, head slot h - g*G (slots >= G are 0).
+ *   counts      device int32 [L*H_kv][B][2]            (K', M') after clamping.
+ *   ws          >= smallkv_select_group_workspace_size bytes.
+ * Errors: as smallkv_select, plus H % H_kv != 0 or G > 8 (SMALLKV_ERR_SHAPE).
+ * Consumed by smallkv_plan_group / smallkv_attend(... SMALLKV_ATTEND_GROUP_SELECTION).
+ */
+size_t smallkv_select_group_workspace_size(const smallkv_cache* slm,
+                                           const smallkv_batch* batch,
+                                           const smallkv_budgets* budgets,
+                                           int32_t n_llm_layers,
+                                           int32_t llm_kv_heads);
+int smallkv_select_group(const uint16_t* slm_q, const smallkv_cache* slm,
+                         const smallkv_batch* batch, const int32_t* head_map,
+                         int32_t n_llm_layers, int32_t llm_q_heads,
+                         int32_t llm_kv_heads, const smallkv_budgets* budgets,
+                         float* slm_logits, float* slm_lse, float* group_score,
+                         int32_t* crit_idx, int32_t* marg_idx, float* marg_w,
+                         int32_t* counts, void* ws, size_t ws_bytes,
+                         void* stream);
+
 /* Bytes of the gather plan of n_llm_layers layers (0 on invalid arguments). */
 size_t smallkv_plan_size(const smallkv_cache* llm, const smallkv_batch* batch,
                          int32_t n_llm_layers);
@@ -205,6 +244,19 @@ int smallkv_plan(const smallkv_cache* llm, const smallkv_batch* batch,
                  const int32_t* crit_idx, const int32_t* marg_idx,
                  const float* marg_w, const int32_t* counts, void* plan,
                  size_t plan_bytes, void* stream);
+
+/*
+ * smallkv_plan_group — smallkv_plan for variant f2: the selection inputs are
+ * smallkv_select_group's group-indexed outputs (crit_idx / marg_idx / marg_w
+ * / counts as documented there); same plan size and buffer rules.  The plan
+ * must be consumed by smallkv_attend with SMALLKV_ATTEND_GROUP_SELECTION.
+ */
+int smallkv_plan_group(const smallkv_cache* llm, const smallkv_batch* batch,
+                       const int32_t* head_map, int32_t n_llm_layers,
+                       const smallkv_budgets* budgets, const int32_t* crit_idx,
+                       const int32_t* marg_idx, const float* marg_w,
+                       const int32_t* counts, void* plan, size_t plan_bytes,
+                       void* stream);
 
 /* Bytes of workspace smallkv_attend needs (0 on invalid arguments). */
 size_t smallkv_attend_workspace_size(const smallkv_cache* llm,
@@ -232,7 +284,8 @@ size_t smallkv_attend_workspace_size(const smallkv_cache* llm,
  *   plan        NULL, or the smallkv_plan buffer of this step (then the
  *               kernel skips its own two rounds of list / page-table loads).
  *   out         device fp32 [B][H][d].
- *   flags       0 or SMALLKV_ATTEND_OVERLAP_PROLOGUE.  The kernel is always
+ *   flags       0 or a combination of SMALLKV_ATTEND_OVERLAP_PROLOGUE and
+ *               SMALLKV_ATTEND_GROUP_SELECTION.  OVERLAP_PROLOGUE: the kernel is always
  *               launched with programmatic dependent launch: it reads q and
  *               writes out only after the previous kernel on `stream` has
  *               completed.  With the flag it may also start BEFORE that, and
@@ -245,9 +298,16 @@ size_t smallkv_attend_workspace_size(const smallkv_cache* llm,
  *   ws          device workspace, >= smallkv_attend_workspace_size bytes (the
  *               split work is merged inside thread-block clusters; no
  *               initialisation needed).
+ *               SMALLKV_ATTEND_GROUP_SELECTION (variant f2, R16): the
+ *               selection inputs are smallkv_select_group's group-indexed
+ *               outputs; every head of group g attends over the group's
+ *               shared C ∪ R' and weights the shared marginal set with its
+ *               own marg_w slot; slm_heads_total is ignored.  The plan (if
+ *               any) must come from smallkv_plan_group.
  * Errors: as smallkv_select, plus H/H_kv > 8, unknown flags (SMALLKV_ERR_SHAPE).
  */
 #define SMALLKV_ATTEND_OVERLAP_PROLOGUE 1
+#define SMALLKV_ATTEND_GROUP_SELECTION 2
 int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
                    const smallkv_cache* llm, const smallkv_batch* batch,
                    const int32_t* head_map, int32_t n_llm_layers,

@@ -117,7 +117,13 @@ __device__ void build_layout(const AttendParams& p, int layer, int b, int g, Gro
     L.rM[0] = Mc;
   }
   __syncthreads();
-  if (tid == 0) {
+  if (tid == 0 && p.group_sel) {
+    // variant f2: one shared selection row per (layer, kv-group), all heads
+    L.rj[0] = layer * p.kv_heads + g;
+    L.rhm[0] = (1u << G) - 1u;
+    L.nrows = 1;
+    L.T = L.Rc + L.rK[0] + L.rM[0];
+  } else if (tid == 0) {
     const int Kc = L.rK[0], Mc = L.rM[0];
     int nr = 0;
     for (int h = 0; h < G; ++h) {
@@ -198,7 +204,7 @@ __device__ void stage_entries(const AttendParams& p, const GroupLayout& L, int b
         mk = L.rhm[k];
       } else {
         pos = __ldg(p.marg_idx + rb * p.max_marg + (x - L.rK[k]));
-        wt = __ldg(p.marg_w + rb * p.max_marg + (x - L.rK[k]));
+        if (!p.group_sel) wt = __ldg(p.marg_w + rb * p.max_marg + (x - L.rK[k]));
         mk = L.rhm[k] << 8;
       }
     }
@@ -278,7 +284,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const AttendParams p
           mk[u] = L.rhm[k];
         } else {
           pos[u] = __ldg(p.marg_idx + rb * p.max_marg + (x - L.rK[k]));
-          wt[u] = __ldg(p.marg_w + rb * p.max_marg + (x - L.rK[k]));
+          if (!p.group_sel) wt[u] = __ldg(p.marg_w + rb * p.max_marg + (x - L.rK[k]));
           mk[u] = L.rhm[k] << 8;
         }
       }
@@ -394,15 +400,18 @@ __global__ void __launch_bounds__(kThreads, 1) attend_kernel(const AttendParams 
 
     // ---- tiles of this batch: runs of K+V entries (recent / critical) in
     // 16-row tiles, runs of V-only (marginal) entries in 32-row tiles — both
-    // fill one 8 KB stage, so the tile count tracks the bytes
+    // fill one 8 KB stage, so the tile count tracks the bytes.  Variant f2:
+    // marginal runs in 16-row tiles whose K half carries the per-head weights.
+    // Packed (first entry - e_b) | count << 16 | vonly << 24 | per-head << 25.
     if (tid == 0) {
       int nt = 0, x = 0;
+      const uint32_t mflag = p.group_sel ? (1u << 25) : (1u << 24);
       auto run = [&](int len, bool vonly) {
         const int a = max(x, e_b), z = min(x + len, e_b + E);
-        const int ts = vonly ? 2 * kTile : kTile;
+        const int ts = vonly && !p.group_sel ? 2 * kTile : kTile;
         for (int y = a; y < z; y += ts)
           s_tiles[nt++] = static_cast<uint32_t>(y - e_b) | (static_cast<uint32_t>(min(ts, z - y)) << 16) |
-                          (vonly ? (1u << 24) : 0u);
+                          (vonly ? mflag : 0u);
         x += len;
       };
       run(L.Rc, false);
@@ -424,7 +433,26 @@ __global__ void __launch_bounds__(kThreads, 1) attend_kernel(const AttendParams 
         uint8_t* st = wst + ((tbase + i) % NSTAGE) * SB;
         const uint32_t td = s_tiles[warp + i * kWarps];
         const int e0 = static_cast<int>(td & 0xffffu), cnt = static_cast<int>((td >> 16) & 0xffu);
-        if (td >> 24) {
+        if (td >> 25) {
+          // f2 marginal tile: 16 V rows in the V half, their per-head weights
+          // [16][8] fp32 (512 B) at the start of the K half
+#pragma unroll
+          for (int grp = 0; grp < kTile / 4; ++grp) {
+            const int eo = grp * 4 + (lane >> 3);
+            const bool ev = eo < cnt;
+            const uint32_t ro = ev ? soff[e0 + eo] : 0u;
+#pragma unroll
+            for (int hf = 0; hf < D / 64; ++hf) {
+              const int ch = hf * 8 + (lane & 7);
+              cp_async16(smem_u32(st + KV_BYTES + eo * ROWB + ((ch ^ (eo & 7)) << 4)), vpool + ro + ch * 8, ev);
+            }
+          }
+          const int eo = lane >> 1;
+          const int64_t m = static_cast<int64_t>(e_b + e0 + eo) - (L.Rc + L.rK[0]);
+          const float* src = p.marg_w + ((static_cast<int64_t>(L.rj[0]) * p.batch + b) * p.max_marg + m) * 8 +
+                             (lane & 1) * 4;
+          cp_async16(smem_u32(st + lane * 16), eo < cnt ? src : p.marg_w, eo < cnt);
+        } else if (td >> 24) {
           // V-only tile: 32 V rows fill the stage
 #pragma unroll
           for (int grp = 0; grp < 2 * kTile / 4; ++grp) {
@@ -468,6 +496,31 @@ __global__ void __launch_bounds__(kThreads, 1) attend_kernel(const AttendParams 
       const uint8_t* vb = st + KV_BYTES;
       const uint32_t td = s_tiles[warp + i * kWarps];
       const int e0 = static_cast<int>(td & 0xffffu), cnt = static_cast<int>((td >> 16) & 0xffu);
+      if (td >> 25) {
+        // ---- f2 marginal tile, 16 rows: O_m^T += V^T · A'^T with per-head
+        // weights a'_{f(h)} staged in the K half ([16][8], head slot gq)
+        const float* wst8 = reinterpret_cast<const float*>(st);
+        float wm[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int tok = (u >> 1) * 8 + 2 * tq + (u & 1);
+          wm[u] = tok < cnt ? wst8[tok * 8 + gq] : 0.f;
+        }
+        uint32_t bh0_, bl0_, bh1_, bl1_;
+        split_bf16x2(wm[0], wm[1], bh0_, bl0_);
+        split_bf16x2(wm[2], wm[3], bh1_, bl1_);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const int r = ((mi >> 1) << 3) + (lane & 7);
+          const int ch = 2 * mt + (mi & 1);
+          uint32_t a0, a1, a2, a3;
+          ldsm_x4_t(smem_u32(vb + r * ROWB + ((ch ^ (r & 7)) << 4)), a0, a1, a2, a3);
+          mma_bf16(om[mt], a0, a1, a2, a3, bh0_, bh1_);
+          mma_bf16(om[mt], a0, a1, a2, a3, bl0_, bl1_);
+        }
+        __syncwarp();
+        continue;
+      }
       if (td >> 24) {
         // ---- V-only tile (marginal entries), 32 rows: O_m^T += V^T · a'^T.
         // B operand: a' of head gq at tokens 2tq, 2tq+1 (+8), hi + lo bf16.

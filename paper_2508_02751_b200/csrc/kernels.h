@@ -51,9 +51,34 @@ struct SelectParams {
   float* acc;                 // f1 running column sums [l*H_s][B][row_stride] or nullptr
   int32_t n_chunks, chunk_tokens;
   int32_t batch, row_stride, max_crit, max_marg;
+  int32_t log_bins;           // histogram on log(score) (variant f2's group scores)
 };
 cudaError_t launch_select(const SelectParams& p, int32_t max_rows, int32_t max_seq_len,
                           bool overlap_previous, cudaStream_t s);
+
+// ---------------------------------------------------------------- variant f2 (R16)
+// Group score rows F_g = Σ_{h in group} a'_{f(l,h)} (+ their ranked-range
+// statistics in K1's float4 format, one chunk per row) and, after the split,
+// the per-head marginal weights of the shared marginal set.
+struct GroupParams {
+  const float* logits;        // SLM logits [l*H_s][B][row_stride] (K1)
+  const float4* stats;        // K1's per-chunk row statistics
+  int32_t n_chunks, chunk_tokens;
+  const int32_t* head_map;    // [L*H]
+  const int32_t* seq_lens;
+  const int32_t* n_recent;
+  float* slm_lse;             // [l*H_s][B][2] (m', lse') of the group's rows
+  float* score;               // [L*H_kv][B][row_stride]
+  float4* gstats;             // [L*H_kv][B] (max, 1, min_ranked, max_ranked)
+  int32_t* rows;              // identity list [L*H_kv] for the split
+  int32_t* layer_off;         // {0, L*H_kv}
+  const int32_t* counts;      // split outputs (group rows)
+  const int32_t* marg_idx;
+  float* marg_w8;             // [L*H_kv][B][max_marg][8]
+  int32_t L, H, H_kv, batch, row_stride, max_marg;
+};
+cudaError_t launch_group_score(const GroupParams& p, cudaStream_t s);
+cudaError_t launch_group_weights(const GroupParams& p, cudaStream_t s);
 
 // ---------------------------------------------------------------- K3 gather_attend (+K4)
 struct AttendParams {
@@ -79,6 +104,8 @@ struct AttendParams {
   int32_t max_chunks;         // CTAs (= cluster size) per (sequence, kv-group)
   float scale_log2;           // log2(e)/sqrt(d)
   int32_t overlap_prologue;   // SMALLKV_ATTEND_OVERLAP_PROLOGUE
+  int32_t group_sel;          // variant f2: selection rows are (layer, kv-group); marg_w is
+                              // [L*H_kv][B][max_marg][8] per-head weights
   uint8_t* plan;              // gather plan (smallkv_plan) or nullptr
 };
 cudaError_t launch_attend(const AttendParams& p, cudaStream_t s);

@@ -166,7 +166,12 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
   const int s0 = warp * seg, s1 = min(N, s0 + seg);
 
   // ---- boundaries as lexicographic thresholds (T, I)
-  const float scale = 255.99f / (vhi - vlo);
+  // Histogram coordinate: the score itself, or (variant f2's group scores —
+  // sums of probabilities, heavily skewed towards 0) its logarithm.  Either is
+  // monotone, so bins stay ordered like scores; exactness comes from the keys.
+  auto bv = [&](float v) { return p.log_bins ? logf(fmaxf(v, 1e-30f)) : v; };
+  const float blo = bv(vlo);
+  const float scale = 255.99f / (bv(vhi) - blo);
   const bool all_equal = !(vhi > vlo);
   if (tid == 0) {
     s_fallback = (!all_equal && !isfinite(scale)) ? 1 : 0;
@@ -192,7 +197,7 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
         uint32_t packed = 0u;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const int bin = min(kBins - 1, static_cast<int>((vv[k] - vlo) * scale));
+          const int bin = iclamp(static_cast<int>((bv(vv[k]) - blo) * scale), 0, kBins - 1);
           packed |= static_cast<uint32_t>(bin & 255) << (8 * k);
           if (base + k < s1) atomicAdd(&hist[warp][bin], 1u);
         }
@@ -201,7 +206,7 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
     } else {
       for (int base = s0; base < s1; base += 32) {
         const int i = base + lane;
-        if (i < s1) atomicAdd(&hist[warp][min(kBins - 1, static_cast<int>((VAL(i) - vlo) * scale))], 1u);
+        if (i < s1) atomicAdd(&hist[warp][iclamp(static_cast<int>((bv(VAL(i)) - blo) * scale), 0, kBins - 1)], 1u);
       }
     }
     __syncthreads();
@@ -265,7 +270,7 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
         }
       } else {
         for (int i = tid; i < N; i += kThreads) {
-          const int bin = min(kBins - 1, static_cast<int>((VAL(i) - vlo) * scale));
+          const int bin = iclamp(static_cast<int>((bv(VAL(i)) - blo) * scale), 0, kBins - 1);
           if (bin == binA || bin == binB) take(i, bin);
         }
       }
@@ -545,6 +550,122 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
 }
 
 
+
+// ---------------------------------------------------------------------------
+// Variant f2 (R16): group score rows and per-head marginal weights.
+constexpr int kGroupThreads = 256;
+
+// (m', lse') of SLM row j for sequence b from K1's per-chunk statistics
+__device__ __forceinline__ float2 row_lse(const GroupParams& p, int j, int b) {
+  const int n = p.seq_lens[b];
+  const int nch = (n + p.chunk_tokens - 1) / p.chunk_tokens;
+  const float4* st = p.stats + (static_cast<int64_t>(j) * p.batch + b) * p.n_chunks;
+  float m = -FLT_MAX, sum = 0.f;
+  for (int c = 0; c < nch; ++c) lse_combine(m, sum, st[c].x, st[c].y);
+  return make_float2(m, m + logf(sum));
+}
+
+// CTA = (layer*H_kv + g, b): F_g[v] = Σ_h exp(s'_{f(l,h)}[v] - lse'_{f(l,h)}) in head
+// order, plus (max, 1, min, max over the ranked range) for the split.
+__global__ void __launch_bounds__(kGroupThreads) group_score_kernel(const GroupParams p) {
+  __shared__ int s_j[8];
+  __shared__ float s_lse[8];
+  __shared__ float s_red[2][kGroupThreads / 32];
+  const int gl = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+  const int l = gl / p.H_kv, g = gl % p.H_kv, G = p.H / p.H_kv;
+  if (b == 0 && tid == 0) {
+    p.rows[gl] = gl;
+    if (gl == 0) {
+      p.layer_off[0] = 0;
+      p.layer_off[1] = p.L * p.H_kv;
+    }
+  }
+  if (tid < G) {
+    const int j = p.head_map[l * p.H + g * G + tid];
+    const float2 ml = row_lse(p, j, b);
+    s_j[tid] = j;
+    s_lse[tid] = ml.y;
+    p.slm_lse[(static_cast<int64_t>(j) * p.batch + b) * 2] = ml.x;
+    p.slm_lse[(static_cast<int64_t>(j) * p.batch + b) * 2 + 1] = ml.y;
+  }
+  __syncthreads();
+  const int n = p.seq_lens[b];
+  const int N = n - iclamp(p.n_recent[b], 0, n);
+  float* out = p.score + (static_cast<int64_t>(gl) * p.batch + b) * p.row_stride;
+  const float* rowp[8];
+#pragma unroll
+  for (int h = 0; h < 8; ++h)
+    rowp[h] = p.logits + (static_cast<int64_t>(s_j[h < G ? h : 0]) * p.batch + b) * p.row_stride;
+  float lo = FLT_MAX, hi = -FLT_MAX;
+  // 4 consecutive positions per thread and all G rows' loads in flight at once
+  for (int v0 = 4 * tid; v0 < n; v0 += 4 * kGroupThreads) {
+    float x[8][4];
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+      if (h >= G) continue;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[h][u] = v0 + u < n ? __ldg(rowp[h] + v0 + u) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int v = v0 + u;
+      if (v >= n) break;
+      float f = 0.f;
+#pragma unroll
+      for (int h = 0; h < 8; ++h)
+        if (h < G) f += __expf(x[h][u] - s_lse[h]);
+      out[v] = f;
+      if (v < N) {
+        lo = fminf(lo, f);
+        hi = fmaxf(hi, f);
+      }
+    }
+  }
+  lo = -warp_max(-lo);
+  hi = warp_max(hi);
+  if ((tid & 31) == 0) {
+    s_red[0][tid >> 5] = lo;
+    s_red[1][tid >> 5] = hi;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < kGroupThreads / 32; ++w) {
+      lo = fminf(lo, s_red[0][w]);
+      hi = fmaxf(hi, s_red[1][w]);
+    }
+    p.gstats[static_cast<int64_t>(gl) * p.batch + b] = make_float4(hi, 1.f, lo, hi);
+  }
+}
+
+// CTA = (layer*H_kv + g, b): marg_w8[m][h] = a'_{f(l,h)}[marg_idx[m]] (Eq. 6), 0 for h >= G.
+__global__ void __launch_bounds__(kGroupThreads) group_weights_kernel(const GroupParams p) {
+  __shared__ int s_j[8];
+  __shared__ float s_lse[8];
+  const int gl = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+  const int l = gl / p.H_kv, g = gl % p.H_kv, G = p.H / p.H_kv;
+  if (tid < G) {
+    const int j = p.head_map[l * p.H + g * G + tid];
+    s_j[tid] = j;
+    s_lse[tid] = p.slm_lse[(static_cast<int64_t>(j) * p.batch + b) * 2 + 1];
+  }
+  __syncthreads();
+  const int64_t gb = static_cast<int64_t>(gl) * p.batch + b;
+  const int Mc = p.counts[gb * 2 + 1];
+  // one marginal entry per thread: its position, then all G rows' logits at once
+  for (int m = tid; m < Mc; m += kGroupThreads) {
+    const int k = p.marg_idx[gb * p.max_marg + m];
+    float x[8];
+#pragma unroll
+    for (int h = 0; h < 8; ++h)
+      x[h] = h < G ? __ldg(p.logits + (static_cast<int64_t>(s_j[h]) * p.batch + b) * p.row_stride + k) : 0.f;
+    float4* dst = reinterpret_cast<float4*>(p.marg_w8 + (gb * p.max_marg + m) * 8);
+    float w[8];
+#pragma unroll
+    for (int h = 0; h < 8; ++h) w[h] = h < G ? __expf(x[h] - s_lse[h]) : 0.f;
+    dst[0] = make_float4(w[0], w[1], w[2], w[3]);
+    dst[1] = make_float4(w[4], w[5], w[6], w[7]);
+  }
+}
 }  // namespace
 
 // overlap_previous: launch with programmatic dependent launch so this grid may
@@ -572,6 +693,16 @@ cudaError_t launch_select(const SelectParams& p, int32_t max_rows, int32_t max_s
     e = cudaLaunchKernelEx(&cfg, select_kernel<false>, p);
   }
   if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_group_score(const GroupParams& p, cudaStream_t s) {
+  group_score_kernel<<<dim3(p.L * p.H_kv, p.batch), kGroupThreads, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_group_weights(const GroupParams& p, cudaStream_t s) {
+  group_weights_kernel<<<dim3(p.L * p.H_kv, p.batch), kGroupThreads, 0, s>>>(p);
   return cudaGetLastError();
 }
 

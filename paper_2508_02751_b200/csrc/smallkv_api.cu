@@ -124,6 +124,27 @@ SelectWs select_ws_layout(int32_t n_slm, int32_t n_layers, int32_t batch, int32_
   return w;
 }
 
+// smallkv_select_group: the SelectWs block, then the group rows' split inputs
+// (identity row list, layer offsets, one statistics chunk per row) and scratch
+// for the split's single-weight outputs (replaced by the per-head weights).
+struct GroupWs {
+  size_t rows, layer_off, gstats, lse, mw, total;
+};
+GroupWs group_ws_layout(const smallkv_cache* slm, const smallkv_batch* b, int32_t max_marg,
+                        int32_t n_llm_layers, int32_t llm_kv_heads) {
+  GroupWs w;
+  const size_t base =
+      select_ws_layout(slm->num_layers * slm->num_q_heads, slm->num_layers, b->batch, b->max_seq_len).total;
+  const size_t ng = static_cast<size_t>(n_llm_layers) * llm_kv_heads;
+  w.rows = base;
+  w.layer_off = w.rows + round256(ng * 4);
+  w.gstats = w.layer_off + 256;
+  w.lse = w.gstats + round256(ng * b->batch * 16);
+  w.mw = w.lse + round256(ng * b->batch * 8);
+  w.total = w.mw + round256(ng * b->batch * static_cast<size_t>(max_marg) * 4);
+  return w;
+}
+
 struct AttendWs {
   size_t total;
   int32_t ctas;
@@ -167,17 +188,26 @@ size_t smallkv_select_workspace_size(const smallkv_cache* slm, const smallkv_bat
                           batch->max_seq_len).total;
 }
 
-int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm, const smallkv_batch* batch,
-                   const int32_t* head_map, int32_t n_llm_heads, const smallkv_budgets* budgets,
-                   float* slm_logits, float* slm_lse, int32_t* crit_idx, int32_t* marg_idx,
-                   float* marg_w, int32_t* counts, float* acc, void* ws, size_t ws_bytes,
-                   void* stream, void* aux_stream) {
+}  // extern "C"
+
+namespace {
+// Shared front half of smallkv_select / smallkv_select_group: argument checks,
+// the SLM K' tensor map, the image-of-f flags (row_flags launch on `s`) and the
+// K1 / K2 parameter blocks.  ws holds the SelectWs layout at offset 0.
+struct ScoringSetup {
+  CUtensorMap map;
+  skv::SlmScoreParams sp;
+  skv::SelectParams se;
+};
+int setup_scoring(const uint16_t* slm_q, const smallkv_cache* slm, const smallkv_batch* batch,
+                  const int32_t* head_map, int32_t n_llm_heads, const smallkv_budgets* budgets,
+                  float* slm_logits, float* slm_lse, void* ws, size_t ws_bytes, size_t ws_need,
+                  cudaStream_t s, ScoringSetup& S) {
   int rc;
   if ((rc = check_cache(slm, false, "slm")) != SMALLKV_OK) return rc;
   if ((rc = check_batch(batch, slm)) != SMALLKV_OK) return rc;
   if ((rc = check_budgets(budgets)) != SMALLKV_OK) return rc;
-  if (!slm_q || !head_map || !slm_logits || !slm_lse || !crit_idx || !marg_idx || !marg_w ||
-      !counts)
+  if (!slm_q || !head_map || !slm_logits || !slm_lse)
     return fail(SMALLKV_ERR_NULL, "smallkv_select: NULL input/output pointer");
   if (n_llm_heads < 1) return fail(SMALLKV_ERR_SHAPE, "n_llm_heads must be >= 1");
   const int G_s = slm->num_q_heads / slm->num_kv_heads;
@@ -194,13 +224,12 @@ int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm, const smallk
                 static_cast<long long>(rows_total));
   if (!aligned(slm_q, 4)) return fail(SMALLKV_ERR_ALIGN, "slm_q must be 4-byte aligned");
   const SelectWs L = select_ws_layout(n_slm, slm->num_layers, batch->batch, batch->max_seq_len);
-  if (!ws || ws_bytes < L.total)
-    return fail(SMALLKV_ERR_WORKSPACE, "select workspace %zu < %zu bytes", ws_bytes, L.total);
+  if (!ws || ws_bytes < ws_need)
+    return fail(SMALLKV_ERR_WORKSPACE, "select workspace %zu < %zu bytes", ws_bytes, ws_need);
   if ((rc = check_device()) != SMALLKV_OK) return rc;
 
   auto fn = encode_fn();
   if (!fn) return fail(SMALLKV_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  CUtensorMap map;
   const int d = slm->head_dim;
   const int box_rows = slm->page_size < 64 ? slm->page_size : 64;
   const bool swz = slm->page_size >= 8;
@@ -208,13 +237,12 @@ int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm, const smallk
   cuuint64_t gstride[1] = {static_cast<cuuint64_t>(d) * 2};
   cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
-  CUresult cr = fn(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(slm->k), gdim,
+  CUresult cr = fn(&S.map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(slm->k), gdim,
                    gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return fail(SMALLKV_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", cr);
 
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
   uint8_t* wsb = static_cast<uint8_t*>(ws);
   uint8_t* flags = wsb + L.flags;
   int32_t* rows = reinterpret_cast<int32_t*>(wsb + L.rows);
@@ -224,7 +252,8 @@ int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm, const smallk
                                         rows, nrows, layer_off, s);
   if (e != cudaSuccess) return cuda_fail(e, "row_flags launch");
 
-  skv::SlmScoreParams sp;
+  skv::SlmScoreParams& sp = S.sp;
+  sp = skv::SlmScoreParams{};
   sp.q = slm_q;
   sp.block_table = slm->block_table;
   sp.seq_lens = batch->seq_lens;
@@ -246,7 +275,8 @@ int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm, const smallk
   sp.box_rows = box_rows;
   sp.swz = swz ? 7u : 0u;
   sp.scale = 1.0f / std::sqrt(static_cast<float>(d));
-  skv::SelectParams se;
+  skv::SelectParams& se = S.se;
+  se = skv::SelectParams{};
   se.logits = slm_logits;
   se.seq_lens = batch->seq_lens;
   se.rows = rows;
@@ -255,18 +285,45 @@ int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm, const smallk
   se.n_recent = budgets->n_recent;
   se.k_marg = budgets->k_marg;
   se.lse = slm_lse;
-  se.crit_idx = crit_idx;
-  se.marg_idx = marg_idx;
-  se.marg_w = marg_w;
-  se.counts = counts;
   se.batch = batch->batch;
   se.row_stride = batch->max_seq_len;
   se.max_crit = budgets->max_crit;
   se.max_marg = budgets->max_marg;
   se.stats = sp.stats;
-  se.acc = acc;
   se.n_chunks = sp.n_chunks;
   se.chunk_tokens = kScoreChunk;
+  return SMALLKV_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm, const smallkv_batch* batch,
+                   const int32_t* head_map, int32_t n_llm_heads, const smallkv_budgets* budgets,
+                   float* slm_logits, float* slm_lse, int32_t* crit_idx, int32_t* marg_idx,
+                   float* marg_w, int32_t* counts, float* acc, void* ws, size_t ws_bytes,
+                   void* stream, void* aux_stream) {
+  int rc0;
+  if ((rc0 = check_cache(slm, false, "slm")) != SMALLKV_OK) return rc0;
+  if ((rc0 = check_batch(batch, slm)) != SMALLKV_OK) return rc0;
+  if ((rc0 = check_budgets(budgets)) != SMALLKV_OK) return rc0;
+  if (!crit_idx || !marg_idx || !marg_w || !counts)
+    return fail(SMALLKV_ERR_NULL, "smallkv_select: NULL input/output pointer");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ScoringSetup S;
+  const size_t need = smallkv_select_workspace_size(slm, batch, n_llm_heads > 0 ? n_llm_heads : 1);
+  int rc = setup_scoring(slm_q, slm, batch, head_map, n_llm_heads, budgets, slm_logits, slm_lse,
+                         ws, ws_bytes, need, s, S);
+  if (rc != SMALLKV_OK) return rc;
+  cudaError_t e;
+  skv::SlmScoreParams& sp = S.sp;
+  skv::SelectParams& se = S.se;
+  const CUtensorMap& map = S.map;
+  se.crit_idx = crit_idx;
+  se.marg_idx = marg_idx;
+  se.marg_w = marg_w;
+  se.counts = counts;
+  se.acc = acc;
   // Score the SLM layers in chunks.  With an auxiliary stream the split of
   // chunk i (ALU-bound K2) runs on it concurrently with the scoring of chunk
   // i+1 (HBM-bound K1) on the main stream — the paper's "update KV cache in
@@ -322,6 +379,98 @@ int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm, const smallk
   }
   for (int i = 0; i < nev; ++i) cudaEventDestroy(evs[i]);
   return rc2;
+}
+
+size_t smallkv_select_group_workspace_size(const smallkv_cache* slm, const smallkv_batch* batch,
+                                           const smallkv_budgets* budgets, int32_t n_llm_layers,
+                                           int32_t llm_kv_heads) {
+  if (!slm || !batch || !budgets || n_llm_layers < 1 || llm_kv_heads < 1 || batch->batch < 1 ||
+      batch->max_seq_len < 1 || budgets->max_marg < 1)
+    return 0;
+  return group_ws_layout(slm, batch, budgets->max_marg, n_llm_layers, llm_kv_heads).total;
+}
+
+int smallkv_select_group(const uint16_t* slm_q, const smallkv_cache* slm, const smallkv_batch* batch,
+                         const int32_t* head_map, int32_t n_llm_layers, int32_t llm_q_heads,
+                         int32_t llm_kv_heads, const smallkv_budgets* budgets, float* slm_logits,
+                         float* slm_lse, float* group_score, int32_t* crit_idx, int32_t* marg_idx,
+                         float* marg_w, int32_t* counts, void* ws, size_t ws_bytes, void* stream) {
+  int rc0;
+  if ((rc0 = check_cache(slm, false, "slm")) != SMALLKV_OK) return rc0;
+  if ((rc0 = check_batch(batch, slm)) != SMALLKV_OK) return rc0;
+  if ((rc0 = check_budgets(budgets)) != SMALLKV_OK) return rc0;
+  if (!group_score || !crit_idx || !marg_idx || !marg_w || !counts)
+    return fail(SMALLKV_ERR_NULL, "smallkv_select_group: NULL output pointer");
+  if (n_llm_layers < 1 || llm_q_heads < 1 || llm_kv_heads < 1 || llm_q_heads % llm_kv_heads != 0)
+    return fail(SMALLKV_ERR_SHAPE, "LLM layers/heads (%d, %d, %d) invalid", n_llm_layers, llm_q_heads,
+                llm_kv_heads);
+  if (llm_q_heads / llm_kv_heads > 8)
+    return fail(SMALLKV_ERR_SHAPE, "LLM GQA group %d > 8 not supported", llm_q_heads / llm_kv_heads);
+  if (static_cast<int64_t>(n_llm_layers) * llm_kv_heads > 65535)
+    return fail(SMALLKV_ERR_SHAPE, "L*H_kv > 65535");
+  if (!aligned(marg_w, 16)) return fail(SMALLKV_ERR_ALIGN, "marg_w must be 16-byte aligned");
+  const size_t need =
+      smallkv_select_group_workspace_size(slm, batch, budgets, n_llm_layers, llm_kv_heads);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ScoringSetup S;
+  const int32_t n_llm_heads = n_llm_layers * llm_q_heads;
+  int rc = setup_scoring(slm_q, slm, batch, head_map, n_llm_heads, budgets, slm_logits, slm_lse, ws,
+                         ws_bytes, need, s, S);
+  if (rc != SMALLKV_OK) return rc;
+  // K1 over all SLM layers
+  S.sp.layer_begin = 0;
+  S.sp.layer_end = slm->num_layers;
+  cudaError_t e = skv::launch_slm_score(S.sp, S.map, batch->max_seq_len, s);
+  if (e != cudaSuccess) return cuda_fail(e, "slm_score launch");
+  // group score rows
+  const GroupWs W = group_ws_layout(slm, batch, budgets->max_marg, n_llm_layers, llm_kv_heads);
+  uint8_t* wsb = static_cast<uint8_t*>(ws);
+  skv::GroupParams gp{};
+  gp.logits = slm_logits;
+  gp.stats = S.sp.stats;
+  gp.n_chunks = S.sp.n_chunks;
+  gp.chunk_tokens = S.sp.chunk_tokens;
+  gp.head_map = head_map;
+  gp.seq_lens = batch->seq_lens;
+  gp.n_recent = budgets->n_recent;
+  gp.slm_lse = slm_lse;
+  gp.score = group_score;
+  gp.gstats = reinterpret_cast<float4*>(wsb + W.gstats);
+  gp.rows = reinterpret_cast<int32_t*>(wsb + W.rows);
+  gp.layer_off = reinterpret_cast<int32_t*>(wsb + W.layer_off);
+  gp.counts = counts;
+  gp.marg_idx = marg_idx;
+  gp.marg_w8 = marg_w;
+  gp.L = n_llm_layers;
+  gp.H = llm_q_heads;
+  gp.H_kv = llm_kv_heads;
+  gp.batch = batch->batch;
+  gp.row_stride = batch->max_seq_len;
+  gp.max_marg = budgets->max_marg;
+  if ((e = skv::launch_group_score(gp, s)) != cudaSuccess) return cuda_fail(e, "group_score launch");
+  // the split (K2) on the group rows: ranked by F_g; its single-weight outputs
+  // go to scratch and are replaced by the per-head weights below
+  skv::SelectParams se = S.se;
+  se.logits = group_score;
+  se.rows = gp.rows;
+  se.layer_off = gp.layer_off;
+  se.layer_begin = 0;
+  se.layer_end = 1;
+  se.lse = reinterpret_cast<float*>(wsb + W.lse);
+  se.crit_idx = crit_idx;
+  se.marg_idx = marg_idx;
+  se.marg_w = reinterpret_cast<float*>(wsb + W.mw);
+  se.counts = counts;
+  se.stats = gp.gstats;
+  se.acc = nullptr;
+  se.n_chunks = 1;
+  se.chunk_tokens = batch->max_seq_len;
+  se.log_bins = 1;
+  if ((e = skv::launch_select(se, n_llm_layers * llm_kv_heads, batch->max_seq_len, false, s)) !=
+      cudaSuccess)
+    return cuda_fail(e, "select launch");
+  if ((e = skv::launch_group_weights(gp, s)) != cudaSuccess) return cuda_fail(e, "group_weights launch");
+  return SMALLKV_OK;
 }
 
 size_t smallkv_attend_workspace_size(const smallkv_cache* llm, const smallkv_batch* batch) {
@@ -407,6 +556,28 @@ int smallkv_plan(const smallkv_cache* llm, const smallkv_batch* batch, const int
   return SMALLKV_OK;
 }
 
+int smallkv_plan_group(const smallkv_cache* llm, const smallkv_batch* batch, const int32_t* head_map,
+                       int32_t n_llm_layers, const smallkv_budgets* budgets, const int32_t* crit_idx,
+                       const int32_t* marg_idx, const float* marg_w, const int32_t* counts, void* plan,
+                       size_t plan_bytes, void* stream) {
+  skv::AttendParams ap;
+  int rc = fill_attend_params(ap, llm, batch, head_map, n_llm_layers, 1, budgets, crit_idx, marg_idx,
+                              marg_w, counts);
+  if (rc != SMALLKV_OK) return rc;
+  const size_t need = smallkv_plan_size(llm, batch, n_llm_layers);
+  if (!plan || plan_bytes < need)
+    return fail(SMALLKV_ERR_WORKSPACE, "plan buffer %zu < %zu bytes", plan_bytes, need);
+  if (!aligned(plan, 16)) return fail(SMALLKV_ERR_ALIGN, "plan must be 16-byte aligned");
+  if (static_cast<int64_t>(n_llm_layers) * batch->batch > 65535)
+    return fail(SMALLKV_ERR_SHAPE, "L*B > 65535");   // plan grid.y
+  if ((rc = check_device()) != SMALLKV_OK) return rc;
+  ap.plan = static_cast<uint8_t*>(plan);
+  ap.group_sel = 1;
+  cudaError_t e = skv::launch_plan(ap, n_llm_layers, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "plan launch");
+  return SMALLKV_OK;
+}
+
 int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
                    const smallkv_cache* llm, const smallkv_batch* batch, const int32_t* head_map,
                    int32_t n_llm_layers, int32_t slm_heads_total, const smallkv_budgets* budgets,
@@ -423,8 +594,10 @@ int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
   if (cache_layer < 0 || cache_layer >= llm->num_layers)
     return fail(SMALLKV_ERR_SHAPE, "cache_layer %d outside [0,%d)", cache_layer,
                 llm->num_layers);
-  if (flags & ~SMALLKV_ATTEND_OVERLAP_PROLOGUE)
+  if (flags & ~(SMALLKV_ATTEND_OVERLAP_PROLOGUE | SMALLKV_ATTEND_GROUP_SELECTION))
     return fail(SMALLKV_ERR_SHAPE, "unknown smallkv_attend flags 0x%x", flags);
+  if ((flags & SMALLKV_ATTEND_GROUP_SELECTION) && !aligned(marg_w, 16))
+    return fail(SMALLKV_ERR_ALIGN, "group selection: marg_w must be 16-byte aligned");
   if (!aligned(q, 4) || !aligned(out, 16) || (plan && !aligned(plan, 16)))
     return fail(SMALLKV_ERR_ALIGN, "q must be 4-byte, out and plan 16-byte aligned");
   const AttendWs L = attend_ws_layout(llm, batch);
@@ -437,6 +610,7 @@ int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
   ap.layer_offset = static_cast<int64_t>(cache_layer) * llm->num_pages * llm->num_kv_heads *
                     llm->page_size * llm->head_dim;
   ap.overlap_prologue = (flags & SMALLKV_ATTEND_OVERLAP_PROLOGUE) ? 1 : 0;
+  ap.group_sel = (flags & SMALLKV_ATTEND_GROUP_SELECTION) ? 1 : 0;
   ap.plan = const_cast<uint8_t*>(static_cast<const uint8_t*>(plan));
   cudaError_t e = skv::launch_attend(ap, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "attend launch");

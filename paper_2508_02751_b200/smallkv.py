@@ -22,13 +22,16 @@ _lock = threading.Lock()
 _lib = None
 
 ATTEND_OVERLAP_PROLOGUE = 1   # include/smallkv.h SMALLKV_ATTEND_OVERLAP_PROLOGUE
+ATTEND_GROUP_SELECTION = 2    # include/smallkv.h SMALLKV_ATTEND_GROUP_SELECTION (variant f2)
 
 STATUS = {0: "OK", 1: "ERR_NULL", 2: "ERR_SHAPE", 3: "ERR_ALIGN", 4: "ERR_WORKSPACE",
           5: "ERR_DEVICE", 6: "ERR_CUDA", 7: "ERR_UNSUPPORTED"}
 
 # exported symbols, in the order include/smallkv.h declares them
 EXPORTS = ("smallkv_last_error", "smallkv_version", "smallkv_budget_from_tau",
-           "smallkv_select_workspace_size", "smallkv_select", "smallkv_plan_size", "smallkv_plan",
+           "smallkv_select_workspace_size", "smallkv_select",
+           "smallkv_select_group_workspace_size", "smallkv_select_group",
+           "smallkv_plan_size", "smallkv_plan", "smallkv_plan_group",
            "smallkv_attend_workspace_size", "smallkv_attend", "smallkv_match_heads_workspace_size", "smallkv_match_heads",
            "smallkv_workspace_init")
 
@@ -76,6 +79,11 @@ def load(path: Optional[str] = None):
         lib.smallkv_select_workspace_size.argtypes = [P, P, i32]
         lib.smallkv_select_workspace_size.restype = sz
         lib.smallkv_select.argtypes = [P, P, P, P, i32, P, P, P, P, P, P, P, P, P, sz, P, P]
+        lib.smallkv_select_group_workspace_size.argtypes = [P, P, P, i32, i32]
+        lib.smallkv_select_group_workspace_size.restype = sz
+        lib.smallkv_select_group.argtypes = [P, P, P, P, i32, i32, i32, P, P, P, P, P, P, P, P,
+                                             P, sz, P]
+        lib.smallkv_plan_group.argtypes = [P, P, P, i32, P, P, P, P, P, P, sz, P]
         lib.smallkv_attend_workspace_size.argtypes = [P, P]
         lib.smallkv_attend_workspace_size.restype = sz
         lib.smallkv_attend.argtypes = [i32, i32, P, P, P, P, i32, i32, P, P, P, P, P, P, P, i32,
@@ -168,7 +176,11 @@ class DecodeStep:
                  llm_block_table, llm_q_heads: int, llm_layers: int, seq_lens: torch.Tensor,
                  max_seq_len: int, head_map: torch.Tensor, k_crit, n_recent, k_marg,
                  max_crit: int, max_marg: int, use_plan: bool = True,
-                 overlap_select: bool = False):
+                 overlap_select: bool = False, variant: str = "default"):
+        """variant: "default" (one split per SLM row) or "f2" (one split
+        per LLM (layer, kv-group) of the summed proxy rows, R16)."""
+        assert variant in ("default", "f2")
+        self.variant = variant
         self.lib = load()
         dev = seq_lens.device
         self._keep = (slm_k, slm_block_table, llm_k, llm_v, llm_block_table, seq_lens, head_map,
@@ -203,6 +215,22 @@ class DecodeStep:
                                             llm_layers)
         self.plan_buf = torch.empty(max(plan_b, 16), dtype=torch.uint8, device=dev) if use_plan else None
         self.planned = False
+        if variant == "f2":
+            H_kv = self.llm.num_kv_heads
+            ng = llm_layers * H_kv
+            self.gout = SelectOut(
+                logits=torch.zeros(ng, B, n, dtype=f32, device=dev),          # group score F_g
+                lse=self.out.lse,
+                crit=torch.zeros(ng, B, max_crit, dtype=i32, device=dev),
+                marg=torch.zeros(ng, B, max_marg, dtype=i32, device=dev),
+                marg_w=torch.zeros(ng, B, max_marg, 8, dtype=f32, device=dev),
+                counts=torch.zeros(ng, B, 2, dtype=i32, device=dev))
+            ws_g = self.lib.smallkv_select_group_workspace_size(
+                ctypes.byref(self.slm), ctypes.byref(self.batch), ctypes.byref(self.budgets),
+                llm_layers, H_kv)
+            if ws_g == 0:
+                raise SmallKVError("smallkv_select_group_workspace_size", 2, "invalid dimensions")
+            self.ws_select = torch.zeros(ws_g, dtype=torch.uint8, device=dev)
         self.aux_stream = torch.cuda.Stream(device=dev) if overlap_select else None
 
     def select(self, slm_q: torch.Tensor, stream=None, acc: Optional[torch.Tensor] = None):
@@ -213,6 +241,9 @@ class DecodeStep:
         if acc is not None:
             assert acc.dtype == torch.float32 and acc.is_contiguous()
             assert acc.shape == self.out.logits.shape
+        if self.variant == "f2":
+            assert acc is None, "f1 accumulation is not combined with f2"
+            return self._select_group(slm_q, stream)
         o = self.out
         aux = self.aux_stream.cuda_stream if self.aux_stream is not None else None
         rc = self.lib.smallkv_select(
@@ -233,24 +264,48 @@ class DecodeStep:
             self.planned = True
         return o
 
+    def _select_group(self, slm_q: torch.Tensor, stream=None):
+        """Variant f2: smallkv_select_group, then smallkv_plan_group."""
+        o, g = self.out, self.gout
+        rc = self.lib.smallkv_select_group(
+            slm_q.data_ptr(), ctypes.byref(self.slm), ctypes.byref(self.batch),
+            self.head_map.data_ptr(), self.llm_layers, self.llm.num_q_heads,
+            self.llm.num_kv_heads, ctypes.byref(self.budgets), o.logits.data_ptr(),
+            o.lse.data_ptr(), g.logits.data_ptr(), g.crit.data_ptr(), g.marg.data_ptr(),
+            g.marg_w.data_ptr(), g.counts.data_ptr(), self.ws_select.data_ptr(),
+            self.ws_select.numel(), _stream(stream))
+        _check("smallkv_select_group", rc)
+        self.planned = False
+        if self.plan_buf is not None:
+            rc = self.lib.smallkv_plan_group(
+                ctypes.byref(self.llm), ctypes.byref(self.batch), self.head_map.data_ptr(),
+                self.llm_layers, ctypes.byref(self.budgets), g.crit.data_ptr(),
+                g.marg.data_ptr(), g.marg_w.data_ptr(), g.counts.data_ptr(),
+                self.plan_buf.data_ptr(), self.plan_buf.numel(), _stream(stream))
+            _check("smallkv_plan_group", rc)
+            self.planned = True
+        return g
+
     def attend(self, llm_layer: int, cache_layer: int, q: torch.Tensor, out: torch.Tensor,
                stream=None, overlap_prologue: bool = False):
         assert q.dtype == torch.bfloat16 and q.is_contiguous()
         assert out.dtype == torch.float32 and out.is_contiguous()
-        o = self.out
+        group = self.variant == "f2"
+        o = self.gout if group else self.out
         rc = self.lib.smallkv_attend(
             int(llm_layer), int(cache_layer), q.data_ptr(), ctypes.byref(self.llm),
             ctypes.byref(self.batch), self.head_map.data_ptr(), self.llm_layers, self.n_slm,
             ctypes.byref(self.budgets), o.crit.data_ptr(), o.marg.data_ptr(),
             o.marg_w.data_ptr(), o.counts.data_ptr(),
             self.plan_buf.data_ptr() if self.planned else None, out.data_ptr(),
-            ATTEND_OVERLAP_PROLOGUE if overlap_prologue else 0,
+            (ATTEND_OVERLAP_PROLOGUE if overlap_prologue else 0)
+            | (ATTEND_GROUP_SELECTION if group else 0),
             self.ws_attend.data_ptr(), self.ws_attend.numel(), _stream(stream))
         _check("smallkv_attend", rc)
         return out
 
 
-def from_problem(p, use_plan: bool = True) -> DecodeStep:
+def from_problem(p, use_plan: bool = True, variant: str = "default") -> DecodeStep:
     """DecodeStep for a smallkv_synth.Problem already on the GPU."""
     return DecodeStep(slm_k=p.slm.k, slm_block_table=p.slm.block_table,
                       slm_q_heads=p.cfg.slm.q_heads, llm_k=p.llm.k, llm_v=p.llm.v,
@@ -258,7 +313,7 @@ def from_problem(p, use_plan: bool = True) -> DecodeStep:
                       llm_layers=p.cfg.llm.layers, seq_lens=p.seq_lens,
                       max_seq_len=p.max_seq_len, head_map=p.head_map, k_crit=p.k_crit,
                       n_recent=p.n_recent, k_marg=p.k_marg, max_crit=p.max_crit,
-                      max_marg=p.max_marg, use_plan=use_plan)
+                      max_marg=p.max_marg, use_plan=use_plan, variant=variant)
 
 
 def match_heads(llm_F: torch.Tensor, slm_F: torch.Tensor, k_match: int, stream=None):
@@ -340,5 +395,6 @@ class DecodeGraph:
         # attend kernel per layer
         nl = self.step.slm.num_layers
         chunks = min(4, nl) if self.step.aux_stream is not None else 1
-        return (1 + 2 * chunks + (1 if self.step.plan_buf is not None else 0)
+        sel = 2 * chunks if self.step.variant == "default" else 4   # f2: + group score, weights
+        return (1 + sel + (1 if self.step.plan_buf is not None else 0)
                 + len(self.plan))

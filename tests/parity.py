@@ -148,3 +148,82 @@ def run_gpu_step(p, step=None, layers=None):
         outs.append(out)
     torch.cuda.synchronize()
     return step, sel, outs
+
+
+# --------------------------------------------------------------------------- variant f2
+def compare_group(p, gpu, sel, layer_slot, out_gpu=None, llm_view=None):
+    """Variant f2 (R16): the GPU's group selection of LLM layer
+    p.llm_layer_ids[layer_slot] (smallkv_select_group outputs `gpu`) against
+    oracle_select_group, the per-head marginal weights against the oracle's
+    rows a'_{f(h)}, and (if out_gpu is given) the attention output against
+    oracle_attend_group evaluated on the GPU's verified sets."""
+    H, H_kv = p.cfg.llm.q_heads, p.cfg.llm.kv_heads
+    G = H // H_kv
+    n_slm = p.cfg.slm.layers * p.cfg.slm.q_heads
+    layer = p.llm_layer_ids[layer_slot]
+    gsel = oracle.select_group(layer, H, H_kv, p.head_map, sel, p.seq_lens, p.k_crit, p.n_recent,
+                               p.k_marg, p.max_crit, p.max_marg, n_slm)
+    slot_of = {int(j): r for r, j in enumerate(sel["rows"])}
+    hm = p.head_map.cpu().numpy()
+    score = gpu.logits.cpu().double().numpy()
+    crit = gpu.crit.cpu().numpy()
+    marg = gpu.marg.cpu().numpy()
+    mw8 = gpu.marg_w.cpu().double().numpy()
+    cnt = gpu.counts.cpu().numpy()
+    rep = {"max_score_err": 0.0, "flips": 0, "exempt_tokens": 0, "max_margw_rel": 0.0,
+           "groups_checked": 0}
+    g_crit = np.zeros_like(gsel["crit"])
+    g_marg = np.zeros_like(gsel["marg"])
+    for g in range(H_kv):
+        gl = layer * H_kv + g
+        for b in range(p.batch):
+            n = int(p.seq_lens[b])
+            F = gsel["score"][g, b, :n]
+            Kc, Mc, Rc = (int(x) for x in gsel["counts"][g, b])
+            err = np.abs(score[gl, b, :n] - F).max() if n else 0.0
+            rep["max_score_err"] = max(rep["max_score_err"], float(err))
+            assert err <= 1e-5 * max(1.0, float(F.max())), f"group score {gl} seq {b}: {err}"
+            assert cnt[gl, b, 0] == Kc and cnt[gl, b, 1] == Mc, (gl, b, cnt[gl, b], Kc, Mc)
+            gC, gM = crit[gl, b, :Kc], marg[gl, b, :Mc]
+            assert np.all(np.diff(gC) > 0) and np.all(np.diff(gM) > 0), "lists not ascending"
+            oC = set(gsel["crit"][g, b, :Kc].tolist())
+            oM = set(gsel["marg"][g, b, :Mc].tolist())
+            order = np.argsort(-F[: n - Rc], kind="stable")
+            bounds = [F[order[k - 1]] for k in (Kc, Kc + Mc) if 0 < k <= n - Rc]
+            exempt = np.zeros(n, bool)
+            for th in bounds:
+                exempt |= np.abs(F - th) < SET_BAND * max(1.0, abs(th))
+            exempt[n - Rc:] = False
+            ex = set(np.nonzero(exempt)[0].tolist())
+            rep["exempt_tokens"] += len(ex)
+            assert set(gC.tolist()) - ex == oC - ex, f"f2 critical set mismatch {gl} seq {b}"
+            assert set(gM.tolist()) - ex == oM - ex, f"f2 marginal set mismatch {gl} seq {b}"
+            flipped = (set(gC.tolist()) ^ oC) | (set(gM.tolist()) ^ oM)
+            if flipped:
+                gap = max(min(abs(F[v] - t) / max(1.0, abs(t)) for t in bounds) for v in flipped)
+                rep["flips"] += len(flipped)
+                assert gap <= FLIP_LOGIT_BAND, f"f2 flip {gap} away from a boundary {gl} seq {b}"
+            assert not (set(gC.tolist()) & set(gM.tolist()))
+            for m in range(Mc):
+                for h in range(8):
+                    w = mw8[gl, b, m, h]
+                    if h >= G:
+                        assert w == 0.0
+                        continue
+                    j = int(hm[layer * H + g * G + h])
+                    ref = sel["a"][slot_of[j], b, gM[m]]
+                    rel = abs(w - ref) / max(ref, 1e-300)
+                    rep["max_margw_rel"] = max(rep["max_margw_rel"], float(rel))
+                    assert rel <= 1e-4, f"f2 marg_w {gl} seq {b} m {m} h {h}: {rel}"
+            g_crit[g, b, :Kc] = gC
+            g_marg[g, b, :Mc] = gM
+            rep["groups_checked"] += 1
+    if out_gpu is not None:
+        llm = llm_view or views(p)[1]
+        gsets = {"crit": g_crit, "marg": g_marg, "counts": gsel["counts"]}
+        ref, _ = oracle.attend_group(layer, layer_slot, p.llm_q[layer_slot], llm, p.seq_lens,
+                                     p.head_map, sel, gsets, n_slm)
+        err = row_normwise(out_gpu.cpu().double().numpy(), ref)
+        rep["max_out_err"] = float(err.max())
+        assert err.max() <= OUT_TOL, f"f2 output error {err.max()}"
+    return rep

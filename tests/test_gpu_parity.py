@@ -372,3 +372,45 @@ def test_f1_accumulated_score_multistep():
     e, _ = parity.compare_attend(pcs, 0, out, sg, llm_view=llm_view)
     assert e <= parity.OUT_TOL
     print("f1", rep, e)
+
+
+# ---------------------------------------------------------------- variant f2 (R16)
+
+def _check_group(p, layers=None):
+    from paper_2508_02751_b200 import smallkv
+    step = smallkv.from_problem(p, variant="f2")
+    _, gout, outs = parity.run_gpu_step(p, step=step, layers=layers)
+    sel = parity.oracle_select(p)
+    reps = []
+    for i, slot in enumerate(range(p.llm.num_layers) if layers is None else layers):
+        reps.append(parity.compare_group(p, gout, sel, slot, out_gpu=outs[i]))
+    return reps
+
+
+@pytest.mark.parametrize("map_kind", ["random", "coherent"])
+def test_f2_group_selection_parity(map_kind):
+    """Variant f2: shared per-KV-group split of the summed proxy rows, per-head
+    marginal weights; ragged lengths incl. n = 1, budgets over n (clamp)."""
+    cfg = _cfg(llm=(2, 8, 2, 128), slm=(2, 8, 2, 64), n=1500, B=4, budget=(150, 60, 200))
+    p = synth.make_problem(cfg, seed=21, page_size=16, seq_lens=[1500, 731, 1, 200],
+                           map_kind=map_kind).to("cuda")
+    for rep in _check_group(p):
+        print("f2", map_kind, rep)
+
+
+@pytest.mark.parametrize("llm,slm", [((2, 28, 4, 128), (2, 14, 2, 64)),   # G = 7 (Qwen2.5-7B)
+                                     ((2, 32, 8, 128), (2, 32, 8, 64)),   # G = 4
+                                     ((1, 16, 16, 64), (1, 8, 8, 64))])   # G = 1, d = 64
+def test_f2_shapes(llm, slm):
+    cfg = _cfg(llm=llm, slm=slm, n=2100, B=2, budget=(210, 105, 210))
+    p = synth.make_problem(cfg, seed=22, page_size=64, seq_lens=[2100, 1337]).to("cuda")
+    for rep in _check_group(p):
+        print("f2 shape", llm, rep)
+
+
+def test_f2_qwen7b_dims():
+    """f2 at config 2's model dims and context (n = 4096), 4 sequences."""
+    cfg = synth.CONFIGS["qwen7b"]
+    p = synth.make_problem(cfg, seed=23, batch=4, llm_layers=[0, 1]).to("cuda")
+    for rep in _check_group(p):
+        print("f2 qwen7b", rep)
