@@ -50,7 +50,7 @@ __device__ __forceinline__ void lse_combine(float& m, float& s, float m2, float 
   m = mm;
 }
 
-template <bool kInSmem>
+template <bool kInSmem, bool kLogBins>
 __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) {
   extern __shared__ __align__(16) float vals[];   // [n] row, then (kInSmem) [n] bin bytes (+16)
   __shared__ uint32_t hist[kWarps][kBins];
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
   // Histogram coordinate: the score itself, or (variant f2's group scores —
   // sums of probabilities, heavily skewed towards 0) its logarithm.  Either is
   // monotone, so bins stay ordered like scores; exactness comes from the keys.
-  auto bv = [&](float v) { return p.log_bins ? logf(fmaxf(v, 1e-30f)) : v; };
+  auto bv = [&](float v) { return kLogBins ? logf(fmaxf(v, 1e-30f)) : v; };
   const float blo = bv(vlo);
   const float scale = 255.99f / (bv(vhi) - blo);
   const bool all_equal = !(vhi > vlo);
@@ -686,11 +686,12 @@ cudaError_t launch_select(const SelectParams& p, int32_t max_rows, int32_t max_s
   cudaError_t e;
   if (max_seq_len <= kSmemCap) {
     cfg.dynamicSmemBytes = static_cast<size_t>(max_seq_len) * 5 + 16;
-    cudaFuncSetAttribute(select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    auto k = p.log_bins ? select_kernel<true, true> : select_kernel<true, false>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(cfg.dynamicSmemBytes));
-    e = cudaLaunchKernelEx(&cfg, select_kernel<true>, p);
+    e = cudaLaunchKernelEx(&cfg, k, p);
   } else {
-    e = cudaLaunchKernelEx(&cfg, select_kernel<false>, p);
+    e = cudaLaunchKernelEx(&cfg, p.log_bins ? select_kernel<false, true> : select_kernel<false, false>, p);
   }
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
