@@ -64,6 +64,9 @@ def _load():
             lib.oracle_select_group.argtypes = [i32, i32, i32, P, P, P, i32, P, i32, P, P, P,
                                                 i32, i32, P, P, P, P]
             lib.oracle_attend_group.argtypes = lib.oracle_attend.argtypes
+            lib.oracle_match_window.argtypes = [i32, i32, i32, i32, P, P]
+            lib.oracle_match_window.restype = ctypes.c_int
+            lib.oracle_prefill_scores.argtypes = [P, P, i32, i32, i32, P]
             lib.oracle_topk.argtypes = [P, i32, i32, P]
             lib.oracle_match_heads.argtypes = [P, i32, P, i32, i32, i32, P, P]
             lib.oracle_accumulate_scores.argtypes = [P, i32, P]
@@ -265,6 +268,28 @@ def attend_group(layer: int, cache_layer: int, q, llm: CacheView, seq_lens, head
                             _ptr(marg), _ptr(counts), crit.shape[2], marg.shape[2],
                             _ptr(out), _ptr(wsum))
     return out, wsum
+
+
+def match_window(n: int, w_min: int = 100, w_max: int = 200, keep_last: bool = True):
+    """Variant f3 window decision (R17): None (DEFER) or (start, len)."""
+    lib = _load()
+    st, ln = ctypes.c_int32(), ctypes.c_int32()
+    ok = lib.oracle_match_window(int(n), int(w_min), int(w_max), int(bool(keep_last)),
+                                 ctypes.byref(st), ctypes.byref(ln))
+    return (st.value, ln.value) if ok else None
+
+
+def prefill_scores(q, cache: CacheView, b: int, start: int, length: int) -> np.ndarray:
+    """Variant f3: F [L*H][length] (fp64) — Eq. 1 column sums over the window
+    [start, start+length) of the causal prefill attention rows of its queries
+    q [L][length][H][d] (bf16) against the paged K of sequence b."""
+    lib = _load()
+    qq = _bf16_bits(q)
+    L, H = cache.struct.num_layers, cache.struct.num_q_heads
+    F = np.zeros((L * H, length), np.float64)
+    lib.oracle_prefill_scores(_ptr(qq), ctypes.byref(cache.struct), int(b), int(start),
+                              int(length), _ptr(F))
+    return F
 
 
 def topk_mask(F, k: int) -> np.ndarray:

@@ -24,6 +24,9 @@
  *                       P:205).
  *   oracle_match_heads— Eq. 2 Jaccard of TopK sets, Eq. 3 argmax.
  *   oracle_select_acc — variant f1: Eq. 1 running column sums.
+ *   oracle_match_window / oracle_prefill_scores — variant f3: matching window
+ *                       (R17) and Eq. 1 column sums of the window's causal
+ *                       prefill attention rows, the F vectors of Eq. 2.
  *   oracle_select_group / oracle_attend_group — variant f2: one split per LLM
  *                       KV head of the summed proxy rows (R16), per-head
  *                       marginal weights.
@@ -427,6 +430,57 @@ void oracle_accumulate_scores(const double* A, int32_t n, double* F) {
     double s = 0.0;
     for (int32_t u = 0; u < n; ++u) s += A[(int64_t)u * n + v];
     F[v] = s;
+  }
+}
+
+/* ------------------------------------------------------------------------- *
+ * Variant f3: prefill-side scores for head matching.
+ * Matching window ("range of 100 to 200 ... delays ... truncate",
+ * R17): n < w_min => DEFER (returns 0); else len = min(n, w_max) and
+ * start = keep_last ? n - len : 0 (SPEC S:157-162 keeps the most recent).
+ * ------------------------------------------------------------------------- */
+int oracle_match_window(int32_t n, int32_t w_min, int32_t w_max, int32_t keep_last,
+                        int32_t* start, int32_t* len) {
+  if (n < w_min) return 0;
+  *len = n < w_max ? n : w_max;
+  *start = keep_last ? n - *len : 0;
+  return 1;
+}
+
+/* F over the window of one sequence (Eq. 1): for every layer l and
+ * head h, the causal prefill attention rows of the window's queries
+ *   A[u][v] = softmax_{v <= pos(u)} (q_{l,u,h} · k_{l,v,kv(h)} / sqrt(d)),
+ *   pos(u) = start + u  (the full causal prefix, P:107 A = Softmax(QK^T/sqrt(d_h)))
+ * summed over the window's rows:  F[l*H + h][v - start] = Σ_u A[u][v] for v in
+ * the window.  q: bf16 [L][len][H][d] (the window's queries); K from the paged
+ * cache of sequence b, layer slots 0..L-1.  F: [L*H][len] doubles. */
+void oracle_prefill_scores(const uint16_t* q, const oracle_cache* c, int32_t b, int32_t start,
+                           int32_t len, double* F) {
+  const int L = c->num_layers, H = c->num_q_heads, d = c->head_dim;
+  const int G = H / c->num_kv_heads;
+  const double scale = 1.0 / sqrt((double)d);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t lh = 0; lh < (int64_t)L * H; ++lh) {
+    const int l = (int)(lh / H), h = (int)(lh % H);
+    double* f = F + lh * len;
+    for (int v = 0; v < len; ++v) f[v] = 0.0;
+    double* s = (double*)malloc(sizeof(double) * (start + len));
+    for (int u = 0; u < len; ++u) {
+      const int pos = start + u;
+      const uint16_t* qu = q + (((int64_t)l * len + u) * H + h) * d;
+      double mx = -INFINITY;
+      for (int v = 0; v <= pos; ++v) {
+        const uint16_t* kr = cache_row(c, c->k, l, b, v, h / G);
+        double dot = 0.0;
+        for (int t = 0; t < d; ++t) dot += bf16_to_double(qu[t]) * bf16_to_double(kr[t]);
+        s[v] = dot * scale;
+        if (s[v] > mx) mx = s[v];
+      }
+      double z = 0.0;
+      for (int v = 0; v <= pos; ++v) z += exp(s[v] - mx);
+      for (int v = start; v <= pos; ++v) f[v - start] += exp(s[v] - mx) / z;
+    }
+    free(s);
   }
 }
 

@@ -466,3 +466,59 @@ def test_P18_f2_attend_shared_sets_own_weights(oracle_mod):
                         w[bm] = a[bm]
                         ref = w @ V
                     np.testing.assert_allclose(out[b, h], ref.numpy(), rtol=1e-12, atol=1e-13)
+
+
+# --------------------------------------------------------------------------- variant f3
+def test_P19_f3_matching_window_spec(oracle_mod):
+    """R17 window: SPEC's worked decisions: 50 -> DEFER, 150 ->
+    [0,150), 1000 -> [800,1000) (keep the most recent); first-w reading -> [0,200)."""
+    w = GOLDEN["matching_window"]
+    for n, want in w["cases"]:
+        got = oracle_mod.match_window(n, w["min_len"], w["max_len"], keep_last=True)
+        assert (None if got is None else [got[0], got[0] + got[1]]) == want
+    assert oracle_mod.match_window(1000, 100, 200, keep_last=False) == (0, 200)
+    assert oracle_mod.match_window(100, 100, 200) == (0, 100)
+    assert oracle_mod.match_window(99, 100, 200) is None
+
+
+def _prefill_problem(n, seed=3):
+    cfg = synth.small_config(llm=(2, 8, 2, 64), slm=(2, 4, 2, 64), seq_len=n, batch=2,
+                             budget=(10, 5, 10))
+    return synth.make_problem(cfg, seed=seed, page_size=16, seq_lens=[n, n])
+
+
+def test_P20_f3_uniform_causal_column_sums(oracle_mod):
+    """q = 0 => every causal row is uniform over its prefix => F = column sums
+    of the uniform causal matrix: (11/6, 5/6, 1/3) for the first 3 tokens
+    (S:61), and Σ_{u>=v} 1/(start+u+1) for a window starting later."""
+    p = _prefill_problem(40)
+    _, llm = _views(oracle_mod, p)
+    H, d = p.cfg.llm.q_heads, p.cfg.llm.head_dim
+    for start, length in ((0, 3), (25, 15)):
+        q = torch.zeros(p.llm.num_layers, length, H, d, dtype=torch.bfloat16)
+        F = oracle_mod.prefill_scores(q, llm, 1, start, length)
+        ref = np.array([sum(1.0 / (start + u + 1) for u in range(v, length)) for v in range(length)])
+        np.testing.assert_allclose(F, np.broadcast_to(ref, F.shape), rtol=1e-13, atol=0)
+        if start == 0:
+            np.testing.assert_allclose(F[0], GOLDEN["column_sums_uniform_causal_n3"]["F"],
+                                       rtol=1e-13)
+
+
+def test_P21_f3_prefill_scores_vs_torch(oracle_mod):
+    """F = torch softmax of the causally masked q·K^T/sqrt(d) over the full
+    prefix, summed over the window's rows, window columns (Eq. 1)."""
+    p = _prefill_problem(60)
+    _, llm = _views(oracle_mod, p)
+    H, d, G = p.cfg.llm.q_heads, p.cfg.llm.head_dim, p.cfg.llm.q_heads // p.cfg.llm.kv_heads
+    g = torch.Generator().manual_seed(5)
+    for start, length in ((0, 60), (37, 23)):
+        q = torch.randn(p.llm.num_layers, length, H, d, generator=g).to(torch.bfloat16)
+        F = oracle_mod.prefill_scores(q, llm, 0, start, length)
+        for l in range(p.llm.num_layers):
+            for h in range(H):
+                K = dense_rows(p.llm, l, 0, start + length, h // G, "k")
+                s = (q[l, :, h].double() @ K.T) / math.sqrt(d)
+                pos = torch.arange(start, start + length).view(-1, 1)
+                s = s.masked_fill(torch.arange(start + length).view(1, -1) > pos, float("-inf"))
+                ref = torch.softmax(s, dim=1).sum(0)[start:]
+                np.testing.assert_allclose(F[l * H + h], ref.numpy(), rtol=1e-12, atol=1e-14)
