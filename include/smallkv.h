@@ -318,6 +318,40 @@ int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
                    void* stream);
 
 /*
+ * Variant f3 (R17) — the prefill side of matching.
+ *
+ * smallkv_match_window — host helper, the matching window of a prompt of n
+ * tokens ("range of 100 to 200 ... delays ... truncate"):
+ *   n < w_min  => *len = 0 (DEFER matching and eviction), *start = 0;
+ *   otherwise     *len = min(n, w_max), *start = keep_last ? n - *len : 0
+ *   (keep_last = 1: the most recent tokens).
+ * Errors: NULL outputs (SMALLKV_ERR_NULL); w_min < 1, w_max < w_min or n < 0
+ * (SMALLKV_ERR_SHAPE).
+ */
+int smallkv_match_window(int32_t n, int32_t w_min, int32_t w_max, int32_t keep_last,
+                         int32_t* start, int32_t* len);
+
+/*
+ * smallkv_prefill_scores — the F vectors of Eq. 2 for one model and one
+ * sequence: for every layer l < cache->num_layers and q-head h,
+ *   A[u][v] = softmax over v <= start+u of q_{l,u,h} · K_{l,kv(h)}[v] / sqrt(d)
+ *   F[l*H + h][v - start] = Σ_{u < len} A[u][v],   v in [start, start+len)
+ * (Eq. 1 column sums, of the window's causal prefill attention rows
+ * over their full prefix).  Feed the LLM's and the SLM's F to
+ * smallkv_match_heads (K0) to build the head map.
+ *   q      device bf16 [num_layers][len][H][d]: the window's post-RoPE queries.
+ *   cache  the model's paged cache (K used; positions [0, start+len) of
+ *          sequence `seq` must be written — the caller's contract).
+ *   seq    row of the block table.
+ *   F      device fp32 [num_layers * H][len], fully written.
+ * Tensor cores (mma.sync) for q·Kᵀ; deterministic.  Errors: NULL pointers,
+ * head_dim not in {64,128}, len not in [1,1024], start < 0 or the window past
+ * the block table, seq < 0, non-sm_100 device.
+ */
+int smallkv_prefill_scores(const uint16_t* q, const smallkv_cache* cache, int32_t seq,
+                           int32_t start, int32_t len, float* F, void* stream);
+
+/*
  * smallkv_match_heads — prefill similarity matching (Eq. 2-3).
  *   llm_F  device fp32 [n_llm][w]  accumulative scores F(A_i, C) (Eq. 1) of
  *          every LLM head over the matching window (R8).

@@ -113,6 +113,18 @@ cudaError_t launch_plan(const AttendParams& p, int32_t n_layers, cudaStream_t s)
 int64_t plan_bytes(int32_t n_layers, int32_t batch, int32_t kv_heads, int32_t max_seq_len);
 int32_t attend_ctas_per_group(int32_t batch, int32_t kv_heads);
 
+// ---------------------------------------------------------------- variant f3 prefill scores (R17)
+struct PrefillParams {
+  const uint16_t* q;          // [L][len][H][d] bf16 (the window's queries)
+  const uint16_t* k;          // paged pool [layer][page][H_kv][page_size][d]
+  const int32_t* block_table; // [B][max_blocks]
+  float* F;                   // [L*H][len]
+  int64_t layer_stride;       // elements between layers of the pool
+  int32_t seq, start, len, layers, heads, kv_heads, head_dim, page_size, ps_shift, max_blocks;
+  float scale;                // 1/sqrt(d)
+};
+cudaError_t launch_prefill_scores(const PrefillParams& p, cudaStream_t s);
+
 // ---------------------------------------------------------------- K0 match_heads
 cudaError_t launch_match_heads(const float* llm_F, int32_t n_llm, const float* slm_F,
                                int32_t n_slm, int32_t w, int32_t k, uint32_t* bits_ws,

@@ -617,6 +617,57 @@ int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
   return SMALLKV_OK;
 }
 
+int smallkv_match_window(int32_t n, int32_t w_min, int32_t w_max, int32_t keep_last,
+                         int32_t* start, int32_t* len) {
+  if (!start || !len) return fail(SMALLKV_ERR_NULL, "smallkv_match_window: NULL output");
+  if (w_min < 1 || w_max < w_min || n < 0)
+    return fail(SMALLKV_ERR_SHAPE, "window bounds [%d, %d] / n %d invalid", w_min, w_max, n);
+  if (n < w_min) {   // P:174 "delays the timing of similarity matching"
+    *start = 0;
+    *len = 0;
+    return SMALLKV_OK;
+  }
+  *len = n < w_max ? n : w_max;
+  *start = keep_last ? n - *len : 0;
+  return SMALLKV_OK;
+}
+
+int smallkv_prefill_scores(const uint16_t* q, const smallkv_cache* cache, int32_t seq,
+                           int32_t start, int32_t len, float* F, void* stream) {
+  int rc;
+  if ((rc = check_cache(cache, false, "prefill cache")) != SMALLKV_OK) return rc;
+  if (!q || !F) return fail(SMALLKV_ERR_NULL, "smallkv_prefill_scores: NULL q/F");
+  if (len < 1 || len > 1024) return fail(SMALLKV_ERR_SHAPE, "window length %d not in [1,1024]", len);
+  if (start < 0 || seq < 0 ||
+      static_cast<int64_t>(start) + len > static_cast<int64_t>(cache->max_blocks) * cache->page_size)
+    return fail(SMALLKV_ERR_SHAPE, "window [%d,%d) / seq %d outside the block table", start,
+                start + len, seq);
+  if (!aligned(q, 4) || !aligned(F, 4)) return fail(SMALLKV_ERR_ALIGN, "q / F must be 4-byte aligned");
+  if ((rc = check_device()) != SMALLKV_OK) return rc;
+  skv::PrefillParams pp{};
+  pp.q = q;
+  pp.k = cache->k;
+  pp.block_table = cache->block_table;
+  pp.F = F;
+  pp.layer_stride = static_cast<int64_t>(cache->num_pages) * cache->num_kv_heads * cache->page_size *
+                    cache->head_dim;
+  pp.seq = seq;
+  pp.start = start;
+  pp.len = len;
+  pp.layers = cache->num_layers;
+  pp.heads = cache->num_q_heads;
+  pp.kv_heads = cache->num_kv_heads;
+  pp.head_dim = cache->head_dim;
+  pp.page_size = cache->page_size;
+  pp.ps_shift = 0;
+  while ((1 << pp.ps_shift) < cache->page_size) ++pp.ps_shift;
+  pp.max_blocks = cache->max_blocks;
+  pp.scale = 1.0f / std::sqrt(static_cast<float>(cache->head_dim));
+  cudaError_t e = skv::launch_prefill_scores(pp, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "prefill_scores launch");
+  return SMALLKV_OK;
+}
+
 size_t smallkv_match_heads_workspace_size(int32_t n_llm, int32_t n_slm) {
   if (n_llm < 1 || n_slm < 1) return 0;
   return static_cast<size_t>(n_llm + n_slm) * 16 * 4;

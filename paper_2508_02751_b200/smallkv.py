@@ -32,7 +32,9 @@ EXPORTS = ("smallkv_last_error", "smallkv_version", "smallkv_budget_from_tau",
            "smallkv_select_workspace_size", "smallkv_select",
            "smallkv_select_group_workspace_size", "smallkv_select_group",
            "smallkv_plan_size", "smallkv_plan", "smallkv_plan_group",
-           "smallkv_attend_workspace_size", "smallkv_attend", "smallkv_match_heads_workspace_size", "smallkv_match_heads",
+           "smallkv_attend_workspace_size", "smallkv_attend",
+           "smallkv_match_window", "smallkv_prefill_scores",
+           "smallkv_match_heads_workspace_size", "smallkv_match_heads",
            "smallkv_workspace_init")
 
 
@@ -91,6 +93,8 @@ def load(path: Optional[str] = None):
         lib.smallkv_plan_size.argtypes = [P, P, i32]
         lib.smallkv_plan_size.restype = sz
         lib.smallkv_plan.argtypes = [P, P, P, i32, i32, P, P, P, P, P, P, sz, P]
+        lib.smallkv_match_window.argtypes = [i32, i32, i32, i32, P, P]
+        lib.smallkv_prefill_scores.argtypes = [P, P, i32, i32, i32, P, P]
         lib.smallkv_match_heads_workspace_size.argtypes = [i32, i32]
         lib.smallkv_match_heads_workspace_size.restype = sz
         lib.smallkv_match_heads.argtypes = [P, i32, P, i32, i32, i32, P, P, P, sz, P]
@@ -314,6 +318,33 @@ def from_problem(p, use_plan: bool = True, variant: str = "default") -> DecodeSt
                       max_seq_len=p.max_seq_len, head_map=p.head_map, k_crit=p.k_crit,
                       n_recent=p.n_recent, k_marg=p.k_marg, max_crit=p.max_crit,
                       max_marg=p.max_marg, use_plan=use_plan, variant=variant)
+
+
+def match_window(n: int, w_min: int = 100, w_max: int = 200, keep_last: bool = True):
+    """Variant f3 window decision (R17): None (DEFER) or (start, length)."""
+    lib = load()
+    st, ln = ctypes.c_int32(), ctypes.c_int32()
+    _check("smallkv_match_window", lib.smallkv_match_window(int(n), int(w_min), int(w_max),
+                                                            int(bool(keep_last)),
+                                                            ctypes.byref(st), ctypes.byref(ln)))
+    return (st.value, ln.value) if ln.value > 0 else None
+
+
+def prefill_scores(q: torch.Tensor, k: torch.Tensor, block_table: torch.Tensor, num_q_heads: int,
+                   seq: int, start: int, stream=None) -> torch.Tensor:
+    """Variant f3: F [L*H][len] fp32 on the GPU — Eq. 1 column sums over the
+    window [start, start+len) of the causal prefill attention rows of its
+    queries q [L][len][H][d] (bf16) against the paged K pool `k` of sequence seq."""
+    lib = load()
+    assert q.dtype == torch.bfloat16 and q.is_contiguous() and q.dim() == 4
+    L, length, H, d = q.shape
+    assert H == num_q_heads and k.shape[0] == L and k.shape[-1] == d
+    cache = make_cache(k, None, block_table, num_q_heads)
+    F = torch.empty(L * H, length, dtype=torch.float32, device=q.device)
+    _check("smallkv_prefill_scores",
+           lib.smallkv_prefill_scores(q.data_ptr(), ctypes.byref(cache), int(seq), int(start),
+                                      int(length), F.data_ptr(), _stream(stream)))
+    return F
 
 
 def match_heads(llm_F: torch.Tensor, slm_F: torch.Tensor, k_match: int, stream=None):

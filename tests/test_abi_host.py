@@ -81,3 +81,14 @@ def test_kv_bytes_model():
     assert bm.kv_cache_bytes(g["L"], g["N_kv"], g["D_kv"], g["S"], g["B"], g["C_b"]) == g["bytes"]
     r = bm.kv_cache_bytes(80, 8, 128, 1, 1, 2) / bm.kv_cache_bytes(28, 4, 128, 1, 1, 2)
     assert abs(r - GOLDEN["kv_ratio_72b_7b"]["value"]) < GOLDEN["kv_ratio_72b_7b"]["tol"]
+
+
+def test_f3_match_window_host():
+    """smallkv_match_window (host) = SPEC's window decisions (R17)."""
+    w = GOLDEN["matching_window"]
+    for n, want in w["cases"]:
+        got = smallkv.match_window(n, w["min_len"], w["max_len"], keep_last=True)
+        assert (None if got is None else [got[0], got[0] + got[1]]) == want
+    assert smallkv.match_window(1000, keep_last=False) == (0, 200)
+    with pytest.raises(smallkv.SmallKVError):
+        smallkv.match_window(10, 200, 100)

@@ -414,3 +414,57 @@ def test_f2_qwen7b_dims():
     p = synth.make_problem(cfg, seed=23, batch=4, llm_layers=[0, 1]).to("cuda")
     for rep in _check_group(p):
         print("f2 qwen7b", rep)
+
+
+# ---------------------------------------------------------------- variant f3 (R17)
+
+@pytest.mark.parametrize("which,window", [("llm", (0, 150)), ("llm", (37, 123)),
+                                          ("slm", (0, 200)), ("slm", (300, 200))])
+def test_f3_prefill_scores_parity(which, window):
+    """F (Eq. 1 column sums of the window's causal prefill rows) vs the fp64
+    oracle; LLM d=128 G=4 / SLM d=64 G=2; windows at 0 and later (keep_last)."""
+    import oracle
+    from paper_2508_02751_b200 import smallkv
+    start, length = window
+    cfg = _cfg(llm=(2, 8, 2, 128), slm=(2, 4, 2, 64), n=start + length + 5, B=2)
+    p = synth.make_problem(cfg, seed=31, page_size=16).to("cuda")
+    cache = p.llm if which == "llm" else p.slm
+    dims = cfg.llm if which == "llm" else cfg.slm
+    g = torch.Generator(device="cuda").manual_seed(7)
+    q = torch.randn(cache.num_layers, length, dims.q_heads, dims.head_dim, device="cuda",
+                    generator=g).to(torch.bfloat16)
+    F = smallkv.prefill_scores(q, cache.k, cache.block_table, dims.q_heads, 1, start)
+    view = oracle.CacheView(cache.k, None, cache.block_table, cache.num_pages, cache.page_size,
+                            cache.num_layers, dims.q_heads, dims.kv_heads, dims.head_dim)
+    ref = oracle.prefill_scores(q, view, 1, start, length)
+    err = np.abs(F.cpu().double().numpy() - ref).max()
+    print("f3", which, window, "max abs err", err, "max F", ref.max())
+    assert err <= 1e-4 * max(1.0, ref.max())
+
+
+def test_f3_head_matching_end_to_end():
+    """Window -> LLM and SLM prefill F on the GPU -> K0 match_heads -> head map;
+    equal to the oracle's match_heads on the GPU's F (Eq. 2-3), and the GPU F
+    within tolerance of the oracle's F."""
+    import oracle
+    from paper_2508_02751_b200 import smallkv
+    n = 420
+    win = smallkv.match_window(n)
+    assert win == oracle.match_window(n) == (220, 200)
+    start, length = win
+    cfg = _cfg(llm=(2, 8, 2, 128), slm=(2, 4, 2, 64), n=n, B=1)
+    p = synth.make_problem(cfg, seed=32, page_size=16).to("cuda")
+    g = torch.Generator(device="cuda").manual_seed(8)
+    ql = torch.randn(2, length, 8, 128, device="cuda", generator=g).to(torch.bfloat16)
+    qs = torch.randn(2, length, 4, 64, device="cuda", generator=g).to(torch.bfloat16)
+    Fl = smallkv.prefill_scores(ql, p.llm.k, p.llm.block_table, 8, 0, start)
+    Fs = smallkv.prefill_scores(qs, p.slm.k, p.slm.block_table, 4, 0, start)
+    k_match = max(16, -(-length // 5))
+    hm, jac = smallkv.match_heads(Fl, Fs, k_match)
+    ohm, ojac = oracle.match_heads(Fl.cpu().double().numpy(), Fs.cpu().double().numpy(), k_match)
+    assert np.array_equal(hm.cpu().numpy(), ohm)
+    np.testing.assert_allclose(jac.cpu().numpy(), ojac, rtol=1e-6)
+    lv = oracle.CacheView(p.llm.k, None, p.llm.block_table, p.llm.num_pages, p.llm.page_size,
+                          2, 8, 2, 128)
+    refl = oracle.prefill_scores(ql, lv, 0, start, length)
+    assert np.abs(Fl.cpu().double().numpy() - refl).max() <= 1e-4 * max(1.0, refl.max())
