@@ -52,7 +52,7 @@ __device__ __forceinline__ long long gtimer() {
 #define SKV_T(i)                                                                         \
   if (g_trace && threadIdx.x == 0) {                                                     \
     const int cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;      \
-    g_trace[cta * 10 + (i)] = gtimer();                                                  \
+    g_trace[(skv_tl * 4096 + cta) * 10 + (i)] = gtimer();                                \
   }
 #else
 #define SKV_T(i)
@@ -328,6 +328,10 @@ __global__ void __launch_bounds__(kThreads, 1) attend_kernel(const AttendParams 
   // Without the overlap flag nothing is read before the previous kernel on the
   // stream has completed.  With it, the prologue below (plan / selection
   // outputs, page tables, K/V tiles) may run during that kernel's tail.
+#ifdef SKV_TRACE
+  const int skv_tl = p.layer;   // trace slot (diagnostic builds only)
+#endif
+  SKV_T(7);
   if (!p.overlap_prologue) griddep_wait();
   SKV_T(0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -335,6 +339,45 @@ __global__ void __launch_bounds__(kThreads, 1) attend_kernel(const AttendParams 
   const uint8_t* rec = p.plan ? p.plan + ((static_cast<int64_t>(p.layer) * p.batch + b) *
                                               p.kv_heads + g) * plan_record_bytes(NC)
                               : nullptr;
+  uint8_t* wst = stages + warp * NSTAGE * SB;
+  const uint16_t* kpool = p.k + p.layer_offset;
+  const uint16_t* vpool = p.v + p.layer_offset;
+  // Early tiles: the list starts with the recent window [n-R', n), whose rows
+  // need only the sequence length, the recent budget and the block table
+  // (small, L2-resident) — so a single-CTA group issues its first tiles'
+  // K/V copies before (and in parallel with) the plan / list loads.
+  int early = 0;
+  if (NC == 1) {
+    const int n = p.seq_lens[b];
+    const int Rc = min(max(p.n_recent[b], 0), n);
+    const int32_t* bt = p.block_table + static_cast<int64_t>(b) * p.max_blocks;
+#pragma unroll
+    for (int i = 0; i < NSTAGE - 1; ++i) {
+      const int j = warp + i * kWarps;   // tile j = entries [16j, 16j+16) of the recent run
+      if (kTile * j >= Rc || early != i) break;
+      const int cnt = min(kTile, Rc - kTile * j);
+      uint8_t* st = wst + i * SB;
+#pragma unroll
+      for (int grp = 0; grp < kTile / 4; ++grp) {
+        const int eo = grp * 4 + (lane >> 3);
+        const bool ev = eo < cnt;
+        const int pos = n - Rc + kTile * j + eo;
+        const uint32_t ro = ev ? static_cast<uint32_t>(
+                                     ((static_cast<int64_t>(__ldg(bt + (pos >> p.ps_shift))) * p.kv_heads + g) *
+                                          p.page_size + (pos & (p.page_size - 1))) * D)
+                               : 0u;
+#pragma unroll
+        for (int hf = 0; hf < D / 64; ++hf) {
+          const int ch = hf * 8 + (lane & 7);
+          const int sw_ = (ch ^ (eo & 7)) << 4;
+          if (ev) cp_async16(smem_u32(st + eo * ROWB + sw_), kpool + ro + ch * 8, true);
+          cp_async16(smem_u32(st + KV_BYTES + eo * ROWB + sw_), vpool + ro + ch * 8, ev);
+        }
+      }
+      cp_async_commit();
+      ++early;
+    }
+  }
   if (rec) {
     // one round: header + this rank's pre-staged first batch (cp.async, 16 B)
     for (int i = tid; i < static_cast<int>(sizeof(GroupLayout)) / 16; i += kThreads)
@@ -355,9 +398,6 @@ __global__ void __launch_bounds__(kThreads, 1) attend_kernel(const AttendParams 
   SKV_T(1);
 
   const int gq = lane >> 2, tq = lane & 3;
-  uint8_t* wst = stages + warp * NSTAGE * SB;
-  const uint16_t* kpool = p.k + p.layer_offset;
-  const uint16_t* vpool = p.v + p.layer_offset;
 
   uint32_t qa[D / 16][2];
   bool q_ready = false;
@@ -485,12 +525,14 @@ __global__ void __launch_bounds__(kThreads, 1) attend_kernel(const AttendParams 
     };
 
 #pragma unroll
-    for (int i = 0; i < NSTAGE - 1; ++i) issue(i);
+    for (int i = 0; i < NSTAGE - 1; ++i)
+      if (!(e_b == e_lo && i < early)) issue(i);   // the early tiles are in flight already
     if (!q_ready) wait_and_load_q();
     for (int i = 0; i < nmy; ++i) {
       issue(i + NSTAGE - 1);
       cp_async_wait<NSTAGE - 1>();
       __syncwarp();
+      if (i == 0) { SKV_T(3); }
       const uint8_t* st = wst + ((tbase + i) % NSTAGE) * SB;
       const uint8_t* kb = st;
       const uint8_t* vb = st + KV_BYTES;
@@ -640,6 +682,57 @@ __global__ void __launch_bounds__(kThreads, 1) attend_kernel(const AttendParams 
   float* wm_s = reinterpret_cast<float*>(stages);              // [kWarps][8]
   float* wl_s = wm_s + kWarps * 8;                              // [kWarps][8]
   float* wo_s = wl_s + kWarps * 8;                              // [kWarps][16][D]: O_c rows h, O_m rows 8+h
+  if (gq == 0) {
+    wm_s[warp * 8 + h0] = m0;
+    wm_s[warp * 8 + h1] = m1;
+    wl_s[warp * 8 + h0] = l0;
+    wl_s[warp * 8 + h1] = l1;
+  }
+  if (NC == 1) {
+    // One CTA per group: every warp folds its softmax normalisation into its
+    // own partial first — c_w = O_c,w · 2^(m_w - M) / L + O_m,w with the
+    // group-wide M and L from the (m, l) of all warps — so only [8][D] floats
+    // per warp go through shared memory and the final merge is a plain sum.
+    __syncthreads();
+    float M0 = -INFINITY, M1 = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      M0 = fmaxf(M0, wm_s[w * 8 + h0]);
+      M1 = fmaxf(M1, wm_s[w * 8 + h1]);
+    }
+    const float M0u = M0 == -INFINITY ? 0.f : M0, M1u = M1 == -INFINITY ? 0.f : M1;
+    float L0 = 0.f, L1 = 0.f;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      L0 += wl_s[w * 8 + h0] * exp2f(wm_s[w * 8 + h0] - M0u);
+      L1 += wl_s[w * 8 + h1] * exp2f(wm_s[w * 8 + h1] - M1u);
+    }
+    const float f0 = L0 > 0.f ? exp2f(m0 - M0u) / L0 : 0.f;
+    const float f1 = L1 > 0.f ? exp2f(m1 - M1u) / L1 : 0.f;
+    float* myc = wo_s + warp * 8 * D;                           // [kWarps][8][D]
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      const int d0 = 16 * mt + gq;
+      myc[h0 * D + d0] = oc[mt][0] * f0 + om[mt][0];
+      myc[h1 * D + d0] = oc[mt][1] * f1 + om[mt][1];
+      myc[h0 * D + d0 + 8] = oc[mt][2] * f0 + om[mt][2];
+      myc[h1 * D + d0 + 8] = oc[mt][3] * f1 + om[mt][3];
+    }
+    __syncthreads();
+    const int64_t bo = static_cast<int64_t>(b) * p.heads + g * G;
+    for (int it = tid; it < G * (D / 4); it += kThreads) {
+      const int h = it / (D / 4), c4 = (it % (D / 4)) * 4;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        const float4 a = *reinterpret_cast<const float4*>(wo_s + (w * 8 + h) * D + c4);
+        acc.x += a.x; acc.y += a.y; acc.z += a.z; acc.w += a.w;
+      }
+      *reinterpret_cast<float4*>(p.out + (bo + h) * D + c4) = acc;
+    }
+    SKV_T(5);
+    return;
+  }
   {
     float* myo = wo_s + warp * 16 * D;
 #pragma unroll
@@ -653,12 +746,6 @@ __global__ void __launch_bounds__(kThreads, 1) attend_kernel(const AttendParams 
       myo[(8 + h1) * D + d0] = om[mt][1];
       myo[(8 + h0) * D + d0 + 8] = om[mt][2];
       myo[(8 + h1) * D + d0 + 8] = om[mt][3];
-    }
-    if (gq == 0) {
-      wm_s[warp * 8 + h0] = m0;
-      wm_s[warp * 8 + h1] = m1;
-      wl_s[warp * 8 + h0] = l0;
-      wl_s[warp * 8 + h1] = l1;
     }
   }
   __syncthreads();
@@ -701,8 +788,8 @@ __global__ void __launch_bounds__(kThreads, 1) attend_kernel(const AttendParams 
     const int cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
     int smid;
     asm("mov.u32 %0, %%smid;" : "=r"(smid));
-    g_trace[cta * 10 + 8] = e_hi - e_lo;
-    g_trace[cta * 10 + 9] = smid;
+    g_trace[(skv_tl * 4096 + cta) * 10 + 8] = e_hi - e_lo;
+    g_trace[(skv_tl * 4096 + cta) * 10 + 9] = smid;
   }
 #endif
   if (NC == 1) return;
