@@ -374,15 +374,25 @@ class DecodeGraph:
     With timing=True, external CUDA events are captured between the calls
     (after select and after every attend) so kernel durations can be read
     back after a replay with `segment_ms()`.
+    host_io: optional (h_slm_q, h_q, h_out) pinned host tensors; the graph then
+    also moves the step's inputs in (h_slm_q -> slm_q, h_q[i] -> layer i's q)
+    and every layer's output out (out -> h_out[i]), each layer's copies on
+    side streams overlapping the other layers' kernels (the q of layer i only
+    gates attend i; the output copy of layer i only waits for attend i).
     """
 
-    def __init__(self, step: DecodeStep, slm_q: torch.Tensor, layer_plan, timing: bool = False):
+    def __init__(self, step: DecodeStep, slm_q: torch.Tensor, layer_plan, timing: bool = False,
+                 host_io=None):
         self.step = step
         self.slm_q = slm_q
         self.plan = list(layer_plan)
         self.timing = timing
+        self.host_io = host_io
         self.events = []
         self.stream = torch.cuda.Stream()
+        if host_io is not None:
+            self.h2d_stream = torch.cuda.Stream()
+            self.d2h_stream = torch.cuda.Stream()
         # eager warm-up on the capture stream (sets kernel attributes, checks args)
         with torch.cuda.stream(self.stream):
             self._calls(record=False)
@@ -395,6 +405,8 @@ class DecodeGraph:
             self._calls(record=timing)
 
     def _calls(self, record: bool):
+        if self.host_io is not None:
+            return self._calls_host_io()
         if record:
             self.events[0].record()
         self.step.select(self.slm_q)
@@ -406,6 +418,34 @@ class DecodeGraph:
             self.step.attend(layer, slot, q, out, overlap_prologue=i > 0)
             if record:
                 self.events[2 + i].record()
+
+    def _calls_host_io(self):
+        """select + attends with the host copies on side streams (see __init__)."""
+        h_slm_q, h_q, h_out = self.host_io
+        main = torch.cuda.current_stream()
+        start = torch.cuda.Event()
+        start.record(main)
+        # the layers' q copies run on a side stream under select (one join
+        # before the first attend: per-layer joins cost more than they save)
+        self.h2d_stream.wait_event(start)
+        with torch.cuda.stream(self.h2d_stream):
+            for i, (_, _, q, _) in enumerate(self.plan):
+                q.copy_(h_q[i], non_blocking=True)
+            q_ready = torch.cuda.Event()
+            q_ready.record(self.h2d_stream)
+        self.slm_q.copy_(h_slm_q, non_blocking=True)
+        self.step.select(self.slm_q)
+        main.wait_event(q_ready)
+        for i, (layer, slot, q, out) in enumerate(self.plan):
+            self.step.attend(layer, slot, q, out, overlap_prologue=i > 0)
+            done = torch.cuda.Event()
+            done.record(main)
+            self.d2h_stream.wait_event(done)
+            with torch.cuda.stream(self.d2h_stream):
+                h_out[i].copy_(out, non_blocking=True)
+        end = torch.cuda.Event()
+        end.record(self.d2h_stream)
+        main.wait_event(end)
 
     def replay(self):
         """Launch the graph on this object's stream (CUDAGraph.replay launches on
