@@ -144,11 +144,28 @@ def run_ours(args, world, rank, local):
     p, resident = build_problem(args.config, rank, world, args.shard, device)
     cfg = p.cfg
     L = cfg.llm.layers
-    step = smallkv.from_problem(p, variant=args.variant)
+    tier = None
+    if args.variant == "f4":
+        # host-tiered pool: the LLM K/V in pinned host memory,
+        # each group's needed rows in an HBM hot pool refreshed per layer
+        assert resident == L, "f4 keeps one hot-pool slot per LLM layer"
+        step = smallkv.from_problem(p, use_plan=False)
+        host_k = torch.empty(p.llm.k.shape, dtype=p.llm.k.dtype, pin_memory=True)
+        host_v = torch.empty(p.llm.v.shape, dtype=p.llm.v.dtype, pin_memory=True)
+        host_k.copy_(p.llm.k)
+        host_v.copy_(p.llm.v)
+        # slots per group = the largest list: R' + (#distinct SLM rows of the group) * (K'+M')
+        H, Hkv = cfg.llm.q_heads, cfg.llm.kv_heads
+        hm = p.head_map.cpu().view(L, Hkv, H // Hkv)
+        rows_max = max(len(set(hm[l, g].tolist())) for l in range(L) for g in range(Hkv))
+        cap = -(-(int(p.n_recent.max()) + rows_max * (p.max_crit + p.max_marg)) // 4) * 4
+        tier = smallkv.TieredKV(step, host_k, host_v, capacity=cap)
+    else:
+        step = smallkv.from_problem(p, variant=args.variant)
     outs = torch.empty(L, p.batch, cfg.llm.q_heads, cfg.llm.head_dim, dtype=torch.float32,
                        device=device)
     plan = [(l, l % resident, p.llm_q[l % resident], outs[l]) for l in range(L)]
-    graph = smallkv.DecodeGraph(step, p.slm_q, plan, timing=False)
+    graph = smallkv.DecodeGraph(step, p.slm_q, plan, timing=False, tier=tier)
     if heads:
         # the exchange step of head sharding: all-gather every layer's per-head
         # outputs [L, B, H/w, d] -> [L, B, H, d] once per step (NCCL / NVLink)
@@ -255,9 +272,10 @@ def run_ours(args, world, rank, local):
     h_q.copy_(p.llm_q)
     h_out = torch.empty(outs.shape, dtype=outs.dtype, pin_memory=True)
     e2e_steps = max(3, min(args.steps, 200))
-    if heads:
+    if heads or tier is not None:
         # head sharding: the step's all-gather sits between the attends and the
-        # output read, so the copies stay outside the graph, in stream order
+        # output read (f4: the hot-pool refresh), so the copies stay outside the
+        # graph, in stream order
         h2d = h_slm_q.numel() * 2 + h_q.numel() * 2
         d2h = h_out.numel() * 4
         barrier()
@@ -335,7 +353,9 @@ def run_ours(args, world, rank, local):
             "head_map": "coherent (every SLM kv-head referenced)",
             "selection": ("f2: one split per LLM (layer, kv-group) of the summed proxy rows "
                           "(SURVEY §8(f) f2, DESIGN.md R16)" if args.variant == "f2"
-                          else "per SLM row (Eq. 6, R1/R14)"),
+                          else "per SLM row (Eq. 6, R1/R14)"
+                          + ("; f4: LLM K/V pool in pinned host memory, per-group HBM hot "
+                             "pools (SURVEY §8(f) f4, DESIGN.md R18)" if args.variant == "f4" else "")),
             "page_size": p.llm.page_size,
             "resident_llm_layers": resident,
             "l2": "inputs larger than L2: %.2f GB touched per step vs 126 MB L2" % (bm["step"] / 1e9),
@@ -366,12 +386,62 @@ def run_ours(args, world, rank, local):
         "gpu_launches": graph.kernels_per_step * args.steps,
         "clocks": clocks,
     }
+    if tier is not None:
+        line["f4"] = f4_report(p, cfg, graph, tier)
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(p, cfg, L, variant=args.variant)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def f4_report(p, cfg, graph, tier, steps: int = 20):
+    """Host-link traffic of the tiered pool: in the steady state (same inputs
+    every step) nothing is fetched after the first step; with the SLM query
+    alternating between two inputs the selection drifts every step and only the
+    rows that were not resident cross the host link."""
+    import torch
+    row_bytes = cfg.llm.head_dim * 2
+    s = graph.stream
+    s.synchronize()
+    f0, ov0 = tier.counters()
+    for _ in range(3):
+        graph.replay()
+    s.synchronize()
+    f1, _ = tier.counters()
+    g = torch.Generator(device=p.slm_q.device).manual_seed(99)
+    q_a = p.slm_q.clone()
+    q_b = (p.slm_q.float() + 0.1 * torch.randn(p.slm_q.shape, device=p.slm_q.device,
+                                               generator=g)).to(torch.bfloat16)
+    with torch.cuda.stream(s):
+        p.slm_q.copy_(q_b)
+    graph.replay()                                   # first drift step (outside the timing)
+    s.synchronize()
+    f2, _ = tier.counters()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for i in range(steps):
+        with torch.cuda.stream(s):
+            p.slm_q.copy_(q_a if i % 2 == 0 else q_b)
+        graph.replay()
+    e1.record(s)
+    e1.synchronize()
+    f3, ov = tier.counters()
+    with torch.cuda.stream(s):
+        p.slm_q.copy_(q_a)
+    s.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    per = (f3 - f2) / steps
+    return {"steady_rows_fetched_per_step": (f1 - f0) / 3,
+            "drift": {"value": round(cfg.llm.layers / (ms / 1e3), 2), "unit": "layer-steps/s",
+                      "ms_per_step": round(ms, 4), "rows_fetched_per_step": per,
+                      "host_link_bytes_per_step": int(per * row_bytes),
+                      "host_link_gbs": round(per * row_bytes / (ms / 1e3) / 1e9, 2),
+                      "note": "SLM query alternating between two inputs each step"},
+            "capacity_overflows": ov,
+            "hot_pool_bytes": int(tier.hot_k.numel() * 4),
+            "host_pool_bytes": int(p.llm.k.numel() * 4)}
 
 
 def cpu_baseline(p, cfg, L, target_s: float = 12.0, variant: str = "default"):
@@ -478,8 +548,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="qwen7b")
-    ap.add_argument("--variant", choices=["default", "f2"], default="default",
-                    help="f2: per-KV-group shared selection (SURVEY §8(f) f2, DESIGN.md R16)")
+    ap.add_argument("--variant", choices=["default", "f2", "f4"], default="default",
+                    help="f2: per-KV-group shared selection (SURVEY §8(f) f2, DESIGN.md R16); "
+                         "f4: host-tiered KV pool (SURVEY §8(f) f4, DESIGN.md R18)")
     ap.add_argument("--shard", choices=["batch", "heads"], default="batch",
                     help="N>1 partition: sequences (weak scaling) or LLM kv-head groups")
     ap.add_argument("--cpu-seqs", type=int, default=4,

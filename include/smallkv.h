@@ -318,6 +318,57 @@ int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
                    void* stream);
 
 /*
+ * Variant f4 (R18) — host-tiered KV (the paper's
+ * memory-saving mode: the KV cache migrates between GPU HBM
+ * and CPU memory, the change being moved each step).  The full paged LLM pool
+ * lives in HOST memory (pinned, UVA-addressable: `host_llm.k/v`); each
+ * (layer, sequence, kv-group) keeps the rows its current list needs in an HBM
+ * hot pool of `capacity` slots:
+ *   host_llm       layer l of its pools holds LLM layer l (num_layers >= L).
+ *   hot_k / hot_v  device bf16 [L][B][H_kv][capacity][d] (caller-owned).
+ *   state          device bytes >= smallkv_tier_state_size(): per group the
+ *                  position->slot and slot->position maps, residency flags, the
+ *                  entries' slots, and two uint64 counters (rows fetched over
+ *                  the host link; capacity overflows).  Initialise once with
+ *                  smallkv_tier_init.
+ * smallkv_tier_update (LLM layers [layer_begin, layer_begin+layer_count) in one
+ * launch — e.g. all of them right after smallkv_select / _select_group, so the
+ * refresh of every layer runs ahead of the attends):
+ * frees the slots of positions the group's list no longer holds, gives every
+ * newly listed position a free slot, and copies from host memory only what is
+ * missing — V for every new position, K only where a critical or recent entry
+ * needs it (marginal rows stay V-only, R11); rows resident at the previous
+ * step are not moved.  capacity must be a multiple of 4 and >= the list size
+ * R' + (#distinct rows)·(K' + M') of every group, else the group is skipped
+ * and counted as an overflow (its outputs are then undefined).
+ * smallkv_attend_tiered: smallkv_attend reading the hot pool (no plan).
+ * flags: SMALLKV_ATTEND_GROUP_SELECTION for variant f2 selections.
+ * Errors: as smallkv_attend, plus max_seq_len > 32768 or bad capacity
+ * (SMALLKV_ERR_SHAPE), small state (SMALLKV_ERR_WORKSPACE).
+ */
+size_t smallkv_tier_state_size(const smallkv_cache* llm, const smallkv_batch* batch,
+                               int32_t n_llm_layers, int32_t capacity);
+int smallkv_tier_init(void* state, size_t state_bytes, const smallkv_cache* llm,
+                      const smallkv_batch* batch, int32_t n_llm_layers, int32_t capacity,
+                      void* stream);
+int smallkv_tier_update(int32_t layer_begin, int32_t layer_count, const smallkv_cache* host_llm,
+                        uint16_t* hot_k, uint16_t* hot_v, int32_t capacity,
+                        const smallkv_batch* batch, const int32_t* head_map,
+                        int32_t n_llm_layers, int32_t slm_heads_total,
+                        const smallkv_budgets* budgets, const int32_t* crit_idx,
+                        const int32_t* marg_idx, const float* marg_w, const int32_t* counts,
+                        int32_t flags, void* state, size_t state_bytes, void* stream);
+int smallkv_attend_tiered(int32_t llm_layer, const uint16_t* q,
+                          const smallkv_cache* host_llm, const uint16_t* hot_k,
+                          const uint16_t* hot_v, int32_t capacity, const void* state,
+                          const smallkv_batch* batch, const int32_t* head_map,
+                          int32_t n_llm_layers, int32_t slm_heads_total,
+                          const smallkv_budgets* budgets, const int32_t* crit_idx,
+                          const int32_t* marg_idx, const float* marg_w,
+                          const int32_t* counts, float* out, int32_t flags, void* ws,
+                          size_t ws_bytes, void* stream);
+
+/*
  * Variant f3 (R17) — the prefill side of matching.
  *
  * smallkv_match_window — host helper, the matching window of a prompt of n

@@ -213,6 +213,14 @@ __device__ void stage_entries(const AttendParams& p, const GroupLayout& L, int b
     sw[i] = wt;
   }
   __syncthreads();
+  if (p.entry_slot) {
+    // variant f4: rows live in the group's hot-pool slots
+    const int32_t* es = p.entry_slot + ((static_cast<int64_t>(p.layer) * p.batch + b) * p.kv_heads + g) * p.hot_cap;
+    for (int i = tid; i < E; i += nthr)
+      soff[i] = static_cast<uint32_t>(((static_cast<int64_t>(b) * p.kv_heads + g) * p.hot_cap + __ldg(es + e_b + i)) * D);
+    __syncthreads();
+    return;
+  }
   const int32_t* bt = p.block_table + static_cast<int64_t>(b) * p.max_blocks;
   for (int i = tid; i < E; i += nthr) {
     const int pos = static_cast<int>(soff[i]);
@@ -347,7 +355,7 @@ __global__ void __launch_bounds__(kThreads, 1) attend_kernel(const AttendParams 
   // (small, L2-resident) — so a single-CTA group issues its first tiles'
   // K/V copies before (and in parallel with) the plan / list loads.
   int early = 0;
-  if (NC == 1) {
+  if (NC == 1 && !p.entry_slot) {
     const int n = p.seq_lens[b];
     const int Rc = min(max(p.n_recent[b], 0), n);
     const int32_t* bt = p.block_table + static_cast<int64_t>(b) * p.max_blocks;
@@ -823,6 +831,141 @@ __global__ void __launch_bounds__(kThreads, 1) attend_kernel(const AttendParams 
   cluster_sync();   // keep every rank's shared memory alive until all reads are done
   SKV_T(6);
 }
+
+// ---------------------------------------------------------------------------
+// Variant f4: host-tiered KV.  The full paged pool lives in
+// host memory; each (layer, sequence, kv-group) keeps the rows its current
+// list needs in an HBM hot pool of `cap` slots.  Per step and layer, one CTA
+// per group: (1) decode the list's positions (the attend kernel's own layout)
+// and mark them, with "needs K" for critical / recent entries; (2) free the
+// slots of positions no longer needed; (3) give every newly needed position a
+// free slot; (4) fetch from host memory (zero-copy over the host link) only
+// what is missing — V for every new position, K only where a critical /
+// recent entry needs it; (5) write each entry's slot for the attend kernel.
+// Rows resident at the previous step are not moved (migrate the
+// change, in parallel with the forward).
+constexpr int kTierThreads = 256;
+constexpr int kTierMaxSeq = 32768;   // bitmaps in shared memory
+
+template <int D>
+__global__ void __launch_bounds__(kTierThreads) tier_update_kernel(const TierParams t) {
+  const AttendParams& p = t.a;
+  __shared__ __align__(16) GroupLayout L;
+  __shared__ uint32_t need_v[kTierMaxSeq / 32], need_k[kTierMaxSeq / 32], claimed[kTierMaxSeq / 32];
+  __shared__ int s_nfree, s_nmiss;
+  extern __shared__ int dyn[];   // [cap] entry positions | [cap] free slots | [cap] missing positions
+  int* s_pos = dyn;
+  int* s_free = dyn + t.cap;
+  int* s_miss = dyn + 2 * t.cap;
+  const int g = blockIdx.x, b = blockIdx.y, layer = t.layer_begin + blockIdx.z, tid = threadIdx.x;
+  build_layout(p, layer, b, g, L);
+  const int n = L.n, T = L.T;
+  if (T > t.cap) {   // the list does not fit the group's slots: reported, nothing changed
+    if (tid == 0) atomicAdd(t.counters + 1, 1ull);
+    return;
+  }
+  const int64_t grp = (static_cast<int64_t>(layer) * p.batch + b) * p.kv_heads + g;
+  int32_t* sop = t.slot_of_pos + grp * t.max_seq_len;
+  int32_t* pos_of = t.pos_of_slot + grp * t.cap;
+  uint8_t* flags = t.slot_flags + grp * t.cap;
+  int32_t* es = t.entry_slot + grp * t.cap;
+  const uint16_t* host_k = t.host_k + static_cast<int64_t>(layer) * t.host_layer_stride;
+  const uint16_t* host_v = t.host_v + static_cast<int64_t>(layer) * t.host_layer_stride;
+  const int64_t hot0 = (static_cast<int64_t>(layer) * p.batch + b) * p.kv_heads + g;
+  uint16_t* hot_k = t.hot_k + hot0 * t.cap * D;
+  uint16_t* hot_v = t.hot_v + hot0 * t.cap * D;
+  for (int i = tid; i < (n + 31) / 32; i += kTierThreads) need_v[i] = need_k[i] = claimed[i] = 0u;
+  if (tid == 0) s_nfree = s_nmiss = 0;
+  __syncthreads();
+  // (1) the list's positions (decoded once) and their needs: K+V for recent /
+  // critical entries, V for marginal ones
+  for (int x = tid; x < T; x += kTierThreads) {
+    int pos, y = x;
+    bool k;
+    if (y < L.Rc) {
+      pos = n - L.Rc + y;
+      k = true;
+    } else {
+      y -= L.Rc;
+      int r = 0;
+      while (r < L.nrows - 1 && y >= L.rK[r] + L.rM[r]) {
+        y -= L.rK[r] + L.rM[r];
+        ++r;
+      }
+      const int64_t rb = static_cast<int64_t>(L.rj[r]) * p.batch + b;
+      k = y < L.rK[r];
+      pos = k ? __ldg(p.crit_idx + rb * p.max_crit + y) : __ldg(p.marg_idx + rb * p.max_marg + (y - L.rK[r]));
+    }
+    s_pos[x] = pos;
+    atomicOr(&need_v[pos >> 5], 1u << (pos & 31));
+    if (k) atomicOr(&need_k[pos >> 5], 1u << (pos & 31));
+  }
+  __syncthreads();
+  // (2) free the slots of positions no longer needed; collect free slots
+  for (int sl = tid; sl < t.cap; sl += kTierThreads) {
+    int pos = pos_of[sl];
+    if (pos >= 0 && !((need_v[pos >> 5] >> (pos & 31)) & 1u)) {
+      pos_of[sl] = -1;
+      flags[sl] = 0;
+      sop[pos] = -1;
+      pos = -1;
+    }
+    if (pos < 0) s_free[atomicAdd(&s_nfree, 1)] = sl;
+  }
+  __syncthreads();
+  // (3) newly needed positions (each once), then their slots
+  for (int x = tid; x < T; x += kTierThreads) {
+    const int pos = s_pos[x];
+    if (sop[pos] < 0 && !((atomicOr(&claimed[pos >> 5], 1u << (pos & 31)) >> (pos & 31)) & 1u))
+      s_miss[atomicAdd(&s_nmiss, 1)] = pos;
+  }
+  __syncthreads();
+  const int nmiss = s_nmiss, nfree = s_nfree;
+  if (tid == 0 && nmiss > nfree) atomicAdd(t.counters + 1, 1ull);
+  for (int i = tid; i < min(nmiss, nfree); i += kTierThreads) {
+    const int pos = s_miss[i], sl = s_free[i];
+    pos_of[sl] = pos;
+    flags[sl] = 0;
+    sop[pos] = sl;
+  }
+  __syncthreads();
+  // (4) entries' slots; fetch what is missing (16-byte chunks over the host link):
+  // V for every newly resident position, K where needed and absent.  Each
+  // position is fetched by its first entry (claimed bits are reused).
+  for (int i = tid; i < (n + 31) / 32; i += kTierThreads) claimed[i] = 0u;
+  __syncthreads();
+  const int32_t* bt = p.block_table + static_cast<int64_t>(b) * p.max_blocks;
+  constexpr int CH = D / 8;
+  for (int x = tid; x < T; x += kTierThreads) {
+    const int pos = s_pos[x];
+    const int sl = sop[pos];
+    es[x] = sl < 0 ? 0 : sl;
+    if (sl < 0) continue;
+    if ((atomicOr(&claimed[pos >> 5], 1u << (pos & 31)) >> (pos & 31)) & 1u) continue;
+    const uint8_t f = flags[sl];
+    const bool nk = (need_k[pos >> 5] >> (pos & 31)) & 1u;
+    const bool getv = !(f & 1u), getk = nk && !(f & 2u);
+    flags[sl] = static_cast<uint8_t>(f | 1u | (nk ? 2u : 0u));
+    if (!getv && !getk) continue;
+    const int64_t src = ((static_cast<int64_t>(__ldg(bt + (pos >> p.ps_shift))) * p.kv_heads + g) *
+                             p.page_size + (pos & (p.page_size - 1))) * D;
+    const int64_t dst = static_cast<int64_t>(sl) * D;
+    // the row's chunks, all loads issued before the stores
+    uint4 kv[2][CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      if (getv) kv[0][c] = reinterpret_cast<const uint4*>(host_v + src)[c];
+      if (getk) kv[1][c] = reinterpret_cast<const uint4*>(host_k + src)[c];
+    }
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      if (getv) reinterpret_cast<uint4*>(hot_v + dst)[c] = kv[0][c];
+      if (getk) reinterpret_cast<uint4*>(hot_k + dst)[c] = kv[1][c];
+    }
+    atomicAdd(t.counters, static_cast<unsigned long long>((getv ? 1 : 0) + (getk ? 1 : 0)));
+  }
+}
+
 }  // namespace
 
 #ifdef SKV_TRACE
@@ -896,6 +1039,19 @@ cudaError_t launch_plan(const AttendParams& p, int32_t n_layers, cudaStream_t s)
   cudaError_t e = p.head_dim == 64 ? cudaLaunchKernelEx(&cfg, plan_kernel<64>, p)
                                    : cudaLaunchKernelEx(&cfg, plan_kernel<128>, p);
   if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tier_update(const TierParams& t, cudaStream_t s) {
+  const size_t sm = static_cast<size_t>(t.cap) * 3 * sizeof(int);
+  dim3 grid(t.a.kv_heads, t.a.batch, t.layer_count);
+  if (t.a.head_dim == 64) {
+    cudaFuncSetAttribute(tier_update_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+    tier_update_kernel<64><<<grid, kTierThreads, sm, s>>>(t);
+  } else {
+    cudaFuncSetAttribute(tier_update_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+    tier_update_kernel<128><<<grid, kTierThreads, sm, s>>>(t);
+  }
   return cudaGetLastError();
 }
 

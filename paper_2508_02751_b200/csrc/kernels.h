@@ -107,7 +107,30 @@ struct AttendParams {
   int32_t group_sel;          // variant f2: selection rows are (layer, kv-group); marg_w is
                               // [L*H_kv][B][max_marg][8] per-head weights
   uint8_t* plan;              // gather plan (smallkv_plan) or nullptr
+  // variant f4 (host-tiered pool): rows come from a per-(layer, b, kv-group) hot pool
+  // [B][H_kv][hot_cap][d] per layer slot; entry e of the group's list lives in slot
+  // entry_slot[((layer*B + b)*H_kv + g)*hot_cap + e]
+  const int32_t* entry_slot;  // nullptr: the paged pool
+  int32_t hot_cap;
 };
+
+// variant f4: keep each group's needed rows in an HBM hot pool, fetching only
+// rows that were not resident at the previous step from the host-resident pool.
+struct TierParams {
+  AttendParams a;             // layout of the group lists (selection, budgets, head map)
+  const uint16_t* host_k;     // paged pool in host memory (UVA pointers), layer l = LLM layer l
+  const uint16_t* host_v;
+  uint16_t* hot_k;            // [L][B][H_kv][cap][d]
+  uint16_t* hot_v;
+  int64_t host_layer_stride;  // elements
+  int32_t* slot_of_pos;       // [L][B][H_kv][max_seq_len]  (-1: not resident)
+  int32_t* pos_of_slot;       // [L][B][H_kv][cap]          (-1: free)
+  uint8_t* slot_flags;        // [L][B][H_kv][cap]          bit0 V resident, bit1 K resident
+  int32_t* entry_slot;        // [L][B][H_kv][cap]
+  unsigned long long* counters;   // [0] rows fetched (K or V), [1] capacity overflows
+  int32_t cap, max_seq_len, layer_begin, layer_count;
+};
+cudaError_t launch_tier_update(const TierParams& p, cudaStream_t s);
 cudaError_t launch_attend(const AttendParams& p, cudaStream_t s);
 cudaError_t launch_plan(const AttendParams& p, int32_t n_layers, cudaStream_t s);
 int64_t plan_bytes(int32_t n_layers, int32_t batch, int32_t kv_heads, int32_t max_seq_len);

@@ -617,6 +617,142 @@ int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
   return SMALLKV_OK;
 }
 
+namespace {
+struct TierState {
+  size_t sop, pos_of, entry, flags, counters, total;
+};
+TierState tier_layout(const smallkv_cache* llm, const smallkv_batch* b, int32_t L, int32_t cap) {
+  TierState t;
+  const size_t groups = static_cast<size_t>(L) * b->batch * llm->num_kv_heads;
+  t.sop = 0;
+  t.pos_of = round256(groups * b->max_seq_len * 4);
+  t.entry = t.pos_of + round256(groups * cap * 4);
+  t.flags = t.entry + round256(groups * cap * 4);
+  t.counters = t.flags + round256(groups * cap);
+  t.total = t.counters + 256;
+  return t;
+}
+int check_tier(const smallkv_cache* llm, const smallkv_batch* batch, int32_t L, int32_t cap) {
+  if (!llm || !batch) return fail(SMALLKV_ERR_NULL, "tier: NULL cache/batch");
+  if (L < 1 || cap < 4 || cap % 4 != 0 || cap > 65536)
+    return fail(SMALLKV_ERR_SHAPE, "tier: layers %d / capacity %d (multiple of 4 in [4,65536])", L, cap);
+  if (batch->max_seq_len > 32768) return fail(SMALLKV_ERR_SHAPE, "tier: max_seq_len > 32768");
+  return SMALLKV_OK;
+}
+}  // namespace
+
+size_t smallkv_tier_state_size(const smallkv_cache* llm, const smallkv_batch* batch,
+                               int32_t n_llm_layers, int32_t capacity) {
+  if (check_tier(llm, batch, n_llm_layers, capacity) != SMALLKV_OK) return 0;
+  return tier_layout(llm, batch, n_llm_layers, capacity).total;
+}
+
+int smallkv_tier_init(void* state, size_t state_bytes, const smallkv_cache* llm,
+                      const smallkv_batch* batch, int32_t n_llm_layers, int32_t capacity,
+                      void* stream) {
+  int rc;
+  if ((rc = check_tier(llm, batch, n_llm_layers, capacity)) != SMALLKV_OK) return rc;
+  const TierState T = tier_layout(llm, batch, n_llm_layers, capacity);
+  if (!state || state_bytes < T.total)
+    return fail(SMALLKV_ERR_WORKSPACE, "tier state %zu < %zu bytes", state_bytes, T.total);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint8_t* st = static_cast<uint8_t*>(state);
+  cudaError_t e = cudaMemsetAsync(st, 0xff, T.flags, s);            // maps = -1
+  if (e == cudaSuccess) e = cudaMemsetAsync(st + T.flags, 0, T.total - T.flags, s);
+  if (e != cudaSuccess) return cuda_fail(e, "tier init");
+  return SMALLKV_OK;
+}
+
+int smallkv_tier_update(int32_t layer_begin, int32_t layer_count, const smallkv_cache* host_llm,
+                        uint16_t* hot_k, uint16_t* hot_v, int32_t capacity,
+                        const smallkv_batch* batch, const int32_t* head_map, int32_t n_llm_layers,
+                        int32_t slm_heads_total, const smallkv_budgets* budgets,
+                        const int32_t* crit_idx, const int32_t* marg_idx, const float* marg_w,
+                        const int32_t* counts, int32_t flags, void* state, size_t state_bytes,
+                        void* stream) {
+  skv::TierParams tp{};
+  int rc = fill_attend_params(tp.a, host_llm, batch, head_map, n_llm_layers, slm_heads_total,
+                              budgets, crit_idx, marg_idx, marg_w, counts);
+  if (rc != SMALLKV_OK) return rc;
+  if ((rc = check_tier(host_llm, batch, n_llm_layers, capacity)) != SMALLKV_OK) return rc;
+  if (!hot_k || !hot_v) return fail(SMALLKV_ERR_NULL, "tier: NULL hot pool");
+  if (flags & ~SMALLKV_ATTEND_GROUP_SELECTION) return fail(SMALLKV_ERR_SHAPE, "tier: unknown flags");
+  if (layer_begin < 0 || layer_count < 1 || layer_begin + layer_count > n_llm_layers ||
+      host_llm->num_layers < n_llm_layers || layer_count > 65535)
+    return fail(SMALLKV_ERR_SHAPE, "tier: layers [%d,%d) vs %d LLM / %d pool layers", layer_begin,
+                layer_begin + layer_count, n_llm_layers, host_llm->num_layers);
+  const TierState T = tier_layout(host_llm, batch, n_llm_layers, capacity);
+  if (!state || state_bytes < T.total)
+    return fail(SMALLKV_ERR_WORKSPACE, "tier state %zu < %zu bytes", state_bytes, T.total);
+  if (!aligned(hot_k, 16) || !aligned(hot_v, 16)) return fail(SMALLKV_ERR_ALIGN, "hot pools 16-byte aligned");
+  if ((rc = check_device()) != SMALLKV_OK) return rc;
+  uint8_t* st = static_cast<uint8_t*>(state);
+  tp.a.group_sel = (flags & SMALLKV_ATTEND_GROUP_SELECTION) ? 1 : 0;
+  tp.host_k = host_llm->k;
+  tp.host_v = host_llm->v;
+  tp.host_layer_stride = static_cast<int64_t>(host_llm->num_pages) * host_llm->num_kv_heads *
+                         host_llm->page_size * host_llm->head_dim;
+  tp.hot_k = hot_k;
+  tp.hot_v = hot_v;
+  tp.slot_of_pos = reinterpret_cast<int32_t*>(st + T.sop);
+  tp.pos_of_slot = reinterpret_cast<int32_t*>(st + T.pos_of);
+  tp.entry_slot = reinterpret_cast<int32_t*>(st + T.entry);
+  tp.slot_flags = st + T.flags;
+  tp.counters = reinterpret_cast<unsigned long long*>(st + T.counters);
+  tp.cap = capacity;
+  tp.max_seq_len = batch->max_seq_len;
+  tp.layer_begin = layer_begin;
+  tp.layer_count = layer_count;
+  cudaError_t e = skv::launch_tier_update(tp, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "tier_update launch");
+  return SMALLKV_OK;
+}
+
+int smallkv_attend_tiered(int32_t llm_layer, const uint16_t* q, const smallkv_cache* host_llm,
+                          const uint16_t* hot_k, const uint16_t* hot_v, int32_t capacity,
+                          const void* state, const smallkv_batch* batch, const int32_t* head_map,
+                          int32_t n_llm_layers, int32_t slm_heads_total,
+                          const smallkv_budgets* budgets, const int32_t* crit_idx,
+                          const int32_t* marg_idx, const float* marg_w, const int32_t* counts,
+                          float* out, int32_t flags, void* ws, size_t ws_bytes, void* stream) {
+  skv::AttendParams ap;
+  int rc = fill_attend_params(ap, host_llm, batch, head_map, n_llm_layers, slm_heads_total, budgets,
+                              crit_idx, marg_idx, marg_w, counts);
+  if (rc != SMALLKV_OK) return rc;
+  if ((rc = check_tier(host_llm, batch, n_llm_layers, capacity)) != SMALLKV_OK) return rc;
+  if (!q || !out || !hot_k || !hot_v || !state)
+    return fail(SMALLKV_ERR_NULL, "smallkv_attend_tiered: NULL pointer");
+  if (llm_layer < 0 || llm_layer >= n_llm_layers)
+    return fail(SMALLKV_ERR_SHAPE, "tiered attend: layer %d outside [0,%d)", llm_layer, n_llm_layers);
+  if (flags & ~(SMALLKV_ATTEND_OVERLAP_PROLOGUE | SMALLKV_ATTEND_GROUP_SELECTION))
+    return fail(SMALLKV_ERR_SHAPE, "unknown smallkv_attend flags 0x%x", flags);
+  if (!aligned(q, 4) || !aligned(out, 16) || !aligned(hot_k, 16) || !aligned(hot_v, 16))
+    return fail(SMALLKV_ERR_ALIGN, "q 4-byte, out / hot pools 16-byte aligned");
+  if (static_cast<int64_t>(batch->batch) * host_llm->num_kv_heads * capacity * host_llm->head_dim >=
+      (int64_t(1) << 32))
+    return fail(SMALLKV_ERR_SHAPE, "one layer of the hot pool must have < 2^32 elements");
+  const AttendWs W = attend_ws_layout(host_llm, batch);
+  if (!ws || ws_bytes < W.total)
+    return fail(SMALLKV_ERR_WORKSPACE, "attend workspace %zu < %zu bytes", ws_bytes, W.total);
+  if ((rc = check_device()) != SMALLKV_OK) return rc;
+  const TierState T = tier_layout(host_llm, batch, n_llm_layers, capacity);
+  ap.q = q;
+  ap.out = out;
+  ap.layer = llm_layer;
+  ap.k = hot_k;
+  ap.v = hot_v;
+  ap.layer_offset = static_cast<int64_t>(llm_layer) * batch->batch * host_llm->num_kv_heads * capacity *
+                    host_llm->head_dim;
+  ap.overlap_prologue = (flags & SMALLKV_ATTEND_OVERLAP_PROLOGUE) ? 1 : 0;
+  ap.group_sel = (flags & SMALLKV_ATTEND_GROUP_SELECTION) ? 1 : 0;
+  ap.plan = nullptr;
+  ap.entry_slot = reinterpret_cast<const int32_t*>(static_cast<const uint8_t*>(state) + T.entry);
+  ap.hot_cap = capacity;
+  cudaError_t e = skv::launch_attend(ap, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "attend launch");
+  return SMALLKV_OK;
+}
+
 int smallkv_match_window(int32_t n, int32_t w_min, int32_t w_max, int32_t keep_last,
                          int32_t* start, int32_t* len) {
   if (!start || !len) return fail(SMALLKV_ERR_NULL, "smallkv_match_window: NULL output");

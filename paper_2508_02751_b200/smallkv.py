@@ -33,6 +33,8 @@ EXPORTS = ("smallkv_last_error", "smallkv_version", "smallkv_budget_from_tau",
            "smallkv_select_group_workspace_size", "smallkv_select_group",
            "smallkv_plan_size", "smallkv_plan", "smallkv_plan_group",
            "smallkv_attend_workspace_size", "smallkv_attend",
+           "smallkv_tier_state_size", "smallkv_tier_init", "smallkv_tier_update",
+           "smallkv_attend_tiered",
            "smallkv_match_window", "smallkv_prefill_scores",
            "smallkv_match_heads_workspace_size", "smallkv_match_heads",
            "smallkv_workspace_init")
@@ -93,6 +95,13 @@ def load(path: Optional[str] = None):
         lib.smallkv_plan_size.argtypes = [P, P, i32]
         lib.smallkv_plan_size.restype = sz
         lib.smallkv_plan.argtypes = [P, P, P, i32, i32, P, P, P, P, P, P, sz, P]
+        lib.smallkv_tier_state_size.argtypes = [P, P, i32, i32]
+        lib.smallkv_tier_state_size.restype = sz
+        lib.smallkv_tier_init.argtypes = [P, sz, P, P, i32, i32, P]
+        lib.smallkv_tier_update.argtypes = [i32, i32, P, P, P, i32, P, P, i32, i32, P, P, P, P,
+                                            P, i32, P, sz, P]
+        lib.smallkv_attend_tiered.argtypes = [i32, P, P, P, P, i32, P, P, P, i32, i32, P, P, P,
+                                              P, P, P, i32, P, sz, P]
         lib.smallkv_match_window.argtypes = [i32, i32, i32, i32, P, P]
         lib.smallkv_prefill_scores.argtypes = [P, P, i32, i32, i32, P, P]
         lib.smallkv_match_heads_workspace_size.argtypes = [i32, i32]
@@ -309,6 +318,79 @@ class DecodeStep:
         return out
 
 
+class TieredKV:
+    """Variant f4 (R18): the LLM's paged K/V pool lives in pinned host
+    memory; each (layer, sequence, kv-group) keeps the rows its current list
+    needs in an HBM hot pool of `capacity` slots, refreshed per layer by
+    smallkv_tier_update (only rows not resident at the previous step cross the
+    host link) and read by smallkv_attend_tiered."""
+
+    def __init__(self, step: DecodeStep, host_k: torch.Tensor, host_v: torch.Tensor,
+                 capacity: int):
+        """host_k / host_v: pinned CPU pools [L][pages][kv][ps][d] (layer l = LLM layer l)."""
+        assert host_k.device.type == "cpu" and host_k.is_pinned() and host_v.is_pinned()
+        assert host_k.shape[0] >= step.llm_layers
+        self.step = step
+        self.lib = step.lib
+        bt_keep = step._keep[4]   # llm block table (device)
+        self.host = make_cache(host_k, host_v, bt_keep, step.llm.num_q_heads)
+        self._keep = (host_k, host_v)
+        B, H_kv, d = step.batch.batch, step.llm.num_kv_heads, step.llm.head_dim
+        dev = bt_keep.device
+        self.capacity = int(capacity)
+        self.hot_k = torch.zeros(step.llm_layers, B, H_kv, capacity, d, dtype=torch.bfloat16,
+                                 device=dev)
+        self.hot_v = torch.zeros_like(self.hot_k)
+        nb = self.lib.smallkv_tier_state_size(ctypes.byref(self.host), ctypes.byref(step.batch),
+                                              step.llm_layers, self.capacity)
+        if nb == 0:
+            raise SmallKVError("smallkv_tier_state_size", 2, "invalid dimensions / capacity")
+        self.state = torch.empty(nb, dtype=torch.uint8, device=dev)
+        self.reset()
+
+    def reset(self, stream=None):
+        _check("smallkv_tier_init",
+               self.lib.smallkv_tier_init(self.state.data_ptr(), self.state.numel(),
+                                          ctypes.byref(self.host), ctypes.byref(self.step.batch),
+                                          self.step.llm_layers, self.capacity, _stream(stream)))
+
+    def _sel(self):
+        st = self.step
+        group = st.variant == "f2"
+        return (st.gout if group else st.out), (ATTEND_GROUP_SELECTION if group else 0)
+
+    def update(self, layer_begin: int = 0, layer_count: Optional[int] = None, stream=None):
+        """Refresh the hot pools of LLM layers [layer_begin, layer_begin+layer_count)."""
+        st = self.step
+        o, gflag = self._sel()
+        count = st.llm_layers - layer_begin if layer_count is None else layer_count
+        _check("smallkv_tier_update", self.lib.smallkv_tier_update(
+            int(layer_begin), int(count), ctypes.byref(self.host), self.hot_k.data_ptr(),
+            self.hot_v.data_ptr(), self.capacity, ctypes.byref(st.batch),
+            st.head_map.data_ptr(), st.llm_layers, st.n_slm, ctypes.byref(st.budgets),
+            o.crit.data_ptr(), o.marg.data_ptr(), o.marg_w.data_ptr(), o.counts.data_ptr(), gflag,
+            self.state.data_ptr(), self.state.numel(), _stream(stream)))
+
+    def attend(self, llm_layer: int, q: torch.Tensor, out: torch.Tensor, stream=None,
+               overlap_prologue: bool = False):
+        st = self.step
+        o, gflag = self._sel()
+        _check("smallkv_attend_tiered", self.lib.smallkv_attend_tiered(
+            int(llm_layer), q.data_ptr(), ctypes.byref(self.host),
+            self.hot_k.data_ptr(), self.hot_v.data_ptr(), self.capacity, self.state.data_ptr(),
+            ctypes.byref(st.batch), st.head_map.data_ptr(), st.llm_layers, st.n_slm,
+            ctypes.byref(st.budgets), o.crit.data_ptr(), o.marg.data_ptr(), o.marg_w.data_ptr(),
+            o.counts.data_ptr(), out.data_ptr(),
+            (ATTEND_OVERLAP_PROLOGUE if overlap_prologue else 0) | gflag,
+            st.ws_attend.data_ptr(), st.ws_attend.numel(), _stream(stream)))
+        return out
+
+    def counters(self):
+        """(rows fetched from host memory so far, capacity overflows)."""
+        c = self.state[-256:][:16].view(torch.int64).cpu()   # counters live at the end
+        return int(c[0]), int(c[1])
+
+
 def from_problem(p, use_plan: bool = True, variant: str = "default") -> DecodeStep:
     """DecodeStep for a smallkv_synth.Problem already on the GPU."""
     return DecodeStep(slm_k=p.slm.k, slm_block_table=p.slm.block_table,
@@ -382,8 +464,9 @@ class DecodeGraph:
     """
 
     def __init__(self, step: DecodeStep, slm_q: torch.Tensor, layer_plan, timing: bool = False,
-                 host_io=None):
+                 host_io=None, tier: Optional["TieredKV"] = None):
         self.step = step
+        self.tier = tier   # variant f4: (tier_update, tiered attend) per layer
         self.slm_q = slm_q
         self.plan = list(layer_plan)
         self.timing = timing
@@ -407,6 +490,15 @@ class DecodeGraph:
     def _calls(self, record: bool):
         if self.host_io is not None:
             return self._calls_host_io()
+        if self.tier is not None:
+            # f4: one refresh of every layer's hot pool right after select (ahead
+            # of the attends), then the attends; the first attend reads
+            # what the refresh wrote, so only later ones overlap their prologue
+            self.step.select(self.slm_q)
+            self.tier.update()
+            for i, (layer, slot, q, out) in enumerate(self.plan):
+                self.tier.attend(layer, q, out, overlap_prologue=i > 0)
+            return
         if record:
             self.events[0].record()
         self.step.select(self.slm_q)
@@ -467,5 +559,6 @@ class DecodeGraph:
         nl = self.step.slm.num_layers
         chunks = min(4, nl) if self.step.aux_stream is not None else 1
         sel = 2 * chunks if self.step.variant == "default" else 4   # f2: + group score, weights
-        return (1 + sel + (1 if self.step.plan_buf is not None else 0)
+        tier = 1 if self.tier is not None else 0                   # f4: + one tier_update
+        return (1 + sel + tier + (1 if self.step.plan_buf is not None else 0)
                 + len(self.plan))

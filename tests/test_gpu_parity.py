@@ -468,3 +468,71 @@ def test_f3_head_matching_end_to_end():
                           2, 8, 2, 128)
     refl = oracle.prefill_scores(ql, lv, 0, start, length)
     assert np.abs(Fl.cpu().double().numpy() - refl).max() <= 1e-4 * max(1.0, refl.max())
+
+
+# ---------------------------------------------------------------- variant f4 (R18)
+
+def _tiered_step(p, variant="default"):
+    from paper_2508_02751_b200 import smallkv
+    step = smallkv.from_problem(p, use_plan=False, variant=variant)
+    host_k = torch.empty(p.llm.k.shape, dtype=p.llm.k.dtype, pin_memory=True)
+    host_v = torch.empty(p.llm.v.shape, dtype=p.llm.v.dtype, pin_memory=True)
+    host_k.copy_(p.llm.k)
+    host_v.copy_(p.llm.v)
+    G = p.cfg.llm.q_heads // p.cfg.llm.kv_heads
+    cap = -(-(int(p.n_recent.max()) + G * (p.max_crit + p.max_marg)) // 4) * 4
+    tier = smallkv.TieredKV(step, host_k, host_v, capacity=cap)
+    return step, tier
+
+
+def _run_both(p, step, tier, slm_q):
+    """One decode step through the HBM pool and through the tiered pool."""
+    step.select(slm_q)
+    tier.update()
+    outs = []
+    for slot in range(p.llm.num_layers):
+        layer = p.llm_layer_ids[slot]
+        assert layer == slot   # f4: pool layer l holds LLM layer l
+        ref = torch.empty(p.batch, p.cfg.llm.q_heads, p.cfg.llm.head_dim, device="cuda")
+        got = torch.empty_like(ref)
+        step.attend(layer, slot, p.llm_q[slot], ref)
+        tier.attend(layer, p.llm_q[slot], got)
+        outs.append((ref, got))
+    torch.cuda.synchronize()
+    return outs
+
+
+@pytest.mark.parametrize("variant,map_kind", [("default", "coherent"), ("default", "random"),
+                                              ("f2", "random")])
+def test_f4_tiered_pool_bitwise(variant, map_kind):
+    """Host-resident pool + HBM hot pool: outputs bitwise equal to the
+    HBM-resident path; a repeated step fetches nothing; a changed SLM query
+    fetches only rows that were not resident."""
+    cfg = _cfg(llm=(2, 8, 2, 128), slm=(2, 8, 2, 64), n=1500, B=3, budget=(150, 60, 200))
+    p = synth.make_problem(cfg, seed=41, page_size=16, seq_lens=[1500, 700, 1],
+                           map_kind=map_kind).to("cuda")
+    step, tier = _tiered_step(p, variant)
+    for ref, got in _run_both(p, step, tier, p.slm_q):
+        assert torch.equal(ref, got)
+    f1, ov = tier.counters()
+    assert ov == 0 and f1 > 0
+    for ref, got in _run_both(p, step, tier, p.slm_q):      # same step again: all resident
+        assert torch.equal(ref, got)
+    f2_, _ = tier.counters()
+    assert f2_ == f1, (f1, f2_)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    q2 = (p.slm_q.float() + 0.5 * torch.randn(p.slm_q.shape, device="cuda", generator=g)).to(torch.bfloat16)
+    for ref, got in _run_both(p, step, tier, q2):            # drifted selection: partial refetch
+        assert torch.equal(ref, got)
+    f3, ov = tier.counters()
+    assert ov == 0 and f1 < f3 < 2 * f1, (f1, f3)
+    print("f4", variant, map_kind, "rows fetched: first step", f1, "drifted step", f3 - f1)
+    # and against the oracle on the GPU's own lists (default selection)
+    if variant == "default":
+        both = _run_both(p, step, tier, p.slm_q)   # back to the original query
+        sel = parity.oracle_select(p)
+        parity.compare_select(p, step.out, sel)
+        sg = parity.sel_from_gpu(p, step.out, sel)
+        for slot, (ref, got) in enumerate(both):
+            e, _ = parity.compare_attend(p, slot, got, sg)
+            assert e <= parity.OUT_TOL
