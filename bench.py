@@ -100,7 +100,7 @@ def build_problem(cfg_name: str, rank: int, world: int, shard: str, device):
     import smallkv_synth as synth
     from paper_2508_02751_b200 import dist as pdist
     cfg = synth.CONFIGS[cfg_name]
-    heads = shard == "heads" and world > 1
+    heads = shard in ("heads", "heads-slm") and world > 1
     kv_share = cfg.llm.kv_heads // world if heads else cfg.llm.kv_heads
     # resident LLM layers: all when they fit, else a rotating subset (each slice >> L2)
     per_layer = cfg.batch * kv_share * cfg.seq_len * cfg.llm.head_dim * 2 * 2
@@ -118,9 +118,11 @@ def build_problem(cfg_name: str, rank: int, world: int, shard: str, device):
         k, v, q, hm = pdist.slice_llm_kv_groups(p.llm.k, p.llm.v, p.llm_q, p.head_map, L, H,
                                                 Hkv, g0, g1)
         dims = synth.ModelDims(L, (g1 - g0) * (H // Hkv), g1 - g0, cfg.llm.head_dim)
+        full_hm = p.head_map
         p = dataclasses.replace(p, cfg=dataclasses.replace(cfg, llm=dims),
                                 llm=dataclasses.replace(p.llm, k=k, v=v, dims=dims),
                                 llm_q=q, head_map=hm)
+        p.full_head_map = full_hm   # f3b: the SLM row blocks are cut from the full map
         torch.cuda.empty_cache()
     return p, resident
 
@@ -140,7 +142,8 @@ def run_ours(args, world, rank, local):
         dist.barrier()
     from paper_2508_02751_b200 import bytes_model, smallkv
 
-    heads = args.shard == "heads" and world > 1
+    heads = args.shard in ("heads", "heads-slm") and world > 1
+    slm_part = args.shard == "heads-slm" and world > 1
     p, resident = build_problem(args.config, rank, world, args.shard, device)
     cfg = p.cfg
     L = cfg.llm.layers
@@ -166,6 +169,23 @@ def run_ours(args, world, rank, local):
                        device=device)
     plan = [(l, l % resident, p.llm_q[l % resident], outs[l]) for l in range(L)]
     graph = smallkv.DecodeGraph(step, p.slm_q, plan, timing=False, tier=tier)
+    if slm_part:
+        # f3b: this rank scores / splits only its block of SLM rows, the blocks
+        # are all-gathered (NCCL), then the plan and this rank's kv-group attends
+        # run on the exchanged selection; the step runs eagerly (collective inside)
+        from paper_2508_02751_b200 import dist as pdist
+        n_slm = cfg.slm.layers * cfg.slm.q_heads
+        j0, j1 = pdist.slm_row_block(n_slm, world, rank)
+        shm = pdist.select_head_map(p.full_head_map.to(device), j0, j1)
+
+        def replay_f3b():
+            with torch.cuda.stream(graph.stream):
+                step.select(p.slm_q, select_head_map=shm, plan=False)
+                pdist.exchange_selection(step.out, n_slm)
+                step.plan()
+                for i, (layer, slot, q, out) in enumerate(plan):
+                    step.attend(layer, slot, q, out, overlap_prologue=i > 0)
+        graph.replay = replay_f3b
     if heads:
         # the exchange step of head sharding: all-gather every layer's per-head
         # outputs [L, B, H/w, d] -> [L, B, H, d] once per step (NCCL / NVLink)
@@ -347,8 +367,11 @@ def run_ours(args, world, rank, local):
             "workload": f"{args.config}: {cfg.description}",
             "global_batch": p.batch * units,
             "seq_len": cfg.seq_len,
-            "parallelism": (f"kv-head-group sharded x{world} (+1 NCCL all-gather of outputs "
-                            "per step)" if heads else f"batch-sharded x{world} (no collective)"),
+            "parallelism": (f"kv-head-group sharded x{world}"
+                            + (" + SLM row blocks (f3b: +1 NCCL all-gather of the selection)"
+                               if slm_part else "")
+                            + " (+1 NCCL all-gather of outputs per step)"
+                            if heads else f"batch-sharded x{world} (no collective)"),
             "budget_K_R_M": list(cfg.budget),
             "head_map": "coherent (every SLM kv-head referenced)",
             "selection": ("f2: one split per LLM (layer, kv-group) of the summed proxy rows "
@@ -551,7 +574,7 @@ def main():
     ap.add_argument("--variant", choices=["default", "f2", "f4"], default="default",
                     help="f2: per-KV-group shared selection (SURVEY §8(f) f2, DESIGN.md R16); "
                          "f4: host-tiered KV pool (SURVEY §8(f) f4, DESIGN.md R18)")
-    ap.add_argument("--shard", choices=["batch", "heads"], default="batch",
+    ap.add_argument("--shard", choices=["batch", "heads", "heads-slm"], default="batch",
                     help="N>1 partition: sequences (weak scaling) or LLM kv-head groups")
     ap.add_argument("--cpu-seqs", type=int, default=4,
                     help="sequences per step of the --impl reference sample")

@@ -246,10 +246,14 @@ class DecodeStep:
             self.ws_select = torch.zeros(ws_g, dtype=torch.uint8, device=dev)
         self.aux_stream = torch.cuda.Stream(device=dev) if overlap_select else None
 
-    def select(self, slm_q: torch.Tensor, stream=None, acc: Optional[torch.Tensor] = None):
+    def select(self, slm_q: torch.Tensor, stream=None, acc: Optional[torch.Tensor] = None,
+               select_head_map: Optional[torch.Tensor] = None, plan: bool = True):
         """smallkv_select, then (by default) smallkv_plan for every layer.
         acc: optional fp32 [l*H_s][B][max_seq_len] running column sums (variant
-        f1, zero-filled once by the caller; updated in place)."""
+        f1, zero-filled once by the caller; updated in place).
+        select_head_map: optional head-map subset that defines which SLM rows
+        are scored and split (f3b: a rank's row block, dist.select_head_map);
+        plan=False skips smallkv_plan (call plan() after the selection exchange)."""
         assert slm_q.dtype == torch.bfloat16 and slm_q.is_contiguous()
         if acc is not None:
             assert acc.dtype == torch.float32 and acc.is_contiguous()
@@ -259,13 +263,25 @@ class DecodeStep:
             return self._select_group(slm_q, stream)
         o = self.out
         aux = self.aux_stream.cuda_stream if self.aux_stream is not None else None
+        shm = self.head_map if select_head_map is None else select_head_map
+        assert shm.dtype == torch.int32 and shm.is_contiguous()
+        self.planned = False
+        if shm.numel() == 0:
+            return o   # no row of this block is used
         rc = self.lib.smallkv_select(
             slm_q.data_ptr(), ctypes.byref(self.slm), ctypes.byref(self.batch),
-            self.head_map.data_ptr(), self.head_map.numel(), ctypes.byref(self.budgets),
+            shm.data_ptr(), shm.numel(), ctypes.byref(self.budgets),
             o.logits.data_ptr(), o.lse.data_ptr(), o.crit.data_ptr(), o.marg.data_ptr(),
             o.marg_w.data_ptr(), o.counts.data_ptr(), _ptr(acc), self.ws_select.data_ptr(),
             self.ws_select.numel(), _stream(stream), aux)
         _check("smallkv_select", rc)
+        if plan:
+            self.plan(stream)
+        return o
+
+    def plan(self, stream=None):
+        """smallkv_plan for every layer from the current selection outputs."""
+        o = self.out
         self.planned = False
         if self.plan_buf is not None:
             rc = self.lib.smallkv_plan(

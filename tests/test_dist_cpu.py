@@ -71,3 +71,53 @@ def test_kv_group_ranges_and_head_map_slice():
     assert torch.equal(torch.cat(parts, dim=1).view(-1), hm)
     with pytest.raises(ValueError):
         pdist.kv_group_range(6, 4, 0)
+
+
+def _exchange_worker(rank: int, world: int, port: int, q):
+    import types
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n_slm, B = 7, 3
+        g = torch.Generator().manual_seed(5)
+        ref = types.SimpleNamespace(
+            lse=torch.randn(n_slm, B, 2, generator=g),
+            crit=torch.randint(0, 99, (n_slm, B, 4), generator=g, dtype=torch.int32),
+            marg=torch.randint(0, 99, (n_slm, B, 5), generator=g, dtype=torch.int32),
+            marg_w=torch.rand(n_slm, B, 5, generator=g),
+            counts=torch.randint(0, 4, (n_slm, B, 2), generator=g, dtype=torch.int32))
+        # each rank only computed its own block; other rows hold garbage
+        mine = types.SimpleNamespace(**{k: torch.full_like(v, -7) for k, v in vars(ref).items()})
+        j0, j1 = pdist.slm_row_block(n_slm, world, rank)
+        for k in vars(ref):
+            getattr(mine, k)[j0:j1] = getattr(ref, k)[j0:j1]
+        pdist.exchange_selection(mine, n_slm)
+        ok = all(torch.equal(getattr(mine, k), getattr(ref, k)) for k in vars(ref))
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_f3b_slm_row_blocks_and_selection_exchange():
+    """f3b host logic: SLM row blocks partition [0, n_slm); the head-map subset
+    of a block maps only into it; after the gloo all-gather every rank holds
+    every row of the selection outputs."""
+    for n_slm, w in [(7, 2), (336, 4), (3, 8)]:
+        blocks = [pdist.slm_row_block(n_slm, w, r) for r in range(w)]
+        cover = [j for a, b in blocks for j in range(a, b)]
+        assert cover == list(range(n_slm))
+    hm = torch.tensor([5, 0, 6, 2, 2, 3], dtype=torch.int32)
+    assert pdist.select_head_map(hm, 0, 3).tolist() == [0, 2, 2]
+    assert pdist.select_head_map(hm, 3, 7).tolist() == [5, 6, 3]
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_exchange_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+    assert all(ok for _, ok in res), res

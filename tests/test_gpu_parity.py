@@ -536,3 +536,30 @@ def test_f4_tiered_pool_bitwise(variant, map_kind):
         for slot, (ref, got) in enumerate(both):
             e, _ = parity.compare_attend(p, slot, got, sg)
             assert e <= parity.OUT_TOL
+
+
+def test_f3b_partitioned_slm_virtual_ranks_bit_identical():
+    """f3b on one GPU with 2 virtual ranks: each scores / splits only its SLM row
+    block (head-map subset), the blocks are exchanged (row copies standing in for
+    the all-gather), and the attention over the exchanged selection is bitwise
+    equal to the unsharded step."""
+    from paper_2508_02751_b200 import dist as pdist, smallkv
+    cfg = _cfg(llm=(2, 8, 2, 128), slm=(2, 8, 2, 64), n=1500, B=3)
+    p = synth.make_problem(cfg, seed=51, page_size=16, seq_lens=[1500, 800, 33],
+                           map_kind="random").to("cuda")
+    _, _, full = parity.run_gpu_step(p)
+    n_slm = cfg.slm.layers * cfg.slm.q_heads
+    steps = [smallkv.from_problem(p) for _ in range(2)]
+    for r, st in enumerate(steps):
+        j0, j1 = pdist.slm_row_block(n_slm, 2, r)
+        st.select(p.slm_q, select_head_map=pdist.select_head_map(p.head_map, j0, j1), plan=False)
+    target = steps[0]
+    for name in pdist.SELECTION_FIELDS:
+        j0, j1 = pdist.slm_row_block(n_slm, 2, 1)
+        getattr(target.out, name)[j0:j1] = getattr(steps[1].out, name)[j0:j1]
+    target.plan()
+    for slot in range(p.llm.num_layers):
+        out = torch.empty_like(full[slot])
+        target.attend(p.llm_layer_ids[slot], slot, p.llm_q[slot], out, overlap_prologue=slot > 0)
+        torch.cuda.synchronize()
+        assert torch.equal(out, full[slot])
