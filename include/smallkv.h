@@ -341,7 +341,10 @@ int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
  * step are not moved.  capacity must be a multiple of 4 and >= the list size
  * R' + (#distinct rows)·(K' + M') of every group, else the group is skipped
  * and counted as an overflow (its outputs are then undefined).
- * smallkv_attend_tiered: smallkv_attend reading the hot pool (no plan).
+ * smallkv_plan_tiered: smallkv_plan over the hot-pool slots (after
+ * smallkv_tier_update; plan size as smallkv_plan_size).
+ * smallkv_attend_tiered: smallkv_attend reading the hot pool (plan: NULL or
+ * smallkv_plan_tiered's).
  * flags: SMALLKV_ATTEND_GROUP_SELECTION for variant f2 selections.
  * Errors: as smallkv_attend, plus max_seq_len > 32768 or bad capacity
  * (SMALLKV_ERR_SHAPE), small state (SMALLKV_ERR_WORKSPACE).
@@ -358,6 +361,12 @@ int smallkv_tier_update(int32_t layer_begin, int32_t layer_count, const smallkv_
                         const smallkv_budgets* budgets, const int32_t* crit_idx,
                         const int32_t* marg_idx, const float* marg_w, const int32_t* counts,
                         int32_t flags, void* state, size_t state_bytes, void* stream);
+int smallkv_plan_tiered(const smallkv_cache* host_llm, int32_t capacity, const void* state,
+                        const smallkv_batch* batch, const int32_t* head_map,
+                        int32_t n_llm_layers, int32_t slm_heads_total,
+                        const smallkv_budgets* budgets, const int32_t* crit_idx,
+                        const int32_t* marg_idx, const float* marg_w, const int32_t* counts,
+                        int32_t flags, void* plan, size_t plan_bytes, void* stream);
 int smallkv_attend_tiered(int32_t llm_layer, const uint16_t* q,
                           const smallkv_cache* host_llm, const uint16_t* hot_k,
                           const uint16_t* hot_v, int32_t capacity, const void* state,
@@ -365,8 +374,8 @@ int smallkv_attend_tiered(int32_t llm_layer, const uint16_t* q,
                           int32_t n_llm_layers, int32_t slm_heads_total,
                           const smallkv_budgets* budgets, const int32_t* crit_idx,
                           const int32_t* marg_idx, const float* marg_w,
-                          const int32_t* counts, float* out, int32_t flags, void* ws,
-                          size_t ws_bytes, void* stream);
+                          const int32_t* counts, const void* plan, float* out, int32_t flags,
+                          void* ws, size_t ws_bytes, void* stream);
 
 /*
  * Variant f3 (R17) — the prefill side of matching.

@@ -297,17 +297,29 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const AttendParams p
         }
       }
     }
-    int page[U];
+    uint32_t ro[U];
+    if (p.entry_slot) {
+      // variant f4: the entry's hot-pool slot, row ((b*H_kv + g)*cap + slot)
+      const int32_t* es = p.entry_slot + ((static_cast<int64_t>(layer) * p.batch + b) * p.kv_heads + g) * p.hot_cap;
 #pragma unroll
-    for (int u = 0; u < U; ++u) page[u] = slot_i[u] >= 0 ? __ldg(bt + (pos[u] >> p.ps_shift)) : 0;
+      for (int u = 0; u < U; ++u)
+        ro[u] = slot_i[u] < 0 ? 0u : static_cast<uint32_t>(
+            ((static_cast<int64_t>(b) * p.kv_heads + g) * p.hot_cap + __ldg(es + base + u * kPlanThreads)) * D);
+    } else {
+      int page[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) page[u] = slot_i[u] >= 0 ? __ldg(bt + (pos[u] >> p.ps_shift)) : 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        ro[u] = static_cast<uint32_t>(((static_cast<int64_t>(page[u]) * p.kv_heads + g) * p.page_size +
+                                       (pos[u] & (p.page_size - 1))) * D);
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (slot_i[u] < 0) continue;
       const int c = slot_i[u] / kBatch, i = slot_i[u] % kBatch;
       uint32_t* slot = reinterpret_cast<uint32_t*>(rec + kHdrBytes) + static_cast<int64_t>(c) * kBatch * 3;
-      slot[i] = static_cast<uint32_t>(
-          ((static_cast<int64_t>(page[u]) * p.kv_heads + g) * p.page_size +
-           (pos[u] & (p.page_size - 1))) * D);
+      slot[i] = ro[u];
       slot[kBatch + i] = mk[u];
       reinterpret_cast<float*>(slot)[2 * kBatch + i] = wt[u];
     }
@@ -929,13 +941,14 @@ __global__ void __launch_bounds__(kTierThreads) tier_update_kernel(const TierPar
     sop[pos] = sl;
   }
   __syncthreads();
-  // (4) entries' slots; fetch what is missing (16-byte chunks over the host link):
-  // V for every newly resident position, K where needed and absent.  Each
-  // position is fetched by its first entry (claimed bits are reused).
+  // (4) entries' slots, residency flags, and one fetch job per position that
+  // misses V (new) or K (needed by a critical / recent entry); each position is
+  // handled by its first entry (claimed bits are reused)
   for (int i = tid; i < (n + 31) / 32; i += kTierThreads) claimed[i] = 0u;
+  if (tid == 0) s_nmiss = 0;
   __syncthreads();
-  const int32_t* bt = p.block_table + static_cast<int64_t>(b) * p.max_blocks;
-  constexpr int CH = D / 8;
+  int* s_job = s_free;   // slot | getv << 30 | getk << 31
+  int* s_jpos = s_miss;  // its position
   for (int x = tid; x < T; x += kTierThreads) {
     const int pos = s_pos[x];
     const int sl = sop[pos];
@@ -947,22 +960,25 @@ __global__ void __launch_bounds__(kTierThreads) tier_update_kernel(const TierPar
     const bool getv = !(f & 1u), getk = nk && !(f & 2u);
     flags[sl] = static_cast<uint8_t>(f | 1u | (nk ? 2u : 0u));
     if (!getv && !getk) continue;
+    const int j = atomicAdd(&s_nmiss, 1);
+    s_job[j] = sl | (getv ? (1 << 30) : 0) | (getk ? (1u << 31) : 0);
+    s_jpos[j] = pos;
+  }
+  __syncthreads();
+  // (5) the copies: 16-byte chunks over the host link, spread over all threads
+  const int njob = s_nmiss;
+  const int32_t* bt = p.block_table + static_cast<int64_t>(b) * p.max_blocks;
+  constexpr int CH = D / 8;
+  for (int it = tid; it < njob * 2 * CH; it += kTierThreads) {
+    const int j = it / (2 * CH), which = (it / CH) & 1, c = it % CH;   // which: 0 V, 1 K
+    const uint32_t job = static_cast<uint32_t>(s_job[j]);
+    if (!((job >> (30 + which)) & 1u)) continue;
+    const int pos = s_jpos[j], sl = static_cast<int>(job & 0x3fffffffu);
     const int64_t src = ((static_cast<int64_t>(__ldg(bt + (pos >> p.ps_shift))) * p.kv_heads + g) *
                              p.page_size + (pos & (p.page_size - 1))) * D;
-    const int64_t dst = static_cast<int64_t>(sl) * D;
-    // the row's chunks, all loads issued before the stores
-    uint4 kv[2][CH];
-#pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      if (getv) kv[0][c] = reinterpret_cast<const uint4*>(host_v + src)[c];
-      if (getk) kv[1][c] = reinterpret_cast<const uint4*>(host_k + src)[c];
-    }
-#pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      if (getv) reinterpret_cast<uint4*>(hot_v + dst)[c] = kv[0][c];
-      if (getk) reinterpret_cast<uint4*>(hot_k + dst)[c] = kv[1][c];
-    }
-    atomicAdd(t.counters, static_cast<unsigned long long>((getv ? 1 : 0) + (getk ? 1 : 0)));
+    const uint4 v = reinterpret_cast<const uint4*>((which ? host_k : host_v) + src)[c];
+    reinterpret_cast<uint4*>((which ? hot_k : hot_v) + static_cast<int64_t>(sl) * D)[c] = v;
+    if (c == 0) atomicAdd(t.counters, 1ull);
   }
 }
 
@@ -1045,13 +1061,10 @@ cudaError_t launch_plan(const AttendParams& p, int32_t n_layers, cudaStream_t s)
 cudaError_t launch_tier_update(const TierParams& t, cudaStream_t s) {
   const size_t sm = static_cast<size_t>(t.cap) * 3 * sizeof(int);
   dim3 grid(t.a.kv_heads, t.a.batch, t.layer_count);
-  if (t.a.head_dim == 64) {
-    cudaFuncSetAttribute(tier_update_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-    tier_update_kernel<64><<<grid, kTierThreads, sm, s>>>(t);
-  } else {
-    cudaFuncSetAttribute(tier_update_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-    tier_update_kernel<128><<<grid, kTierThreads, sm, s>>>(t);
-  }
+  auto k = t.a.head_dim == 64 ? tier_update_kernel<64> : tier_update_kernel<128>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+  cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  k<<<grid, kTierThreads, sm, s>>>(t);
   return cudaGetLastError();
 }
 

@@ -708,13 +708,44 @@ int smallkv_tier_update(int32_t layer_begin, int32_t layer_count, const smallkv_
   return SMALLKV_OK;
 }
 
+int smallkv_plan_tiered(const smallkv_cache* host_llm, int32_t capacity, const void* state,
+                        const smallkv_batch* batch, const int32_t* head_map, int32_t n_llm_layers,
+                        int32_t slm_heads_total, const smallkv_budgets* budgets,
+                        const int32_t* crit_idx, const int32_t* marg_idx, const float* marg_w,
+                        const int32_t* counts, int32_t flags, void* plan, size_t plan_bytes,
+                        void* stream) {
+  skv::AttendParams ap;
+  int rc = fill_attend_params(ap, host_llm, batch, head_map, n_llm_layers, slm_heads_total, budgets,
+                              crit_idx, marg_idx, marg_w, counts);
+  if (rc != SMALLKV_OK) return rc;
+  if ((rc = check_tier(host_llm, batch, n_llm_layers, capacity)) != SMALLKV_OK) return rc;
+  if (!state) return fail(SMALLKV_ERR_NULL, "smallkv_plan_tiered: NULL state");
+  if (flags & ~SMALLKV_ATTEND_GROUP_SELECTION) return fail(SMALLKV_ERR_SHAPE, "unknown flags 0x%x", flags);
+  const size_t need = smallkv_plan_size(host_llm, batch, n_llm_layers);
+  if (!plan || plan_bytes < need)
+    return fail(SMALLKV_ERR_WORKSPACE, "plan buffer %zu < %zu bytes", plan_bytes, need);
+  if (!aligned(plan, 16)) return fail(SMALLKV_ERR_ALIGN, "plan must be 16-byte aligned");
+  if (static_cast<int64_t>(n_llm_layers) * batch->batch > 65535)
+    return fail(SMALLKV_ERR_SHAPE, "L*B > 65535");
+  if ((rc = check_device()) != SMALLKV_OK) return rc;
+  const TierState T = tier_layout(host_llm, batch, n_llm_layers, capacity);
+  ap.plan = static_cast<uint8_t*>(plan);
+  ap.group_sel = (flags & SMALLKV_ATTEND_GROUP_SELECTION) ? 1 : 0;
+  ap.entry_slot = reinterpret_cast<const int32_t*>(static_cast<const uint8_t*>(state) + T.entry);
+  ap.hot_cap = capacity;
+  cudaError_t e = skv::launch_plan(ap, n_llm_layers, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "plan launch");
+  return SMALLKV_OK;
+}
+
 int smallkv_attend_tiered(int32_t llm_layer, const uint16_t* q, const smallkv_cache* host_llm,
                           const uint16_t* hot_k, const uint16_t* hot_v, int32_t capacity,
                           const void* state, const smallkv_batch* batch, const int32_t* head_map,
                           int32_t n_llm_layers, int32_t slm_heads_total,
                           const smallkv_budgets* budgets, const int32_t* crit_idx,
                           const int32_t* marg_idx, const float* marg_w, const int32_t* counts,
-                          float* out, int32_t flags, void* ws, size_t ws_bytes, void* stream) {
+                          const void* plan, float* out, int32_t flags, void* ws, size_t ws_bytes,
+                          void* stream) {
   skv::AttendParams ap;
   int rc = fill_attend_params(ap, host_llm, batch, head_map, n_llm_layers, slm_heads_total, budgets,
                               crit_idx, marg_idx, marg_w, counts);
@@ -745,7 +776,8 @@ int smallkv_attend_tiered(int32_t llm_layer, const uint16_t* q, const smallkv_ca
                     host_llm->head_dim;
   ap.overlap_prologue = (flags & SMALLKV_ATTEND_OVERLAP_PROLOGUE) ? 1 : 0;
   ap.group_sel = (flags & SMALLKV_ATTEND_GROUP_SELECTION) ? 1 : 0;
-  ap.plan = nullptr;
+  if (plan && !aligned(plan, 16)) return fail(SMALLKV_ERR_ALIGN, "plan must be 16-byte aligned");
+  ap.plan = const_cast<uint8_t*>(static_cast<const uint8_t*>(plan));
   ap.entry_slot = reinterpret_cast<const int32_t*>(static_cast<const uint8_t*>(state) + T.entry);
   ap.hot_cap = capacity;
   cudaError_t e = skv::launch_attend(ap, static_cast<cudaStream_t>(stream));

@@ -34,7 +34,7 @@ EXPORTS = ("smallkv_last_error", "smallkv_version", "smallkv_budget_from_tau",
            "smallkv_plan_size", "smallkv_plan", "smallkv_plan_group",
            "smallkv_attend_workspace_size", "smallkv_attend",
            "smallkv_tier_state_size", "smallkv_tier_init", "smallkv_tier_update",
-           "smallkv_attend_tiered",
+           "smallkv_plan_tiered", "smallkv_attend_tiered",
            "smallkv_match_window", "smallkv_prefill_scores",
            "smallkv_match_heads_workspace_size", "smallkv_match_heads",
            "smallkv_workspace_init")
@@ -100,8 +100,10 @@ def load(path: Optional[str] = None):
         lib.smallkv_tier_init.argtypes = [P, sz, P, P, i32, i32, P]
         lib.smallkv_tier_update.argtypes = [i32, i32, P, P, P, i32, P, P, i32, i32, P, P, P, P,
                                             P, i32, P, sz, P]
+        lib.smallkv_plan_tiered.argtypes = [P, i32, P, P, P, i32, i32, P, P, P, P, P, i32, P, sz,
+                                            P]
         lib.smallkv_attend_tiered.argtypes = [i32, P, P, P, P, i32, P, P, P, i32, i32, P, P, P,
-                                              P, P, P, i32, P, sz, P]
+                                              P, P, P, P, i32, P, sz, P]
         lib.smallkv_match_window.argtypes = [i32, i32, i32, i32, P, P]
         lib.smallkv_prefill_scores.argtypes = [P, P, i32, i32, i32, P, P]
         lib.smallkv_match_heads_workspace_size.argtypes = [i32, i32]
@@ -342,7 +344,7 @@ class TieredKV:
     host link) and read by smallkv_attend_tiered."""
 
     def __init__(self, step: DecodeStep, host_k: torch.Tensor, host_v: torch.Tensor,
-                 capacity: int):
+                 capacity: int, use_plan: bool = True):
         """host_k / host_v: pinned CPU pools [L][pages][kv][ps][d] (layer l = LLM layer l)."""
         assert host_k.device.type == "cpu" and host_k.is_pinned() and host_v.is_pinned()
         assert host_k.shape[0] >= step.llm_layers
@@ -362,6 +364,10 @@ class TieredKV:
         if nb == 0:
             raise SmallKVError("smallkv_tier_state_size", 2, "invalid dimensions / capacity")
         self.state = torch.empty(nb, dtype=torch.uint8, device=dev)
+        plan_b = self.lib.smallkv_plan_size(ctypes.byref(self.host), ctypes.byref(step.batch),
+                                            step.llm_layers)
+        self.plan_buf = torch.empty(max(plan_b, 16), dtype=torch.uint8, device=dev) if use_plan else None
+        self.planned = False
         self.reset()
 
     def reset(self, stream=None):
@@ -386,6 +392,15 @@ class TieredKV:
             st.head_map.data_ptr(), st.llm_layers, st.n_slm, ctypes.byref(st.budgets),
             o.crit.data_ptr(), o.marg.data_ptr(), o.marg_w.data_ptr(), o.counts.data_ptr(), gflag,
             self.state.data_ptr(), self.state.numel(), _stream(stream)))
+        self.planned = False
+        if self.plan_buf is not None:
+            _check("smallkv_plan_tiered", self.lib.smallkv_plan_tiered(
+                ctypes.byref(self.host), self.capacity, self.state.data_ptr(),
+                ctypes.byref(st.batch), st.head_map.data_ptr(), st.llm_layers, st.n_slm,
+                ctypes.byref(st.budgets), o.crit.data_ptr(), o.marg.data_ptr(),
+                o.marg_w.data_ptr(), o.counts.data_ptr(), gflag, self.plan_buf.data_ptr(),
+                self.plan_buf.numel(), _stream(stream)))
+            self.planned = True
 
     def attend(self, llm_layer: int, q: torch.Tensor, out: torch.Tensor, stream=None,
                overlap_prologue: bool = False):
@@ -396,8 +411,8 @@ class TieredKV:
             self.hot_k.data_ptr(), self.hot_v.data_ptr(), self.capacity, self.state.data_ptr(),
             ctypes.byref(st.batch), st.head_map.data_ptr(), st.llm_layers, st.n_slm,
             ctypes.byref(st.budgets), o.crit.data_ptr(), o.marg.data_ptr(), o.marg_w.data_ptr(),
-            o.counts.data_ptr(), out.data_ptr(),
-            (ATTEND_OVERLAP_PROLOGUE if overlap_prologue else 0) | gflag,
+            o.counts.data_ptr(), self.plan_buf.data_ptr() if self.planned else None,
+            out.data_ptr(), (ATTEND_OVERLAP_PROLOGUE if overlap_prologue else 0) | gflag,
             st.ws_attend.data_ptr(), st.ws_attend.numel(), _stream(stream)))
         return out
 
@@ -575,6 +590,6 @@ class DecodeGraph:
         nl = self.step.slm.num_layers
         chunks = min(4, nl) if self.step.aux_stream is not None else 1
         sel = 2 * chunks if self.step.variant == "default" else 4   # f2: + group score, weights
-        tier = 1 if self.tier is not None else 0                   # f4: + one tier_update
+        tier = 0 if self.tier is None else (2 if self.tier.plan_buf is not None else 1)  # f4
         return (1 + sel + tier + (1 if self.step.plan_buf is not None else 0)
                 + len(self.plan))
