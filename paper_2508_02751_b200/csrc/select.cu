@@ -600,25 +600,40 @@ __global__ void __launch_bounds__(kGroupThreads) group_score_kernel(const GroupP
   // 4 consecutive positions per thread and all G rows' loads in flight at once
   for (int v0 = 4 * tid; v0 < n; v0 += 4 * kGroupThreads) {
     float x[8][4];
+    const bool vec = (p.row_stride & 3) == 0 && v0 + 3 < n;   // 16-byte loads
 #pragma unroll
     for (int h = 0; h < 8; ++h) {
       if (h >= G) continue;
+      if (vec) {
+        const float4 f4 = __ldg(reinterpret_cast<const float4*>(rowp[h] + v0));
+        x[h][0] = f4.x;
+        x[h][1] = f4.y;
+        x[h][2] = f4.z;
+        x[h][3] = f4.w;
+      } else {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) x[h][u] = v0 + u < n ? __ldg(rowp[h] + v0 + u) : 0.f;
+        for (int u = 0; u < 4; ++u) x[h][u] = v0 + u < n ? __ldg(rowp[h] + v0 + u) : 0.f;
+      }
     }
+    float f[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int v = v0 + u;
-      if (v >= n) break;
-      float f = 0.f;
+      f[u] = 0.f;
 #pragma unroll
       for (int h = 0; h < 8; ++h)
-        if (h < G) f += __expf(x[h][u] - s_lse[h]);
-      out[v] = f;
+        if (h < G) f[u] += __expf(x[h][u] - s_lse[h]);
       if (v < N) {
-        lo = fminf(lo, f);
-        hi = fmaxf(hi, f);
+        lo = fminf(lo, f[u]);
+        hi = fmaxf(hi, f[u]);
       }
+    }
+    if (vec) {
+      *reinterpret_cast<float4*>(out + v0) = make_float4(f[0], f[1], f[2], f[3]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (v0 + u < n) out[v0 + u] = f[u];
     }
   }
   lo = -warp_max(-lo);
