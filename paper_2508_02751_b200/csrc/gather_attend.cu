@@ -175,6 +175,31 @@ __device__ __forceinline__ int split_begin(const GroupLayout& L, int c, int NC) 
   return x;
 }
 
+// Entry x of a group's virtual list [recent | crit(r_0) | marg(r_0) | crit(r_1) | ...]:
+// its position, head mask (bits 0..7 critical, 8..15 marginal), and the
+// marginal weight of a per-row selection (0 for recent / critical entries and
+// for group selections, whose per-head weights live elsewhere).
+struct ListEntry {
+  int pos;
+  uint32_t mask;
+  float w;
+};
+__device__ __forceinline__ ListEntry list_entry(const AttendParams& p, const GroupLayout& L, int b,
+                                                int x, uint32_t allc) {
+  if (x < L.Rc) return {L.n - L.Rc + x, allc, 0.f};
+  x -= L.Rc;
+  int k = 0;
+  while (k < L.nrows - 1 && x >= L.rK[k] + L.rM[k]) {
+    x -= L.rK[k] + L.rM[k];
+    ++k;
+  }
+  const int64_t rb = static_cast<int64_t>(L.rj[k]) * p.batch + b;
+  if (x < L.rK[k]) return {__ldg(p.crit_idx + rb * p.max_crit + x), L.rhm[k], 0.f};
+  const int m = x - L.rK[k];
+  return {__ldg(p.marg_idx + rb * p.max_marg + m), L.rhm[k] << 8,
+          p.group_sel ? 0.f : __ldg(p.marg_w + rb * p.max_marg + m)};
+}
+
 // All threads: stage entries [e_b, e_b + E) of the group's virtual list:
 // row offset in the layer's pool (elements), head mask, marginal weight.
 // Two dependent rounds of loads (list values, page table).
@@ -185,32 +210,10 @@ __device__ void stage_entries(const AttendParams& p, const GroupLayout& L, int b
   const int G = p.heads / p.kv_heads;
   const uint32_t allc = (1u << G) - 1u;
   for (int i = tid; i < E; i += nthr) {
-    int x = e_b + i, pos;
-    uint32_t mk;
-    float wt = 0.f;
-    if (x < L.Rc) {
-      pos = L.n - L.Rc + x;
-      mk = allc;
-    } else {
-      x -= L.Rc;
-      int k = 0;
-      while (k < L.nrows - 1 && x >= L.rK[k] + L.rM[k]) {
-        x -= L.rK[k] + L.rM[k];
-        ++k;
-      }
-      const int64_t rb = static_cast<int64_t>(L.rj[k]) * p.batch + b;
-      if (x < L.rK[k]) {
-        pos = __ldg(p.crit_idx + rb * p.max_crit + x);
-        mk = L.rhm[k];
-      } else {
-        pos = __ldg(p.marg_idx + rb * p.max_marg + (x - L.rK[k]));
-        if (!p.group_sel) wt = __ldg(p.marg_w + rb * p.max_marg + (x - L.rK[k]));
-        mk = L.rhm[k] << 8;
-      }
-    }
-    soff[i] = static_cast<uint32_t>(pos);
-    smk[i] = mk;
-    sw[i] = wt;
+    const ListEntry le = list_entry(p, L, b, e_b + i, allc);
+    soff[i] = static_cast<uint32_t>(le.pos);
+    smk[i] = le.mask;
+    sw[i] = le.w;
   }
   __syncthreads();
   if (p.entry_slot) {
@@ -275,27 +278,10 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const AttendParams p
       const int i = x0 - s_split[c];
       if (i >= kBatch) continue;
       slot_i[u] = c * kBatch + i;
-      int x = x0;
-      if (x < L.Rc) {
-        pos[u] = L.n - L.Rc + x;
-        mk[u] = allc;
-      } else {
-        x -= L.Rc;
-        int k = 0;
-        while (k < L.nrows - 1 && x >= L.rK[k] + L.rM[k]) {
-          x -= L.rK[k] + L.rM[k];
-          ++k;
-        }
-        const int64_t rb = static_cast<int64_t>(L.rj[k]) * p.batch + b;
-        if (x < L.rK[k]) {
-          pos[u] = __ldg(p.crit_idx + rb * p.max_crit + x);
-          mk[u] = L.rhm[k];
-        } else {
-          pos[u] = __ldg(p.marg_idx + rb * p.max_marg + (x - L.rK[k]));
-          if (!p.group_sel) wt[u] = __ldg(p.marg_w + rb * p.max_marg + (x - L.rK[k]));
-          mk[u] = L.rhm[k] << 8;
-        }
-      }
+      const ListEntry le = list_entry(p, L, b, x0, allc);
+      pos[u] = le.pos;
+      mk[u] = le.mask;
+      wt[u] = le.w;
     }
     uint32_t ro[U];
     if (p.entry_slot) {
@@ -892,22 +878,9 @@ __global__ void __launch_bounds__(kTierThreads) tier_update_kernel(const TierPar
   // (1) the list's positions (decoded once) and their needs: K+V for recent /
   // critical entries, V for marginal ones
   for (int x = tid; x < T; x += kTierThreads) {
-    int pos, y = x;
-    bool k;
-    if (y < L.Rc) {
-      pos = n - L.Rc + y;
-      k = true;
-    } else {
-      y -= L.Rc;
-      int r = 0;
-      while (r < L.nrows - 1 && y >= L.rK[r] + L.rM[r]) {
-        y -= L.rK[r] + L.rM[r];
-        ++r;
-      }
-      const int64_t rb = static_cast<int64_t>(L.rj[r]) * p.batch + b;
-      k = y < L.rK[r];
-      pos = k ? __ldg(p.crit_idx + rb * p.max_crit + y) : __ldg(p.marg_idx + rb * p.max_marg + (y - L.rK[r]));
-    }
+    const ListEntry le = list_entry(p, L, b, x, 0xffu);
+    const int pos = le.pos;
+    const bool k = (le.mask & 0xffu) != 0u;   // critical / recent: K needed
     s_pos[x] = pos;
     atomicOr(&need_v[pos >> 5], 1u << (pos & 31));
     if (k) atomicOr(&need_k[pos >> 5], 1u << (pos & 31));
