@@ -65,9 +65,11 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
   __shared__ uint32_t s_pref[2];
   __shared__ int s_rem[2];
 
-  const int r = p.layer_off[p.layer_begin] + static_cast<int>(blockIdx.x);
+  // grid (B, max_rows): the CTAs of a row are consecutive and the rows past the
+  // launch's image (idle CTAs) come last
+  const int r = p.layer_off[p.layer_begin] + static_cast<int>(blockIdx.y);
   if (r >= p.layer_off[p.layer_end]) return;
-  const int b = blockIdx.y;
+  const int b = blockIdx.x;
 
   const int j = p.rows[r];
   const int n = p.seq_lens[b];
@@ -690,7 +692,7 @@ __global__ void __launch_bounds__(kGroupThreads) group_weights_kernel(const Grou
 cudaError_t launch_select(const SelectParams& p, int32_t max_rows, int32_t max_seq_len,
                           bool overlap_previous, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(max_rows, p.batch);
+  cfg.gridDim = dim3(p.batch, max_rows);
   cfg.blockDim = dim3(kThreads);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
