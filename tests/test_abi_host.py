@@ -92,3 +92,32 @@ def test_f3_match_window_host():
     assert smallkv.match_window(1000, keep_last=False) == (0, 200)
     with pytest.raises(smallkv.SmallKVError):
         smallkv.match_window(10, 200, 100)
+
+
+def test_next_row_entry_points_validate_before_launch(lib):
+    """f2 / f3 / f4 entry points: argument errors are reported on the host
+    (no device needed), with the documented status codes."""
+    P = ctypes.c_void_p
+    c = smallkv.CCache(16, 16, 16, 4, 4, 16, 2, 8, 2, 128)
+    b = smallkv.CBatch(16, 2, 64)
+    bu = smallkv.CBudgets(16, 16, 16, 8, 8)
+    # f2: G = 8 / 2 = 4 ok; H % H_kv != 0 rejected
+    rc = lib.smallkv_select_group(16, ctypes.byref(c), ctypes.byref(b), 16, 2, 8, 3,
+                                  ctypes.byref(bu), 16, 16, 16, 16, 16, 16, 16, 16, 1 << 20, None)
+    assert rc == 2 and b"invalid" in lib.smallkv_last_error()
+    rc = lib.smallkv_select_group(16, ctypes.byref(c), ctypes.byref(b), 16, 2, 8, 2,
+                                  ctypes.byref(bu), 16, 16, None, 16, 16, 16, 16, 16, 1 << 20, None)
+    assert rc == 1
+    # f3: window length bounds
+    rc = lib.smallkv_prefill_scores(16, ctypes.byref(c), 0, 0, 2000, 16, None)
+    assert rc == 2
+    rc = lib.smallkv_prefill_scores(None, ctypes.byref(c), 0, 0, 10, 16, None)
+    assert rc == 1
+    # f4: capacity must be a multiple of 4; state size reported
+    assert lib.smallkv_tier_state_size(ctypes.byref(c), ctypes.byref(b), 2, 30) == 0
+    assert lib.smallkv_tier_state_size(ctypes.byref(c), ctypes.byref(b), 2, 32) > 0
+    rc = lib.smallkv_tier_init(16, 8, ctypes.byref(c), ctypes.byref(b), 2, 32, None)
+    assert rc == 4   # ERR_WORKSPACE: state too small
+    rc = lib.smallkv_tier_update(0, 3, ctypes.byref(c), 16, 16, 32, ctypes.byref(b), 16, 2, 16,
+                                 ctypes.byref(bu), 16, 16, 16, 16, 0, 16, 1 << 30, None)
+    assert rc == 2   # layers [0, 3) past the 2 LLM layers
