@@ -67,6 +67,9 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
 
   // grid (B, max_rows): the CTAs of a row are consecutive and the rows past the
   // launch's image (idle CTAs) come last
+  // launched with programmatic dependent launch: K1's logits / statistics are
+  // read only after the previous grid has completed
+  griddep_wait();
   const int r = p.layer_off[p.layer_begin] + static_cast<int>(blockIdx.y);
   if (r >= p.layer_off[p.layer_end]) return;
   const int b = blockIdx.x;

@@ -343,7 +343,7 @@ int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm, const smallk
     se.layer_end = chunk_lo(i + 1);
     const int rows_max = (se.layer_end - se.layer_begin) * slm->num_q_heads;
     return skv::launch_select(se, rows_max < n_llm_heads ? rows_max : n_llm_heads,
-                              batch->max_seq_len, false, st);
+                              batch->max_seq_len, true, st);
   };
   cudaEvent_t evs[9] = {};
   const int nev = aux && nchunk > 1 ? nchunk + 1 : 0;
