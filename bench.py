@@ -411,7 +411,7 @@ def run_ours(args, world, rank, local):
     }
     if tier is not None:
         line["f4"] = f4_report(p, cfg, graph, tier)
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:   # the oracle baseline: rank 0 at N = 1 only
         line["cpu_baseline"] = cpu_baseline(p, cfg, L, variant=args.variant)
     print(json.dumps(line), flush=True)
     if world > 1:
