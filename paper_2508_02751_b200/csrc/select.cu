@@ -575,6 +575,7 @@ __device__ __forceinline__ float2 row_lse(const GroupParams& p, int j, int b) {
 __global__ void __launch_bounds__(kGroupThreads) group_score_kernel(const GroupParams p) {
   __shared__ int s_j[8];
   __shared__ float s_lse[8];
+  __shared__ float s_mult[8];   // multiplicity of each distinct row (0 for repeats)
   __shared__ float s_red[2][kGroupThreads / 32];
   const int gl = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
   const int l = gl / p.H_kv, g = gl % p.H_kv, G = p.H / p.H_kv;
@@ -594,6 +595,21 @@ __global__ void __launch_bounds__(kGroupThreads) group_score_kernel(const GroupP
     p.slm_lse[(static_cast<int64_t>(j) * p.batch + b) * 2 + 1] = ml.y;
   }
   __syncthreads();
+  if (tid < G) {
+    // heads sharing a row contribute the same a' row: read it once, weight it by
+    // the number of heads (F_g = Σ_h a'_{f(h)} = Σ_distinct j mult_j · a'_j)
+    int first = tid;
+    for (int h = 0; h < tid; ++h)
+      if (s_j[h] == s_j[tid]) {
+        first = h;
+        break;
+      }
+    float m = 0.f;
+    if (first == tid)
+      for (int h = tid; h < G; ++h) m += s_j[h] == s_j[tid] ? 1.f : 0.f;
+    s_mult[tid] = m;
+  }
+  __syncthreads();
   const int n = p.seq_lens[b];
   const int N = n - iclamp(p.n_recent[b], 0, n);
   float* out = p.score + (static_cast<int64_t>(gl) * p.batch + b) * p.row_stride;
@@ -608,7 +624,7 @@ __global__ void __launch_bounds__(kGroupThreads) group_score_kernel(const GroupP
     const bool vec = (p.row_stride & 3) == 0 && v0 + 3 < n;   // 16-byte loads
 #pragma unroll
     for (int h = 0; h < 8; ++h) {
-      if (h >= G) continue;
+      if (h >= G || s_mult[h] == 0.f) continue;
       if (vec) {
         const float4 f4 = __ldg(reinterpret_cast<const float4*>(rowp[h] + v0));
         x[h][0] = f4.x;
@@ -627,7 +643,7 @@ __global__ void __launch_bounds__(kGroupThreads) group_score_kernel(const GroupP
       f[u] = 0.f;
 #pragma unroll
       for (int h = 0; h < 8; ++h)
-        if (h < G) f[u] += __expf(x[h][u] - s_lse[h]);
+        if (h < G && s_mult[h] != 0.f) f[u] += s_mult[h] * __expf(x[h][u] - s_lse[h]);
       if (v < N) {
         lo = fminf(lo, f[u]);
         hi = fmaxf(hi, f[u]);
