@@ -60,6 +60,7 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
   __shared__ int wsel[kWarps][2];
   __shared__ int s_have_counts;
   __shared__ int s_bin[2], s_above[2], s_nc[2], s_fallback;
+  __shared__ int s_refine[2], s_sub[2];
   __shared__ uint32_t s_tk[2];
   __shared__ int s_ti[2];
   __shared__ uint32_t s_pref[2];
@@ -89,6 +90,15 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
   float* accrow = p.acc ? p.acc + rb * p.row_stride : nullptr;
   const float* score = accrow ? accrow : row;
   auto VAL = [&](int i) -> float { return kInSmem ? vals[i] : score[i]; };
+  // positions i..i+3 (i a multiple of 4): shared memory, or global memory with
+  // one 16-byte load when the row is 16-byte aligned (long rows)
+  const bool g_al = (p.row_stride & 3) == 0;
+  auto LOAD4 = [&](int i) -> float4 {
+    if (kInSmem) return *reinterpret_cast<const float4*>(vals + i);
+    // (plain loads, not the read-only path: the f1 scores were written by this kernel)
+    if (g_al) return *reinterpret_cast<const float4*>(score + i);
+    return make_float4(score[i], score[i + 1], score[i + 2], score[i + 3]);
+  };
 
   // ---- pass 1: stage the row; (max, Σexp) over [0, n) and the ranked range
   // [min, max] over [0, N) are merged from K1's per-chunk statistics (fixed order)
@@ -181,6 +191,7 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
   if (tid == 0) {
     s_fallback = (!all_equal && !isfinite(scale)) ? 1 : 0;
     s_have_counts = 0;
+    s_refine[0] = s_refine[1] = 0;
   }
   __syncthreads();
   if (all_equal) {
@@ -209,9 +220,19 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
         *reinterpret_cast<uint32_t*>(sbin + base) = packed;
       }
     } else {
-      for (int base = s0; base < s1; base += 32) {
-        const int i = base + lane;
-        if (i < s1) atomicAdd(&hist[warp][iclamp(static_cast<int>((bv(VAL(i)) - blo) * scale), 0, kBins - 1)], 1u);
+      // long rows, read from global memory (L2): 4 positions per lane, 2 x 16 B in flight
+      for (int base = s0 + 4 * lane; base < s1; base += 256) {
+        float4 v4[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) v4[q] = base + 128 * q < s1 ? LOAD4(base + 128 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const float vv[4] = {v4[q].x, v4[q].y, v4[q].z, v4[q].w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (base + 128 * q + k < s1)
+              atomicAdd(&hist[warp][iclamp(static_cast<int>((bv(vv[k]) - blo) * scale), 0, kBins - 1)], 1u);
+        }
       }
     }
     __syncthreads();
@@ -241,24 +262,81 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
           s_bin[warp] = kBins - 1 - (lane * 8 + q);
           s_above[warp] = above;
           s_nc[warp] = c[q];
-          if (c[q] > kCandCap) s_fallback = 1;
+          s_refine[warp] = c[q] > kCandCap ? 1 : 0;   // refine inside the bin (long rows)
         }
         above += c[q];
       }
     }
     __syncthreads();
+    // Second level for an overfull boundary bin (long rows): 256 value-linear
+    // sub-bins inside it; the boundary becomes (bin, sub-bin) and only that
+    // sub-bin's positions are candidates.  (Per-warp output counts are then
+    // recounted before the emission.)  Still overfull: radix fallback.
+    const bool refine = s_refine[0] | s_refine[1];
+    auto sub_of = [&](int t, float v) {
+      return iclamp(static_cast<int>((bv(v) - (blo + static_cast<float>(s_bin[t]) / scale)) * (scale * 256.f)),
+                    0, kBins - 1);
+    };
+    auto bin_of = [&](float v) { return iclamp(static_cast<int>((bv(v) - blo) * scale), 0, kBins - 1); };
+    if (refine && !s_fallback) {
+      for (int i = tid; i < 2 * kBins; i += kThreads) (&hist[0][0])[i] = 0u;
+      __syncthreads();
+      for (int i4 = 4 * tid; i4 < N; i4 += 4 * kThreads) {
+        const float4 v4 = LOAD4(i4);
+        const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (i4 + k >= N) break;
+          const int bin = bin_of(vv[k]);
+#pragma unroll
+          for (int t = 0; t < 2; ++t)
+            if (s_refine[t] && bin == s_bin[t]) atomicAdd(&hist[t][sub_of(t, vv[k])], 1u);
+        }
+      }
+      __syncthreads();
+      if (warp < 2 && s_refine[warp]) {
+        const int rem = (warp == 0 ? rA : rB) - s_above[warp];
+        int c[8], tot = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          c[q] = static_cast<int>(hist[warp][kBins - 1 - (lane * 8 + q)]);
+          tot += c[q];
+        }
+        int incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        int above = incl - tot;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (above < rem && rem <= above + c[q]) {
+            s_sub[warp] = kBins - 1 - (lane * 8 + q);
+            s_above[warp] += above;
+            s_nc[warp] = c[q];
+            if (c[q] > kCandCap) s_fallback = 1;
+          }
+          above += c[q];
+        }
+      }
+      __syncthreads();
+    }
     if (!s_fallback) {
       const int binA = rA > 0 ? s_bin[0] : -1, binB = s_bin[1];
-      const bool shared = binA == binB;
+      const bool shared = binA == binB && !refine;
       __shared__ int s_cnt[2];
       if (tid < 2) s_cnt[tid] = 0;
       __syncthreads();
       const uint8_t* sbin = reinterpret_cast<const uint8_t*>(vals + n);
       auto take = [&](int i, int bin) {
+        const float v = VAL(i);
         const unsigned long long kv =
-            (static_cast<unsigned long long>(desc_key(VAL(i))) << 32) | static_cast<uint32_t>(i);
-        if (bin == binA) cand[0][atomicAdd(&s_cnt[0], 1)] = kv;
-        if (bin == binB && !shared) cand[1][atomicAdd(&s_cnt[1], 1)] = kv;
+            (static_cast<unsigned long long>(desc_key(v)) << 32) | static_cast<uint32_t>(i);
+        if (bin == binA && (!s_refine[0] || sub_of(0, v) == s_sub[0]))
+          cand[0][atomicAdd(&s_cnt[0], 1)] = kv;
+        if (bin == binB && !shared && (!s_refine[1] || sub_of(1, v) == s_sub[1]))
+          cand[1][atomicAdd(&s_cnt[1], 1)] = kv;
       };
       if (kInSmem) {
         // 4 bin bytes per load; SIMD byte compares skip words without a boundary bin
@@ -274,9 +352,15 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
             if (((hit >> (8 * k)) & 0xffu) && i4 + k < N) take(i4 + k, static_cast<int>((w >> (8 * k)) & 0xffu));
         }
       } else {
-        for (int i = tid; i < N; i += kThreads) {
-          const int bin = iclamp(static_cast<int>((bv(VAL(i)) - blo) * scale), 0, kBins - 1);
-          if (bin == binA || bin == binB) take(i, bin);
+        for (int i4 = 4 * tid; i4 < N; i4 += 4 * kThreads) {
+          const float4 v4 = LOAD4(i4);
+          const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (i4 + k >= N) break;
+            const int bin = iclamp(static_cast<int>((bv(vv[k]) - blo) * scale), 0, kBins - 1);
+            if (bin == binA || bin == binB) take(i4 + k, bin);
+          }
         }
       }
       __syncthreads();
@@ -316,7 +400,7 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
           if (v <= thr) atomicAdd(&wsel[static_cast<int>(v & 0xffffffffu) / seg][t], 1);
         }
       }
-      {
+      if (!refine) {   // (after a refinement the per-warp histograms are gone: recount)
         int ab[2] = {0, 0};
         for (int t = 0; t < 2; ++t) {
           const int bt_ = (t == 0 && rA == 0) ? kBins : s_bin[t];
@@ -446,7 +530,7 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
   const int IA = s_ti[0], IB = s_ti[1];
   // per-lane classification of positions i..i+3 (shared-memory path)
   auto classify4 = [&](int i, uint32_t& cm, uint32_t& mm, float (&xs)[4]) {
-    const float4 v4 = i < s1 ? *reinterpret_cast<const float4*>(vals + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 v4 = i < s1 ? LOAD4(i) : make_float4(0.f, 0.f, 0.f, 0.f);
     xs[0] = v4.x;
     xs[1] = v4.y;
     xs[2] = v4.z;
@@ -465,7 +549,7 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
   };
   if (!s_have_counts) {
     int cc = 0, cb = 0;
-    if (kInSmem) {
+    if (true) {
       for (int base = s0 + 4 * lane; base < s1; base += 128) {
         uint32_t cm, mm;
         float xs[4];
@@ -504,7 +588,7 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
   int32_t* crit = p.crit_idx + rb * p.max_crit;
   int32_t* marg = p.marg_idx + rb * p.max_marg;
   float* mw = p.marg_w + rb * p.max_marg;
-  if (kInSmem) {
+  if (true) {
     // 128 positions per warp step: per-lane masks, one packed warp scan
     for (int base0 = s0; base0 < s1; base0 += 128) {
       const int base = base0 + 4 * lane;

@@ -99,7 +99,9 @@ def compare_select(p, gpu, sel, rows=None, batch_idx=None, logit_atol=2e-4, rank
             assert np.all(gC < n - Rc) and np.all(gM < n - Rc)
             if Mc:
                 ref = o_a[gM]
-                rel = np.abs(mw[j, b, :Mc] - ref) / np.maximum(ref, 1e-300)
+                # fp32 output (R15): weights below fp32's normal range (1e-38) cannot
+                # be represented, so they are compared absolutely at 1e-30 scale
+                rel = np.abs(mw[j, b, :Mc] - ref) / np.maximum(ref, 1e-30)
                 rep["max_margw_rel"] = max(rep["max_margw_rel"], float(rel.max()))
                 assert rel.max() <= 1e-4, f"marg_w row {j} seq {b}: {rel.max()}"
             rep["rows_checked"] += 1

@@ -245,6 +245,19 @@ def test_two_valued_logits_radix_fallback():
     _check(p)
 
 
+def test_dense_boundary_bin_refinement():
+    """A few outlier logits stretch the value-linear histogram so that the
+    boundary bin holds thousands of positions: K2 refines inside that bin
+    (256 sub-bins) instead of falling back to the radix select."""
+    cfg = _cfg(n=32000, B=1, budget=(3200, 500, 3200))
+    p = synth.make_problem(cfg, seed=17, page_size=64, seq_lens=[32000])
+    k = p.slm.k.clone()
+    k[:, :, :, 3] *= 40.0                 # one row per page: far outliers (both signs)
+    p = dataclasses.replace(p, slm=dataclasses.replace(p.slm, k=k)).to("cuda")
+    rep, _, _ = _check(p, logit_atol=2e-3)
+    print("refinement", rep)
+
+
 def _head_shard(p, g0, g1):
     from paper_2508_02751_b200 import dist as pdist
     L, H, Hkv = p.cfg.llm.layers, p.cfg.llm.q_heads, p.cfg.llm.kv_heads
