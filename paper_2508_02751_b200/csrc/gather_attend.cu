@@ -348,7 +348,16 @@ __global__ void __launch_bounds__(kThreads, 1) attend_kernel(const AttendParams 
   uint8_t* wst = stages + warp * NSTAGE * SB;
   const uint16_t* kpool = p.k + p.layer_offset;
   const uint16_t* vpool = p.v + p.layer_offset;
-  // Early tiles: the list starts with the recent window [n-R', n), whose rows
+  if (rec) {
+    // one round: header + this rank's pre-staged first batch (cp.async, 16 B)
+    for (int i = tid; i < static_cast<int>(sizeof(GroupLayout)) / 16; i += kThreads)
+      cp_async16(smem_u32(reinterpret_cast<uint8_t*>(&L) + 16 * i), rec + 16 * i, true);
+    const uint8_t* slot = rec + kHdrBytes + static_cast<int64_t>(c) * kBatch * 12;
+    for (int i = tid; i < kBatch * 12 / 16; i += kThreads)
+      cp_async16(smem_u32(smem + 16 * i), slot + 16 * i, true);
+    cp_async_commit();
+  }
+  // Early tiles (issued after the plan copy, waited for separately): the list starts with the recent window [n-R', n), whose rows
   // need only the sequence length, the recent budget and the block table
   // (small, L2-resident) — so a single-CTA group issues its first tiles'
   // K/V copies before (and in parallel with) the plan / list loads.
@@ -385,14 +394,10 @@ __global__ void __launch_bounds__(kThreads, 1) attend_kernel(const AttendParams 
     }
   }
   if (rec) {
-    // one round: header + this rank's pre-staged first batch (cp.async, 16 B)
-    for (int i = tid; i < static_cast<int>(sizeof(GroupLayout)) / 16; i += kThreads)
-      cp_async16(smem_u32(reinterpret_cast<uint8_t*>(&L) + 16 * i), rec + 16 * i, true);
-    const uint8_t* slot = rec + kHdrBytes + static_cast<int64_t>(c) * kBatch * 12;
-    for (int i = tid; i < kBatch * 12 / 16; i += kThreads)
-      cp_async16(smem_u32(smem + 16 * i), slot + 16 * i, true);
-    cp_async_commit();
-    cp_async_wait<0>();
+    // wait for the plan group only (the oldest); the early tiles stay in flight
+    if (early == 2) cp_async_wait<2>();
+    else if (early == 1) cp_async_wait<1>();
+    else cp_async_wait<0>();
     __syncthreads();
   } else {
     build_layout(p, p.layer, b, g, L);
