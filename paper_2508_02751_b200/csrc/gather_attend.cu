@@ -93,8 +93,17 @@ static_assert(sizeof(GroupLayout) <= kHdrBytes && sizeof(GroupLayout) % 16 == 0,
 
 // Plan record of one (layer, sequence, kv-group): header + for each cluster
 // rank the first kBatch staged entries (row offset, head mask, marginal weight).
+// Tile table of one batch: word 0 = the tile count, then one packed word per
+// tile; kTileTableBytes per cluster rank in the plan record (first batch).
+constexpr int kMaxTiles = kBatch / kTile + 2 * 8 + 2;
+constexpr int kTileTableBytes = 384;
+static_assert((kMaxTiles + 1) * 4 <= kTileTableBytes && kTileTableBytes % 16 == 0, "tile table");
 __host__ __device__ constexpr int64_t plan_record_bytes(int nc) {
-  return kHdrBytes + static_cast<int64_t>(nc) * kBatch * 12;
+  return kHdrBytes + static_cast<int64_t>(nc) * (kTileTableBytes + kBatch * 12);
+}
+// record layout: [header][tile tables: nc x kTileTableBytes][slots: nc x kBatch x 12]
+__host__ __device__ constexpr int64_t plan_slot_offset(int nc, int c) {
+  return kHdrBytes + static_cast<int64_t>(nc) * kTileTableBytes + static_cast<int64_t>(c) * kBatch * 12;
 }
 
 // All threads: distinct SLM rows of the group's heads (first occurrence order)
@@ -173,6 +182,31 @@ __device__ __forceinline__ int split_begin(const GroupLayout& L, int c, int NC) 
     if (seg(L.rM[k], 1, out)) return out;
   }
   return x;
+}
+
+// One thread: the tile table of entries [e_b, e_b + E) of the group's list —
+// runs of K+V entries (recent / critical) in 16-row tiles, runs of V-only
+// (marginal) entries in 32-row tiles (both fill one 8 KB stage, so the tile
+// count tracks the bytes); variant f2: marginal runs in 16-row tiles whose K
+// half carries the per-head weights.  tt[0] = count, tt[1 + i] = tile i packed
+// (first entry - e_b) | count << 16 | vonly << 24 | per-head << 25.
+__device__ void build_tile_table(const GroupLayout& L, int e_b, int E, bool group_sel, uint32_t* tt) {
+  int nt = 0, x = 0;
+  const uint32_t mflag = group_sel ? (1u << 25) : (1u << 24);
+  auto run = [&](int len, bool vonly) {
+    const int a = max(x, e_b), z = min(x + len, e_b + E);
+    const int ts = vonly && !group_sel ? 2 * kTile : kTile;
+    for (int y = a; y < z; y += ts)
+      tt[1 + nt++] = static_cast<uint32_t>(y - e_b) | (static_cast<uint32_t>(min(ts, z - y)) << 16) |
+                     (vonly ? mflag : 0u);
+    x += len;
+  };
+  run(L.Rc, false);
+  for (int k = 0; k < L.nrows; ++k) {
+    run(L.rK[k], false);
+    run(L.rM[k], true);
+  }
+  tt[0] = static_cast<uint32_t>(nt);
 }
 
 // Entry x of a group's virtual list [recent | crit(r_0) | marg(r_0) | crit(r_1) | ...]:
@@ -259,6 +293,11 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const AttendParams p
   __shared__ int s_split[9];
   if (threadIdx.x <= NC) s_split[threadIdx.x] = split_begin(L, threadIdx.x, NC);
   __syncthreads();
+  if (threadIdx.x < NC) {   // each rank's first-batch tile table
+    const int c = threadIdx.x, e0 = s_split[c];
+    build_tile_table(L, e0, min(kBatch, s_split[c + 1] - e0), p.group_sel != 0,
+                     reinterpret_cast<uint32_t*>(rec + kHdrBytes + c * kTileTableBytes));
+  }
   constexpr int U = 4;
   const int T = L.T;
   for (int base = threadIdx.x; base < T; base += U * kPlanThreads) {
@@ -304,7 +343,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const AttendParams p
     for (int u = 0; u < U; ++u) {
       if (slot_i[u] < 0) continue;
       const int c = slot_i[u] / kBatch, i = slot_i[u] % kBatch;
-      uint32_t* slot = reinterpret_cast<uint32_t*>(rec + kHdrBytes) + static_cast<int64_t>(c) * kBatch * 3;
+      uint32_t* slot = reinterpret_cast<uint32_t*>(rec + plan_slot_offset(NC, c));
       slot[i] = ro[u];
       slot[kBatch + i] = mk[u];
       reinterpret_cast<float*>(slot)[2 * kBatch + i] = wt[u];
@@ -325,9 +364,8 @@ __global__ void __launch_bounds__(kThreads, 1) attend_kernel(const AttendParams 
   float* sw = reinterpret_cast<float*>(smk + kBatch);
   uint8_t* stages = reinterpret_cast<uint8_t*>(sw + kBatch);
   __shared__ __align__(16) GroupLayout L;
-  constexpr int kMaxTiles = kBatch / kTile + 2 * 8 + 2;
-  __shared__ uint32_t s_tiles[kMaxTiles];
-  __shared__ int s_ntile;
+  __shared__ __align__(16) uint32_t s_tt[kTileTableBytes / 4];   // [count][tiles]
+  const uint32_t* s_tiles = s_tt + 1;
 
   const int c = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
   const int NC = gridDim.x;
@@ -352,7 +390,10 @@ __global__ void __launch_bounds__(kThreads, 1) attend_kernel(const AttendParams 
     // one round: header + this rank's pre-staged first batch (cp.async, 16 B)
     for (int i = tid; i < static_cast<int>(sizeof(GroupLayout)) / 16; i += kThreads)
       cp_async16(smem_u32(reinterpret_cast<uint8_t*>(&L) + 16 * i), rec + 16 * i, true);
-    const uint8_t* slot = rec + kHdrBytes + static_cast<int64_t>(c) * kBatch * 12;
+    const uint8_t* tts = rec + kHdrBytes + static_cast<int64_t>(c) * kTileTableBytes;
+    for (int i = tid; i < kTileTableBytes / 16; i += kThreads)
+      cp_async16(smem_u32(reinterpret_cast<uint8_t*>(s_tt) + 16 * i), tts + 16 * i, true);
+    const uint8_t* slot = rec + plan_slot_offset(NC, c);
     for (int i = tid; i < kBatch * 12 / 16; i += kThreads)
       cp_async16(smem_u32(smem + 16 * i), slot + 16 * i, true);
     cp_async_commit();
@@ -449,31 +490,10 @@ __global__ void __launch_bounds__(kThreads, 1) attend_kernel(const AttendParams 
     if (!(rec && e_b == e_lo)) stage_entries<D>(p, L, b, g, e_b, E, soff, smk, sw);
     SKV_T(2);
 
-    // ---- tiles of this batch: runs of K+V entries (recent / critical) in
-    // 16-row tiles, runs of V-only (marginal) entries in 32-row tiles — both
-    // fill one 8 KB stage, so the tile count tracks the bytes.  Variant f2:
-    // marginal runs in 16-row tiles whose K half carries the per-head weights.
-    // Packed (first entry - e_b) | count << 16 | vonly << 24 | per-head << 25.
-    if (tid == 0) {
-      int nt = 0, x = 0;
-      const uint32_t mflag = p.group_sel ? (1u << 25) : (1u << 24);
-      auto run = [&](int len, bool vonly) {
-        const int a = max(x, e_b), z = min(x + len, e_b + E);
-        const int ts = vonly && !p.group_sel ? 2 * kTile : kTile;
-        for (int y = a; y < z; y += ts)
-          s_tiles[nt++] = static_cast<uint32_t>(y - e_b) | (static_cast<uint32_t>(min(ts, z - y)) << 16) |
-                          (vonly ? mflag : 0u);
-        x += len;
-      };
-      run(L.Rc, false);
-      for (int k = 0; k < L.nrows; ++k) {
-        run(L.rK[k], false);
-        run(L.rM[k], true);
-      }
-      s_ntile = nt;
-    }
+    // ---- tiles of this batch (from the plan for its first batch)
+    if (!(rec && e_b == e_lo) && tid == 0) build_tile_table(L, e_b, E, p.group_sel != 0, s_tt);
     __syncthreads();
-    const int ntile = s_ntile;
+    const int ntile = static_cast<int>(s_tt[0]);
     const int nmy = ntile > warp ? (ntile - warp + kWarps - 1) / kWarps : 0;
 
     // Each cp.async instruction of the warp moves 4 rows x 128 contiguous bytes:
