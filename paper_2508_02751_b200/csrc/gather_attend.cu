@@ -60,12 +60,18 @@ __device__ __forceinline__ long long gtimer() {
 
 namespace {
 constexpr int kTile = 16;      // rows (tokens) per warp tile
-constexpr int kWarps = 8;      // one CTA per SM (8 warps x 3-stage rings = 192 KB)
+#ifndef SKV_ATTEND_WARPS
+#define SKV_ATTEND_WARPS 8
+#endif
+#ifndef SKV_ATTEND_STAGES
+#define SKV_ATTEND_STAGES 3
+#endif
+constexpr int kWarps = SKV_ATTEND_WARPS;      // one CTA per SM (8 warps x 3-stage rings = 192 KB)
 constexpr int kThreads = kWarps * 32;
 constexpr int kBatch = 1024;   // entries whose positions/pages/weights are staged at once
 
 template <int D>
-constexpr int stages_for() { return 3; }
+constexpr int stages_for() { return SKV_ATTEND_STAGES; }
 template <int D>
 constexpr int stage_bytes() { return 2 * kTile * D * 2; }
 
@@ -352,7 +358,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const AttendParams p
 }
 
 template <int D>
-__global__ void __launch_bounds__(kThreads, 1) attend_kernel(const AttendParams p) {
+__global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const AttendParams p) {
   constexpr int NSTAGE = stages_for<D>();
   constexpr int ROWB = D * 2;                // bytes per K or V row
   constexpr int KV_BYTES = kTile * ROWB;
@@ -397,6 +403,22 @@ __global__ void __launch_bounds__(kThreads, 1) attend_kernel(const AttendParams 
     for (int i = tid; i < kBatch * 12 / 16; i += kThreads)
       cp_async16(smem_u32(smem + 16 * i), slot + 16 * i, true);
     cp_async_commit();
+    // the next layer's record of this (sequence, group, rank) -> L2: the plan of
+    // all layers is written once per step, so by a late layer it has been
+    // evicted by the K/V stream and its read would otherwise be an HBM miss on
+    // that launch's critical path
+    if (p.layer + 1 < p.n_layers) {
+      const uint8_t* nx = rec + static_cast<int64_t>(p.batch) * p.kv_heads * plan_record_bytes(NC);
+      constexpr int kHdrLines = (kHdrBytes + kTileTableBytes) / 128 + 1;
+      if (tid < kHdrLines + kBatch * 12 / 128) {
+        const uint8_t* a = tid < kHdrLines
+                               ? nx + (tid < kHdrBytes / 128 ? 128 * tid
+                                                             : kHdrBytes + static_cast<int64_t>(c) * kTileTableBytes +
+                                                                   128 * (tid - kHdrBytes / 128))
+                               : nx + plan_slot_offset(NC, c) + 128 * (tid - kHdrLines);
+        asm volatile("prefetch.global.L2 [%0];\n" ::"l"(a));
+      }
+    }
   }
   // Early tiles (issued after the plan copy, waited for separately): the list starts with the recent window [n-R', n), whose rows
   // need only the sequence length, the recent budget and the block table
@@ -436,7 +458,8 @@ __global__ void __launch_bounds__(kThreads, 1) attend_kernel(const AttendParams 
   }
   if (rec) {
     // wait for the plan group only (the oldest); the early tiles stay in flight
-    if (early == 2) cp_async_wait<2>();
+    if (early == 3) cp_async_wait<3>();
+    else if (early == 2) cp_async_wait<2>();
     else if (early == 1) cp_async_wait<1>();
     else cp_async_wait<0>();
     __syncthreads();
@@ -1016,6 +1039,8 @@ static cudaError_t launch_d(const AttendParams& p, cudaStream_t s) {
   const size_t sm = smem_bytes<D>();
   cudaError_t e = cudaFuncSetAttribute(attend_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(sm));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(attend_kernel<D>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.max_chunks, p.kv_heads, p.batch);

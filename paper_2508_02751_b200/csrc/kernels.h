@@ -107,6 +107,7 @@ struct AttendParams {
   int32_t group_sel;          // variant f2: selection rows are (layer, kv-group); marg_w is
                               // [L*H_kv][B][max_marg][8] per-head weights
   uint8_t* plan;              // gather plan (smallkv_plan) or nullptr
+  int32_t n_layers;           // LLM layers the plan holds (next-layer L2 prefetch)
   // variant f4 (host-tiered pool): rows come from a per-(layer, b, kv-group) hot pool
   // [B][H_kv][hot_cap][d] per layer slot; entry e of the group's list lives in slot
   // entry_slot[((layer*B + b)*H_kv + g)*hot_cap + e]

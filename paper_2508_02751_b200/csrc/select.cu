@@ -23,9 +23,13 @@
 //   locates I.
 // Both lists are then emitted in ascending order by one writing pass with
 // per-warp ballot prefix sums (per-warp counts come from the per-warp
-// histograms and the boundary candidates; the fallback adds a counting pass).  Rows up to kSmemCap tokens
-// are held in shared memory; longer rows are re-read from global memory (they
-// stay L2-resident across the passes).  All reductions use a fixed order.
+// histograms and the boundary candidates; the fallback adds a counting pass).
+// Row storage by length: up to kThreads*kRegRow (4096) tokens the row lives in
+// registers (16 consecutive positions per thread, bins packed 4 per register,
+// SIMD byte compares for the candidate and emission passes, output offsets
+// from one block-wide scan); up to kSmemCap tokens it is staged in shared
+// memory; longer rows are re-read from global memory (L2-resident across the
+// passes).  All reductions use a fixed order.
 #include <float.h>
 #include <math.h>
 
@@ -39,10 +43,17 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kBins = 256;
 constexpr int kCandCap = 1024;
+constexpr int kRegRow = 16;     // rows up to kThreads * 16 tokens are held in registers
 constexpr int kSmemCap = 8192;   // rows staged in shared memory (40 KB); longer rows read L2 directly
                                  // (measured faster from 16K tokens up: more CTAs per SM)
 
 __device__ __forceinline__ int iclamp(int x, int lo, int hi) { return x < lo ? lo : (x > hi ? hi : x); }
+// 0xff in byte k iff k < r (r positions left in a 4-position word; r <= 0: none)
+__device__ __forceinline__ uint32_t valid_bytes(int r) {
+  return r >= 4 ? 0xffffffffu : (r <= 0 ? 0u : (1u << (8 * r)) - 1u);
+}
+// byte mask (0x00 / 0xff per byte) -> 4-bit mask
+__device__ __forceinline__ uint32_t bytes_to_bits(uint32_t x) { return ((x & 0x08040201u) * 0x01010101u) >> 24; }
 
 // deterministic combine of per-thread (max, Σexp) pairs
 __device__ __forceinline__ void lse_combine(float& m, float& s, float m2, float s2) {
@@ -51,8 +62,15 @@ __device__ __forceinline__ void lse_combine(float& m, float& s, float m2, float 
   m = mm;
 }
 
-template <bool kInSmem, bool kLogBins>
-__global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) {
+// kRegE > 0 (rows of <= kThreads * kRegE tokens): each thread holds positions
+// [kRegE*tid, kRegE*tid + kRegE) of the row in registers for the histogram,
+// candidate and emission passes (no staging, no per-warp segments: output
+// offsets come from one block-wide scan); the rare refinement / radix paths
+// re-read the row from global memory (L2).
+template <bool kInSmem, bool kLogBins, int kRegE>
+__global__ void __launch_bounds__(kThreads, kRegE > 0 ? 4 : 1) select_kernel(const SelectParams p) {
+  constexpr bool kRegs = kRegE > 0;
+  static_assert(!(kRegs && kInSmem), "register rows read the rare paths from global memory");
   extern __shared__ __align__(16) float vals[];   // [n] row, then (kInSmem) [n] bin bytes (+16)
   __shared__ uint32_t hist[kWarps][kBins];
   __shared__ unsigned long long cand[2][kCandCap];
@@ -101,6 +119,28 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
     return make_float4(score[i], score[i + 1], score[i + 2], score[i + 3]);
   };
 
+  float x[kRegs ? kRegE : 1];
+  uint32_t pbin[kRegs ? kRegE / 4 : 1];
+  const int i0 = kRegs ? kRegE * tid : 0;
+  if (kRegs && !accrow) {
+#pragma unroll
+    for (int q = 0; q < (kRegs ? kRegE / 4 : 0); ++q) {
+      const int i = i0 + 4 * q;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (g_al && i + 3 < n) {
+        v = *reinterpret_cast<const float4*>(row + i);
+      } else {
+        if (i < n) v.x = row[i];
+        if (i + 1 < n) v.y = row[i + 1];
+        if (i + 2 < n) v.z = row[i + 2];
+        if (i + 3 < n) v.w = row[i + 3];
+      }
+      x[4 * q] = v.x;
+      x[4 * q + 1] = v.y;
+      x[4 * q + 2] = v.z;
+      x[4 * q + 3] = v.w;
+    }
+  }
   // ---- pass 1: stage the row; (max, Σexp) over [0, n) and the ranked range
   // [min, max] over [0, N) are merged from K1's per-chunk statistics (fixed order)
   if (kInSmem && !accrow) {
@@ -148,7 +188,22 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
   if (accrow) {
     // f1: acc[v] += a'_v for v < n (in place), rank on acc; range over [0, N)
     float lo = FLT_MAX, hi = -FLT_MAX;
-    for (int i = tid; i < n; i += kThreads) {
+    if (kRegs) {
+#pragma unroll
+      for (int e = 0; e < (kRegs ? kRegE : 0); ++e) {
+        const int i = i0 + e;
+        if (i < n) {
+          const float v = accrow[i] + __expf(row[i] - lse);
+          accrow[i] = v;
+          x[e] = v;
+          if (i < N) {
+            lo = fminf(lo, v);
+            hi = fmaxf(hi, v);
+          }
+        }
+      }
+    }
+    for (int i = kRegs ? n : tid; i < n; i += kThreads) {
       const float v = accrow[i] + __expf(row[i] - lse);
       accrow[i] = v;
       if (kInSmem) vals[i] = v;
@@ -206,7 +261,19 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
     for (int i = tid; i < kWarps * kBins; i += kThreads) (&hist[0][0])[i] = 0u;
     __syncthreads();
     uint8_t* sbin = reinterpret_cast<uint8_t*>(vals + n);
-    if (kInSmem) {
+    if (kRegs) {
+#pragma unroll
+      for (int q = 0; q < (kRegs ? kRegE / 4 : 0); ++q) {
+        uint32_t packed = 0u;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int bin = iclamp(static_cast<int>((bv(x[4 * q + k]) - blo) * scale), 0, kBins - 1);
+          packed |= static_cast<uint32_t>(bin) << (8 * k);
+          if (i0 + 4 * q + k < N) atomicAdd(&hist[warp][bin], 1u);
+        }
+        pbin[q] = packed;
+      }
+    } else if (kInSmem) {
       // 4 consecutive positions per lane: one 16-B load, one 4-B bin store
       for (int base = s0 + 4 * lane; base < s1; base += 128) {
         const float4 v4 = *reinterpret_cast<const float4*>(vals + base);
@@ -330,8 +397,7 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
       if (tid < 2) s_cnt[tid] = 0;
       __syncthreads();
       const uint8_t* sbin = reinterpret_cast<const uint8_t*>(vals + n);
-      auto take = [&](int i, int bin) {
-        const float v = VAL(i);
+      auto take = [&](int i, int bin, float v) {
         const unsigned long long kv =
             (static_cast<unsigned long long>(desc_key(v)) << 32) | static_cast<uint32_t>(i);
         if (bin == binA && (!s_refine[0] || sub_of(0, v) == s_sub[0]))
@@ -339,7 +405,23 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
         if (bin == binB && !shared && (!s_refine[1] || sub_of(1, v) == s_sub[1]))
           cand[1][atomicAdd(&s_cnt[1], 1)] = kv;
       };
-      if (kInSmem) {
+      if (kRegs) {
+        // SIMD byte compares of the packed bins, 4 positions per instruction
+        const uint32_t pa = binA >= 0 ? static_cast<uint32_t>(binA) * 0x01010101u : 0u;
+        const uint32_t pb = static_cast<uint32_t>(binB) * 0x01010101u;
+#pragma unroll
+        for (int q = 0; q < (kRegs ? kRegE / 4 : 0); ++q) {
+          uint32_t hit = __vcmpeq4(pbin[q], pb);
+          if (binA >= 0) hit |= __vcmpeq4(pbin[q], pa);
+          hit = bytes_to_bits(hit & valid_bytes(N - (i0 + 4 * q)));
+          if (hit) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if ((hit >> k) & 1u)
+                take(i0 + 4 * q + k, static_cast<int>((pbin[q] >> (8 * k)) & 0xffu), x[4 * q + k]);
+          }
+        }
+      } else if (kInSmem) {
         // 4 bin bytes per load; SIMD byte compares skip words without a boundary bin
         const uint32_t pa = binA >= 0 ? static_cast<uint32_t>(binA) * 0x01010101u : 0u;
         const uint32_t pb = static_cast<uint32_t>(binB) * 0x01010101u;
@@ -350,7 +432,7 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
           if (hit == 0u) continue;
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            if (((hit >> (8 * k)) & 0xffu) && i4 + k < N) take(i4 + k, static_cast<int>((w >> (8 * k)) & 0xffu));
+            if (((hit >> (8 * k)) & 0xffu) && i4 + k < N) take(i4 + k, static_cast<int>((w >> (8 * k)) & 0xffu), VAL(i4 + k));
         }
       } else {
         for (int i4 = 4 * tid; i4 < N; i4 += 4 * kThreads) {
@@ -360,7 +442,7 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
           for (int k = 0; k < 4; ++k) {
             if (i4 + k >= N) break;
             const int bin = iclamp(static_cast<int>((bv(vv[k]) - blo) * scale), 0, kBins - 1);
-            if (bin == binA || bin == binB) take(i4 + k, bin);
+            if (bin == binA || bin == binB) take(i4 + k, bin, vv[k]);
           }
         }
       }
@@ -390,7 +472,7 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
       // selected candidates of each warp's segment (no counting pass)
       if (tid < 2 * kWarps) (&wsel[0][0])[tid] = 0;
       __syncthreads();
-      for (int t = 0; t < 2; ++t) {
+      for (int t = 0; t < (kRegs ? 0 : 2); ++t) {
         const int rr = t == 0 ? rA : rB;
         if (rr == 0) continue;
         const int li = (t == 1 && shared) ? 0 : t;
@@ -401,7 +483,7 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
           if (v <= thr) atomicAdd(&wsel[static_cast<int>(v & 0xffffffffu) / seg][t], 1);
         }
       }
-      if (!refine) {   // (after a refinement the per-warp histograms are gone: recount)
+      if (!refine && !kRegs) {   // (after a refinement the per-warp histograms are gone: recount)
         int ab[2] = {0, 0};
         for (int t = 0; t < 2; ++t) {
           const int bt_ = (t == 0 && rA == 0) ? kBins : s_bin[t];
@@ -548,36 +630,84 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
       mm |= static_cast<uint32_t>(inB && !isC) << k;
     }
   };
+  int32_t* crit = p.crit_idx + rb * p.max_crit;
+  int32_t* marg = p.marg_idx + rb * p.max_marg;
+  float* mw = p.marg_w + rb * p.max_marg;
+  if constexpr (kRegs) {
+    // register rows: per-thread masks, one block-wide exclusive scan of the
+    // packed (critical | marginal << 16) counts, then each thread writes its
+    // positions in ascending order
+    // Positions in bins strictly above / below a boundary bin are decided by
+    // their bin (bins are monotone in the score and each threshold lies in its
+    // boundary bin); boundary-bin positions, and rows without bins (all ties,
+    // radix fallback), compare exactly.
+    const bool use_bins = !all_equal && !s_fallback;
+    const uint32_t ea = rA > 0 && use_bins ? static_cast<uint32_t>(s_bin[0]) * 0x01010101u : 0u;
+    const uint32_t eb = use_bins ? static_cast<uint32_t>(s_bin[1]) * 0x01010101u : 0u;
+    uint32_t cm = 0u, bsel = 0u;
+#pragma unroll
+    for (int q = 0; q < kRegE / 4; ++q) {
+      const uint32_t vm = valid_bytes(N - (i0 + 4 * q));
+      uint32_t c4 = 0u, b4 = 0u, ex = bytes_to_bits(vm);
+      if (use_bins) {
+        if (rA > 0) c4 = bytes_to_bits(__vcmpgtu4(pbin[q], ea) & vm);
+        b4 = bytes_to_bits(__vcmpgtu4(pbin[q], eb) & vm);
+        ex = bytes_to_bits(((rA > 0 ? __vcmpeq4(pbin[q], ea) : 0u) | __vcmpeq4(pbin[q], eb)) & vm);
+      }
+      if (ex) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if ((ex >> k) & 1u) {
+            const int i = i0 + 4 * q + k;
+            const float v = x[4 * q + k];
+            const uint32_t isC = ((v > XA) | ((v == XA) & (i <= IA))) ? 1u : 0u;
+            const uint32_t inB = ((v > XB) | ((v == XB) & (i <= IB))) ? 1u : 0u;
+            c4 = (c4 & ~(1u << k)) | (isC << k);
+            b4 = (b4 & ~(1u << k)) | (inB << k);
+          }
+        }
+      }
+      cm |= c4 << (4 * q);
+      bsel |= b4 << (4 * q);
+    }
+    const uint32_t mm = bsel & ~cm;
+    const int own = __popc(cm) | (__popc(mm) << 16);
+    int incl = own;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wcnt[warp][0] = incl;
+    __syncthreads();
+    int ex = incl - own;
+    for (int w = 0; w < warp; ++w) ex += wcnt[w][0];
+    int ac = ex & 0xffff, am = ex >> 16;
+    // ascending set bits; a' re-read from the logits row (L1 / L2 hit: this
+    // thread loaded it; for f1 the logit is not the ranking value anyway)
+    for (uint32_t m = cm; m; m &= m - 1u) crit[ac++] = i0 + __ffs(m) - 1;
+    for (uint32_t m = mm; m; m &= m - 1u) {
+      const int i = i0 + __ffs(m) - 1;
+      marg[am] = i;
+      mw[am] = __expf(row[i] - lse);   // a' of the current step (Eq. 6)
+      ++am;
+    }
+    return;
+  }
   if (!s_have_counts) {
     int cc = 0, cb = 0;
-    if (true) {
-      for (int base = s0 + 4 * lane; base < s1; base += 128) {
-        uint32_t cm, mm;
-        float xs[4];
-        classify4(base, cm, mm, xs);
-        cc += __popc(cm);
-        cb += __popc(mm);
-      }
-      cc = warp_sum_i(cc);
-      cb = warp_sum_i(cb);
-      if (lane == 0) {
-        wcnt[warp][0] = cc;
-        wcnt[warp][1] = cb;
-      }
-    } else {
-      for (int base = s0; base < s1; base += 32) {
-        const int i = base + lane;
-        const bool valid = i < s1;
-        const float x = valid ? VAL(i) : -FLT_MAX;
-        const bool isC = valid && (x > XA || (x == XA && i <= IA));
-        const bool inB = valid && (x > XB || (x == XB && i <= IB));
-        cc += __popc(__ballot_sync(0xffffffffu, isC));
-        cb += __popc(__ballot_sync(0xffffffffu, inB));
-      }
-      if (lane == 0) {
-        wcnt[warp][0] = cc;
-        wcnt[warp][1] = cb - cc;
-      }
+    for (int base = s0 + 4 * lane; base < s1; base += 128) {
+      uint32_t cm, mm;
+      float xs[4];
+      classify4(base, cm, mm, xs);
+      cc += __popc(cm);
+      cb += __popc(mm);
+    }
+    cc = warp_sum_i(cc);
+    cb = warp_sum_i(cb);
+    if (lane == 0) {
+      wcnt[warp][0] = cc;
+      wcnt[warp][1] = cb;
     }
     __syncthreads();
   }
@@ -586,60 +716,34 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const SelectParams p) 
     oc += wcnt[w][0];
     om += wcnt[w][1];
   }
-  int32_t* crit = p.crit_idx + rb * p.max_crit;
-  int32_t* marg = p.marg_idx + rb * p.max_marg;
-  float* mw = p.marg_w + rb * p.max_marg;
-  if (true) {
-    // 128 positions per warp step: per-lane masks, one packed warp scan
-    for (int base0 = s0; base0 < s1; base0 += 128) {
-      const int base = base0 + 4 * lane;
-      uint32_t cm, mm;
-      float xs[4];
-      classify4(base, cm, mm, xs);
-      const int own = __popc(cm) | (__popc(mm) << 16);
-      int incl = own;
+  // 128 positions per warp step: per-lane masks, one packed warp scan
+  for (int base0 = s0; base0 < s1; base0 += 128) {
+    const int base = base0 + 4 * lane;
+    uint32_t cm, mm;
+    float xs[4];
+    classify4(base, cm, mm, xs);
+    const int own = __popc(cm) | (__popc(mm) << 16);
+    int incl = own;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      int ac = oc + ((incl - own) & 0xffff), am = om + ((incl - own) >> 16);
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int ac = oc + ((incl - own) & 0xffff), am = om + ((incl - own) >> 16);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if ((cm >> k) & 1u) crit[ac++] = base + k;
-        if ((mm >> k) & 1u) {
-          marg[am] = base + k;
-          mw[am] = __expf((accrow ? row[base + k] : xs[k]) - lse);   // a' of the current step (Eq. 6)
-          ++am;
-        }
+    for (int k = 0; k < 4; ++k) {
+      if ((cm >> k) & 1u) crit[ac++] = base + k;
+      if ((mm >> k) & 1u) {
+        marg[am] = base + k;
+        mw[am] = __expf((accrow ? row[base + k] : xs[k]) - lse);   // a' of the current step (Eq. 6)
+        ++am;
       }
-      const int tot = __shfl_sync(0xffffffffu, incl, 31);
-      oc += tot & 0xffff;
-      om += tot >> 16;
     }
-  } else {
-    for (int base = s0; base < s1; base += 32) {
-      const int i = base + lane;
-      const bool valid = i < s1;
-      const float x = valid ? VAL(i) : -FLT_MAX;
-      const bool isC = valid && (x > XA || (x == XA && i <= IA));
-      const bool inB = valid && (x > XB || (x == XB && i <= IB));
-      const bool isM = inB && !isC;
-      const uint32_t bc = __ballot_sync(0xffffffffu, isC);
-      const uint32_t bm = __ballot_sync(0xffffffffu, isM);
-      const int c_at = oc + __popc(bc & lt), m_at = om + __popc(bm & lt);
-      if (isC) crit[c_at] = i;
-      if (isM) {
-        marg[m_at] = i;
-        mw[m_at] = __expf((accrow ? row[i] : x) - lse);   // a' of the current step (Eq. 6)
-      }
-      oc += __popc(bc);
-      om += __popc(bm);
-    }
+    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+    oc += tot & 0xffff;
+    om += tot >> 16;
   }
 }
-
-
 
 // ---------------------------------------------------------------------------
 // Variant f2 (R16): group score rows and per-head marginal weights.
@@ -805,14 +909,16 @@ cudaError_t launch_select(const SelectParams& p, int32_t max_rows, int32_t max_s
   cfg.attrs = attr;
   cfg.numAttrs = overlap_previous ? 1 : 0;
   cudaError_t e;
-  if (max_seq_len <= kSmemCap) {
+  if (max_seq_len <= kThreads * kRegRow) {
+    e = cudaLaunchKernelEx(&cfg, p.log_bins ? select_kernel<false, true, kRegRow> : select_kernel<false, false, kRegRow>, p);
+  } else if (max_seq_len <= kSmemCap) {
     cfg.dynamicSmemBytes = static_cast<size_t>(max_seq_len) * 5 + 16;
-    auto k = p.log_bins ? select_kernel<true, true> : select_kernel<true, false>;
+    auto k = p.log_bins ? select_kernel<true, true, 0> : select_kernel<true, false, 0>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(cfg.dynamicSmemBytes));
     e = cudaLaunchKernelEx(&cfg, k, p);
   } else {
-    e = cudaLaunchKernelEx(&cfg, p.log_bins ? select_kernel<false, true> : select_kernel<false, false>, p);
+    e = cudaLaunchKernelEx(&cfg, p.log_bins ? select_kernel<false, true, 0> : select_kernel<false, false, 0>, p);
   }
   if (e != cudaSuccess) return e;
   return cudaGetLastError();

@@ -526,6 +526,7 @@ int fill_attend_params(skv::AttendParams& ap, const smallkv_cache* llm, const sm
   ap.kv_heads = llm->num_kv_heads;
   ap.head_dim = llm->head_dim;
   ap.batch = batch->batch;
+  ap.n_layers = n_llm_layers;
   ap.row_stride = batch->max_seq_len;
   ap.max_crit = budgets->max_crit;
   ap.max_marg = budgets->max_marg;

@@ -132,6 +132,21 @@ def test_duplicate_keys_exact_ties():
     _check(p)
 
 
+@pytest.mark.parametrize("n", [4000, 8000, 12000])
+def test_massive_ties_radix_fallback(n):
+    """Two distinct K' rows (alternating by page): two distinct logits, so the
+    boundary bins (and their sub-bins) hold thousands of equal keys and K2 takes
+    the exact radix select + index tie-break.  n covers the three K2 variants
+    (register rows, shared-memory rows, global rows)."""
+    cfg = _cfg(n=n, B=1, budget=(n // 10, 20, n // 10))
+    p = synth.make_problem(cfg, seed=21, page_size=256, seq_lens=[n])
+    k = p.slm.k.clone()
+    k[:, 0::2] = p.slm.k[:, :1, :, :1]        # even pages: page 0's first row
+    k[:, 1::2] = p.slm.k[:, 1:2, :, :1]       # odd pages: page 1's first row
+    p = dataclasses.replace(p, slm=dataclasses.replace(p.slm, k=k)).to("cuda")
+    _check(p)
+
+
 def test_extreme_logits():
     """Logits near ±80 (fp32 exp underflow): ranking on logits stays exact."""
     cfg = _cfg(n=800, B=1, budget=(80, 20, 100))
@@ -245,12 +260,15 @@ def test_two_valued_logits_radix_fallback():
     _check(p)
 
 
-def test_dense_boundary_bin_refinement():
+@pytest.mark.parametrize("n", [32000, 4000])
+def test_dense_boundary_bin_refinement(n):
     """A few outlier logits stretch the value-linear histogram so that the
     boundary bin holds thousands of positions: K2 refines inside that bin
-    (256 sub-bins) instead of falling back to the radix select."""
-    cfg = _cfg(n=32000, B=1, budget=(3200, 500, 3200))
-    p = synth.make_problem(cfg, seed=17, page_size=64, seq_lens=[32000])
+    (256 sub-bins) instead of falling back to the radix select.  n = 4000 runs
+    the register-row variant (rows <= 4096 tokens), whose refinement re-reads
+    the row from global memory."""
+    cfg = _cfg(n=n, B=1, budget=(n // 10, n // 64, n // 10))
+    p = synth.make_problem(cfg, seed=17, page_size=64, seq_lens=[n])
     k = p.slm.k.clone()
     k[:, :, :, 3] *= 40.0                 # one row per page: far outliers (both signs)
     p = dataclasses.replace(p, slm=dataclasses.replace(p.slm, k=k)).to("cuda")
