@@ -802,48 +802,76 @@ __global__ void __launch_bounds__(kGroupThreads) group_score_kernel(const GroupP
   const int n = p.seq_lens[b];
   const int N = n - iclamp(p.n_recent[b], 0, n);
   float* out = p.score + (static_cast<int64_t>(gl) * p.batch + b) * p.row_stride;
+  // distinct rows only (first occurrence order), each with its multiplicity
+  int nd = 0;
   const float* rowp[8];
+  float dm[8], dl[8];
 #pragma unroll
-  for (int h = 0; h < 8; ++h)
-    rowp[h] = p.logits + (static_cast<int64_t>(s_j[h < G ? h : 0]) * p.batch + b) * p.row_stride;
+  for (int h = 0; h < 8; ++h) {
+    rowp[h] = nullptr;
+    dm[h] = 0.f;
+    dl[h] = 0.f;
+  }
+  for (int h = 0; h < G; ++h) {
+    if (s_mult[h] == 0.f) continue;
+#pragma unroll
+    for (int d = 0; d < 8; ++d)
+      if (d == nd) {
+        rowp[d] = p.logits + (static_cast<int64_t>(s_j[h]) * p.batch + b) * p.row_stride;
+        dm[d] = s_mult[h];
+        dl[d] = s_lse[h];
+      }
+    ++nd;
+  }
   float lo = FLT_MAX, hi = -FLT_MAX;
-  // 4 consecutive positions per thread and all G rows' loads in flight at once
-  for (int v0 = 4 * tid; v0 < n; v0 += 4 * kGroupThreads) {
-    float x[8][4];
-    const bool vec = (p.row_stride & 3) == 0 && v0 + 3 < n;   // 16-byte loads
+  // 4 consecutive positions per thread per step, U steps per round: each
+  // distinct row's U 16-byte loads are in flight together
+  constexpr int U = 4;
+  const bool al = (p.row_stride & 3) == 0;
+  for (int r0 = 4 * tid; r0 < n; r0 += U * 4 * kGroupThreads) {
+    float f[U][4];
 #pragma unroll
-    for (int h = 0; h < 8; ++h) {
-      if (h >= G || s_mult[h] == 0.f) continue;
-      if (vec) {
-        const float4 f4 = __ldg(reinterpret_cast<const float4*>(rowp[h] + v0));
-        x[h][0] = f4.x;
-        x[h][1] = f4.y;
-        x[h][2] = f4.z;
-        x[h][3] = f4.w;
-      } else {
+    for (int it = 0; it < U; ++it) f[it][0] = f[it][1] = f[it][2] = f[it][3] = 0.f;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) x[h][u] = v0 + u < n ? __ldg(rowp[h] + v0 + u) : 0.f;
+    for (int d = 0; d < 8; ++d) {
+      if (d >= nd) break;
+      float x[U][4];
+#pragma unroll
+      for (int it = 0; it < U; ++it) {
+        const int v0 = r0 + it * 4 * kGroupThreads;
+        if (al && v0 + 3 < n) {
+          const float4 f4 = __ldg(reinterpret_cast<const float4*>(rowp[d] + v0));
+          x[it][0] = f4.x;
+          x[it][1] = f4.y;
+          x[it][2] = f4.z;
+          x[it][3] = f4.w;
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) x[it][u] = v0 + u < n ? __ldg(rowp[d] + v0 + u) : 0.f;
+        }
       }
-    }
-    float f[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int v = v0 + u;
-      f[u] = 0.f;
+      for (int it = 0; it < U; ++it)
 #pragma unroll
-      for (int h = 0; h < 8; ++h)
-        if (h < G && s_mult[h] != 0.f) f[u] += s_mult[h] * __expf(x[h][u] - s_lse[h]);
-      if (v < N) {
-        lo = fminf(lo, f[u]);
-        hi = fmaxf(hi, f[u]);
-      }
+        for (int u = 0; u < 4; ++u) f[it][u] += dm[d] * __expf(x[it][u] - dl[d]);
     }
-    if (vec) {
-      *reinterpret_cast<float4*>(out + v0) = make_float4(f[0], f[1], f[2], f[3]);
-    } else {
+#pragma unroll
+    for (int it = 0; it < U; ++it) {
+      const int v0 = r0 + it * 4 * kGroupThreads;
+      if (v0 >= n) break;
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        if (v0 + u < n) out[v0 + u] = f[u];
+        if (v0 + u < N) {
+          lo = fminf(lo, f[it][u]);
+          hi = fmaxf(hi, f[it][u]);
+        }
+      if (al && v0 + 3 < n) {
+        *reinterpret_cast<float4*>(out + v0) = make_float4(f[it][0], f[it][1], f[it][2], f[it][3]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (v0 + u < n) out[v0 + u] = f[it][u];
+      }
     }
   }
   lo = -warp_max(-lo);
