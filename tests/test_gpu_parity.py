@@ -370,14 +370,28 @@ def test_qwen14b_full_size_sampled():
     print("qwen14b n=16384", _full_size_sampled(cfg16, budget=(1638, 819, 1638), n_seqs=2))
 
 
-def test_f1_accumulated_score_multistep():
+@pytest.mark.parametrize("n", [4096, 4097, 6000, 9000])
+def test_select_row_storage_variants(n):
+    """K2 keeps a row in registers (n <= 4096), shared memory (<= 8192) or
+    reads it from global memory (longer): the same exact split from each,
+    at the boundaries of the variants, with a ragged second sequence."""
+    cfg = _cfg(n=n, B=2, budget=(n // 10, n // 20, n // 10))
+    p = synth.make_problem(cfg, seed=23, page_size=16, seq_lens=[n, n // 3 + 1]).to("cuda")
+    rep, _, _ = _check(p)
+    print(n, rep)
+
+
+@pytest.mark.parametrize("n0", [1500, 6000, 9000])
+def test_f1_accumulated_score_multistep(n0):
     """Variant f1 over 4 decode steps (n grows by one each step): the GPU's
     running sums track the oracle's fp64 chain and the sets match within the
-    A18 band (relative 1e-6 for sums > 1), outputs within 2e-3."""
+    A18 band (relative 1e-6 for sums > 1), outputs within 2e-3.  n0 covers the
+    register / shared-memory / global K2 variants."""
     import oracle
     from paper_2508_02751_b200 import smallkv
-    cfg = _cfg(n=1500, B=2, budget=(120, 40, 160))
-    p = synth.make_problem(cfg, seed=17, page_size=16, seq_lens=[1500, 900]).to("cuda")
+    n1 = 900 if n0 == 1500 else n0 // 2
+    cfg = _cfg(n=n0, B=2, budget=(120, 40, 160))
+    p = synth.make_problem(cfg, seed=17, page_size=16, seq_lens=[n0, n1]).to("cuda")
     step = smallkv.from_problem(p)
     acc = torch.zeros_like(step.out.logits)
     pc = p.to("cpu")
@@ -385,14 +399,14 @@ def test_f1_accumulated_score_multistep():
     rows = oracle.image_rows(pc.head_map)
     oacc = np.zeros((len(rows), p.batch, p.max_seq_len), np.float64)
     for d in (3, 2, 1, 0):
-        sl = torch.tensor([1500 - d, 900 - d], dtype=torch.int32)
+        sl = torch.tensor([n0 - d, n1 - d], dtype=torch.int32)
         p.seq_lens.copy_(sl)
         sel_gpu = step.select(p.slm_q, acc=acc)
         torch.cuda.synchronize()
         sel = oracle.select_acc(pc.slm_q, slm_view, sl, rows, pc.k_crit, pc.n_recent,
                                 pc.k_marg, p.max_crit, p.max_marg, p.max_seq_len, oacc)
     ga = acc.cpu().double().numpy()[rows]
-    for b, n in enumerate([1500, 900]):
+    for b, n in enumerate([n0, n1]):
         np.testing.assert_allclose(ga[:, b, :n], oacc[:, b, :n], rtol=2e-5, atol=1e-7)
     # sets: ranked by the oracle's running sums
     pcs = dataclasses.replace(pc, seq_lens=sl)
