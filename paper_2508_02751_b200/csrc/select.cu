@@ -240,7 +240,11 @@ __global__ void __launch_bounds__(kThreads, kRegE > 0 ? 4 : 5) select_kernel(con
   // Histogram coordinate: the score itself, or (variant f2's group scores —
   // sums of probabilities, heavily skewed towards 0) its logarithm.  Either is
   // monotone, so bins stay ordered like scores; exactness comes from the keys.
-  auto bv = [&](float v) { return kLogBins ? logf(fmaxf(v, 1e-30f)) : v; };
+  // (log coordinate: the bit pattern of a positive float, a monotone piecewise-
+  // linear log2 — integer conversion instead of a full-precision logf)
+  auto bv = [&](float v) {
+    return kLogBins ? static_cast<float>(__float_as_uint(fmaxf(v, 1e-30f))) : v;
+  };
   const float blo = bv(vlo);
   const float scale = 255.99f / (bv(vhi) - blo);
   const bool all_equal = !(vhi > vlo);
