@@ -546,17 +546,19 @@ class DecodeGraph:
         """select + attends with the host copies on side streams (see __init__)."""
         h_slm_q, h_q, h_out = self.host_io
         main = torch.cuda.current_stream()
+        # q' first (select needs it); the layers' q copies are forked after it,
+        # so that they do not queue ahead of q' on the host link, and run on a
+        # side stream under select (one join before the first attend:
+        # per-layer joins cost more than they save)
+        self.slm_q.copy_(h_slm_q, non_blocking=True)
         start = torch.cuda.Event()
         start.record(main)
-        # the layers' q copies run on a side stream under select (one join
-        # before the first attend: per-layer joins cost more than they save)
         self.h2d_stream.wait_event(start)
         with torch.cuda.stream(self.h2d_stream):
             for i, (_, _, q, _) in enumerate(self.plan):
                 q.copy_(h_q[i], non_blocking=True)
             q_ready = torch.cuda.Event()
             q_ready.record(self.h2d_stream)
-        self.slm_q.copy_(h_slm_q, non_blocking=True)
         self.step.select(self.slm_q)
         main.wait_event(q_ready)
         for i, (layer, slot, q, out) in enumerate(self.plan):
