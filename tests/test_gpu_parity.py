@@ -608,3 +608,41 @@ def test_f3b_partitioned_slm_virtual_ranks_bit_identical():
         target.attend(p.llm_layer_ids[slot], slot, p.llm_q[slot], out, overlap_prologue=slot > 0)
         torch.cuda.synchronize()
         assert torch.equal(out, full[slot])
+
+
+# ---------------------------------------------------------------- public API: graphs
+
+@pytest.mark.parametrize("adjacent", [True, False])
+def test_decode_graph_host_io_matches_device_run(adjacent):
+    """DecodeGraph(host_io=...) (the e2e path of bench.py): q' and every layer's
+    q copied in from pinned host memory, every layer's output read back inside
+    the graph (pairs of layers in one copy when the buffers are adjacent, per
+    layer otherwise; an odd layer count leaves a single last layer).  The host
+    outputs equal the eager device run bit for bit, and the oracle check of the
+    device run holds."""
+    from paper_2508_02751_b200 import smallkv
+    cfg = _cfg(llm=(3, 8, 2, 128), slm=(2, 8, 2, 64), n=1300, B=2, budget=(130, 50, 130))
+    p = synth.make_problem(cfg, seed=31, page_size=16, seq_lens=[1300, 777]).to("cuda")
+    L = p.llm.num_layers
+    step, _, outs_ref = parity.run_gpu_step(p)
+    shape = (p.batch, cfg.llm.q_heads, cfg.llm.head_dim)
+    if adjacent:
+        outs_all = torch.empty((L,) + shape, dtype=torch.float32, device="cuda")
+        outs = [outs_all[l] for l in range(L)]
+        h_out = torch.zeros((L,) + shape, dtype=torch.float32, pin_memory=True)
+    else:
+        outs = [torch.empty(shape, dtype=torch.float32, device="cuda") for _ in range(L)]
+        h_out = [torch.zeros(shape, dtype=torch.float32, pin_memory=True) for _ in range(L)]
+    h_slm_q = p.slm_q.cpu().pin_memory()
+    h_q = [p.llm_q[l].cpu().pin_memory() for l in range(L)]
+    q_dev = [torch.zeros_like(p.llm_q[l]) for l in range(L)]
+    slm_q_dev = torch.zeros_like(p.slm_q)
+    plan = [(p.llm_layer_ids[l], l, q_dev[l], outs[l]) for l in range(L)]
+    g = smallkv.DecodeGraph(step, slm_q_dev, plan, host_io=(h_slm_q, h_q, h_out))
+    for _ in range(2):
+        g.replay()
+    g.stream.synchronize()
+    for l in range(L):
+        assert torch.equal(h_out[l], outs_ref[l].cpu()), l
+    rep, _, _ = _check(p)
+    print("host_io", adjacent, rep)
