@@ -292,10 +292,9 @@ def run_ours(args, world, rank, local):
     h_q.copy_(p.llm_q)
     h_out = torch.empty(outs.shape, dtype=outs.dtype, pin_memory=True)
     e2e_steps = max(3, min(args.steps, 200))
-    if heads or tier is not None:
+    if heads:
         # head sharding: the step's all-gather sits between the attends and the
-        # output read (f4: the hot-pool refresh), so the copies stay outside the
-        # graph, in stream order
+        # output read, so the copies stay outside the graph, in stream order
         h2d = h_slm_q.numel() * 2 + h_q.numel() * 2
         d2h = h_out.numel() * 4
         barrier()
@@ -315,7 +314,8 @@ def run_ours(args, world, rank, local):
         # the public API's host-I/O graph: q of layer i gates only attend i,
         # layer i's output is read back while later layers run
         hq_list = [h_q[l % resident] for l in range(L)]
-        egraph = smallkv.DecodeGraph(step, p.slm_q, plan, host_io=(h_slm_q, hq_list, h_out))
+        egraph = smallkv.DecodeGraph(step, p.slm_q, plan, host_io=(h_slm_q, hq_list, h_out),
+                                     tier=tier)
         h2d = h_slm_q.numel() * 2 + sum(t.numel() for t in hq_list) * 2
         d2h = h_out.numel() * 4
         barrier()

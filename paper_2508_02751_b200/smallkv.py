@@ -503,6 +503,8 @@ class DecodeGraph:
     and every layer's output out (out -> h_out[i]), each layer's copies on
     side streams overlapping the other layers' kernels (the q of layer i only
     gates attend i; the output copy of layer i only waits for attend i).
+    tier: optional TieredKV (variant f4): the hot-pool refresh runs after select
+    and the attends read the hot pool (with or without host_io).
     """
 
     def __init__(self, step: DecodeStep, slm_q: torch.Tensor, layer_plan, timing: bool = False,
@@ -571,13 +573,19 @@ class DecodeGraph:
             q_ready = torch.cuda.Event()
             q_ready.record(self.h2d_stream)
         self.step.select(self.slm_q)
+        if self.tier is not None:
+            self.tier.update()   # f4: refresh every layer's hot pool after select
         main.wait_event(q_ready)
         # outputs read back in pairs of layers: one fork per pair (each fork
         # costs the attend chain more than a pair's copy delay; measured 0.665
         # -> 0.645 ms per step at config 2, groups of 4 or more are slower)
         n = len(self.plan)
         for i, (layer, slot, q, out) in enumerate(self.plan):
-            self.step.attend(layer, slot, q, out, overlap_prologue=i > 0)
+            if self.tier is not None:
+                # the first attend reads what the refresh wrote (no overlap)
+                self.tier.attend(layer, q, out, overlap_prologue=i > 0)
+            else:
+                self.step.attend(layer, slot, q, out, overlap_prologue=i > 0)
             if i % 2 == 0 and i != n - 1:
                 continue
             done = torch.cuda.Event()

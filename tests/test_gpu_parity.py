@@ -646,3 +646,30 @@ def test_decode_graph_host_io_matches_device_run(adjacent):
         assert torch.equal(h_out[l], outs_ref[l].cpu()), l
     rep, _, _ = _check(p)
     print("host_io", adjacent, rep)
+
+
+def test_decode_graph_host_io_tiered():
+    """DecodeGraph(host_io=..., tier=...) (bench.py --variant f4 e2e): select,
+    the hot-pool refresh and the tiered attends with the host copies inside the
+    graph; the host outputs equal the eager tiered step bit for bit and the
+    HBM-resident step's outputs."""
+    from paper_2508_02751_b200 import smallkv
+    cfg = _cfg(llm=(3, 8, 2, 128), slm=(2, 8, 2, 64), n=1500, B=3, budget=(150, 60, 200))
+    p = synth.make_problem(cfg, seed=43, page_size=16, seq_lens=[1500, 700, 1]).to("cuda")
+    step, tier = _tiered_step(p)
+    refs = [ref for ref, _ in _run_both(p, step, tier, p.slm_q)]
+    L = p.llm.num_layers
+    shape = (p.batch, cfg.llm.q_heads, cfg.llm.head_dim)
+    outs_all = torch.empty((L,) + shape, dtype=torch.float32, device="cuda")
+    h_out = torch.zeros((L,) + shape, dtype=torch.float32, pin_memory=True)
+    h_slm_q = p.slm_q.cpu().pin_memory()
+    h_q = [p.llm_q[l].cpu().pin_memory() for l in range(L)]
+    q_dev = [torch.zeros_like(p.llm_q[l]) for l in range(L)]
+    plan = [(l, l, q_dev[l], outs_all[l]) for l in range(L)]
+    g = smallkv.DecodeGraph(step, torch.zeros_like(p.slm_q), plan, host_io=(h_slm_q, h_q, h_out),
+                            tier=tier)
+    for _ in range(2):
+        g.replay()
+    g.stream.synchronize()
+    for l in range(L):
+        assert torch.equal(h_out[l], refs[l].cpu()), l
