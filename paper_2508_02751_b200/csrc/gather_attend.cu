@@ -748,29 +748,40 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
     // group-wide M and L from the (m, l) of all warps — so only [8][D] floats
     // per warp go through shared memory and the final merge is a plain sum.
     __syncthreads();
+    SKV_T(8);
+    // (h0, h1 = h0 + 1) are adjacent: one 8-byte load per warp for each of m, l
+    float2 wm[kWarps], wl[kWarps];
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      wm[w] = *reinterpret_cast<const float2*>(wm_s + w * 8 + h0);
+      wl[w] = *reinterpret_cast<const float2*>(wl_s + w * 8 + h0);
+    }
     float M0 = -INFINITY, M1 = -INFINITY;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) {
-      M0 = fmaxf(M0, wm_s[w * 8 + h0]);
-      M1 = fmaxf(M1, wm_s[w * 8 + h1]);
+      M0 = fmaxf(M0, wm[w].x);
+      M1 = fmaxf(M1, wm[w].y);
     }
     const float M0u = M0 == -INFINITY ? 0.f : M0, M1u = M1 == -INFINITY ? 0.f : M1;
     float L0 = 0.f, L1 = 0.f;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) {
-      L0 += wl_s[w * 8 + h0] * exp2f(wm_s[w * 8 + h0] - M0u);
-      L1 += wl_s[w * 8 + h1] * exp2f(wm_s[w * 8 + h1] - M1u);
+      L0 += wl[w].x * exp2f(wm[w].x - M0u);
+      L1 += wl[w].y * exp2f(wm[w].y - M1u);
     }
     const float f0 = L0 > 0.f ? exp2f(m0 - M0u) / L0 : 0.f;
     const float f1 = L1 > 0.f ? exp2f(m1 - M1u) / L1 : 0.f;
-    float* myc = wo_s + warp * 8 * D;                           // [kWarps][8][D]
+    // rows padded to D + 4 floats: the 4 head rows a warp's lanes write (tq)
+    // fall in different banks
+    constexpr int RS = D + 4;
+    float* myc = wo_s + warp * 8 * RS;                          // [kWarps][8][D + 4]
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) {
       const int d0 = 16 * mt + gq;
-      myc[h0 * D + d0] = oc[mt][0] * f0 + om[mt][0];
-      myc[h1 * D + d0] = oc[mt][1] * f1 + om[mt][1];
-      myc[h0 * D + d0 + 8] = oc[mt][2] * f0 + om[mt][2];
-      myc[h1 * D + d0 + 8] = oc[mt][3] * f1 + om[mt][3];
+      myc[h0 * RS + d0] = oc[mt][0] * f0 + om[mt][0];
+      myc[h1 * RS + d0] = oc[mt][1] * f1 + om[mt][1];
+      myc[h0 * RS + d0 + 8] = oc[mt][2] * f0 + om[mt][2];
+      myc[h1 * RS + d0 + 8] = oc[mt][3] * f1 + om[mt][3];
     }
     __syncthreads();
     const int64_t bo = static_cast<int64_t>(b) * p.heads + g * G;
@@ -779,7 +790,7 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) {
-        const float4 a = *reinterpret_cast<const float4*>(wo_s + (w * 8 + h) * D + c4);
+        const float4 a = *reinterpret_cast<const float4*>(wo_s + (w * 8 + h) * RS + c4);
         acc.x += a.x; acc.y += a.y; acc.z += a.z; acc.w += a.w;
       }
       *reinterpret_cast<float4*>(p.out + (bo + h) * D + c4) = acc;
