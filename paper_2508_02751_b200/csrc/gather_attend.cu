@@ -735,7 +735,8 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
   // ---- merge warps (fixed order)
   float* wm_s = reinterpret_cast<float*>(stages);              // [kWarps][8]
   float* wl_s = wm_s + kWarps * 8;                              // [kWarps][8]
-  float* wo_s = wl_s + kWarps * 8;                              // [kWarps][16][D]: O_c rows h, O_m rows 8+h
+  float* wo_s = wl_s + kWarps * 8;                              // [kWarps][16][D + 4]: O_c rows h, O_m rows 8+h
+  constexpr int RSW = D + 4;   // padded row stride of the per-warp partials (banks)
   if (gq == 0) {
     wm_s[warp * 8 + h0] = m0;
     wm_s[warp * 8 + h1] = m1;
@@ -799,24 +800,24 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
     return;
   }
   {
-    float* myo = wo_s + warp * 16 * D;
+    float* myo = wo_s + warp * 16 * RSW;                       // rows padded (bank-conflict free)
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) {
       const int d0 = 16 * mt + gq;
-      myo[h0 * D + d0] = oc[mt][0];
-      myo[h1 * D + d0] = oc[mt][1];
-      myo[h0 * D + d0 + 8] = oc[mt][2];
-      myo[h1 * D + d0 + 8] = oc[mt][3];
-      myo[(8 + h0) * D + d0] = om[mt][0];
-      myo[(8 + h1) * D + d0] = om[mt][1];
-      myo[(8 + h0) * D + d0 + 8] = om[mt][2];
-      myo[(8 + h1) * D + d0 + 8] = om[mt][3];
+      myo[h0 * RSW + d0] = oc[mt][0];
+      myo[h1 * RSW + d0] = oc[mt][1];
+      myo[h0 * RSW + d0 + 8] = oc[mt][2];
+      myo[h1 * RSW + d0 + 8] = oc[mt][3];
+      myo[(8 + h0) * RSW + d0] = om[mt][0];
+      myo[(8 + h1) * RSW + d0] = om[mt][1];
+      myo[(8 + h0) * RSW + d0 + 8] = om[mt][2];
+      myo[(8 + h1) * RSW + d0 + 8] = om[mt][3];
     }
   }
   __syncthreads();
   const int64_t bh0 = static_cast<int64_t>(b) * p.heads + g * G;
   // this CTA's merged state: [M 8][L 8][O_c 8 x D][O_m 8 x D] (read by rank 0 over DSMEM)
-  float* cst = reinterpret_cast<float*>(stages + (kWarps * 16 * D + 2 * kWarps * 8) * 4);
+  float* cst = reinterpret_cast<float*>(stages + (kWarps * 16 * RSW + 2 * kWarps * 8) * 4);
   for (int it = tid; it < G * (D / 4); it += kThreads) {
     const int h = it / (D / 4), c4 = (it % (D / 4)) * 4;
     float M = -INFINITY;
@@ -829,8 +830,8 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
     for (int w = 0; w < kWarps; ++w) {
       const float f = exp2f(wm_s[w * 8 + h] - Mu);
       L += wl_s[w * 8 + h] * f;
-      const float4 a = *reinterpret_cast<const float4*>(wo_s + (w * 16 + h) * D + c4);
-      const float4 m = *reinterpret_cast<const float4*>(wo_s + (w * 16 + h + 8) * D + c4);
+      const float4 a = *reinterpret_cast<const float4*>(wo_s + (w * 16 + h) * RSW + c4);
+      const float4 m = *reinterpret_cast<const float4*>(wo_s + (w * 16 + h + 8) * RSW + c4);
       oc.x += a.x * f; oc.y += a.y * f; oc.z += a.z * f; oc.w += a.w * f;
       om.x += m.x; om.y += m.y; om.z += m.z; om.w += m.w;
     }
