@@ -277,7 +277,10 @@ __device__ void stage_entries(const AttendParams& p, const GroupLayout& L, int b
 // K3a — gather plan for every layer of the step (one launch after select):
 // CTA (g, layer*B + b) stages the first batch of every cluster rank's share
 // of the group's list: 2 rounds of loads, 4 entries in flight per thread.
-constexpr int kPlanThreads = 256;
+#ifndef SKV_PLAN_THREADS
+#define SKV_PLAN_THREADS 128
+#endif
+constexpr int kPlanThreads = SKV_PLAN_THREADS;
 template <int D>
 __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const AttendParams p) {
   __shared__ __align__(16) GroupLayout L;
@@ -304,7 +307,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const AttendParams p
     build_tile_table(L, e0, min(kBatch, s_split[c + 1] - e0), p.group_sel != 0,
                      reinterpret_cast<uint32_t*>(rec + kHdrBytes + c * kTileTableBytes));
   }
-  constexpr int U = 4;
+  constexpr int U = 1024 / kPlanThreads;
   const int T = L.T;
   for (int base = threadIdx.x; base < T; base += U * kPlanThreads) {
     int pos[U], slot_i[U];

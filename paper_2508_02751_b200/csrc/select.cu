@@ -67,8 +67,11 @@ __device__ __forceinline__ void lse_combine(float& m, float& s, float m2, float 
 // candidate and emission passes (no staging, no per-warp segments: output
 // offsets come from one block-wide scan); the rare refinement / radix paths
 // re-read the row from global memory (L2).
+#ifndef SKV_SELECT_REG_MINB
+#define SKV_SELECT_REG_MINB 5
+#endif
 template <bool kInSmem, bool kLogBins, int kRegE>
-__global__ void __launch_bounds__(kThreads, kRegE > 0 ? 4 : 5) select_kernel(const SelectParams p) {
+__global__ void __launch_bounds__(kThreads, kRegE > 0 ? SKV_SELECT_REG_MINB : 5) select_kernel(const SelectParams p) {
   constexpr bool kRegs = kRegE > 0;
   static_assert(!(kRegs && kInSmem), "register rows read the rare paths from global memory");
   extern __shared__ __align__(16) float vals[];   // [n] row, then (kInSmem) [n] bin bytes (+16)
