@@ -53,6 +53,9 @@ slm_score_kernel(const __grid_constant__ CUtensorMap map, const SlmScoreParams p
   const int b = blockIdx.z % p.batch;
   // the select kernel of the previous layer chunk may run alongside (PDL)
   griddep_launch_dependents();
+  // launched with programmatic dependent launch behind row_flags: the CTAs
+  // become resident while it runs; nothing global is read before it completes
+  griddep_wait();
   const int G = p.heads / p.kv_heads;
   const int n = p.seq_lens[b];
   const int t_begin = blockIdx.x * p.chunk_tokens;
@@ -223,6 +226,7 @@ __global__ void row_flags_kernel(const int32_t* __restrict__ head_map, int32_t n
                                  uint8_t* __restrict__ needed, int32_t* __restrict__ rows,
                                  int32_t* __restrict__ n_rows, int32_t* __restrict__ layer_off) {
   extern __shared__ uint8_t flags[];
+  griddep_launch_dependents();   // K1 may be scheduled now; it waits for our completion
   for (int i = threadIdx.x; i < n_slm; i += blockDim.x) flags[i] = 0;
   __syncthreads();
   for (int i = threadIdx.x; i < n_llm; i += blockDim.x) {
@@ -265,15 +269,30 @@ cudaError_t launch_slm_score(const SlmScoreParams& p, const CUtensorMap& map, in
                              cudaStream_t s) {
   dim3 grid((max_seq_len + p.chunk_tokens - 1) / p.chunk_tokens, p.kv_heads,
             (p.layer_end - p.layer_begin) * p.batch);
+  // programmatic dependent launch: the grid is scheduled during the previous
+  // kernel's tail (row_flags) and waits for its completion in griddep_wait()
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e;
   if (p.head_dim == 64) {
     constexpr int sm = smem_bytes<64>();
     cudaFuncSetAttribute(slm_score_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    slm_score_kernel<64><<<grid, kThreads, sm, s>>>(map, p);
+    cfg.dynamicSmemBytes = sm;
+    e = cudaLaunchKernelEx(&cfg, slm_score_kernel<64>, map, p);
   } else {
     constexpr int sm = smem_bytes<128>();
     cudaFuncSetAttribute(slm_score_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    slm_score_kernel<128><<<grid, kThreads, sm, s>>>(map, p);
+    cfg.dynamicSmemBytes = sm;
+    e = cudaLaunchKernelEx(&cfg, slm_score_kernel<128>, map, p);
   }
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
