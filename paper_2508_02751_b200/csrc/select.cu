@@ -91,7 +91,11 @@ __global__ void __launch_bounds__(kThreads, kRegE > 0 ? SKV_SELECT_REG_MINB : 5)
   // grid (B, max_rows): the CTAs of a row are consecutive and the rows past the
   // launch's image (idle CTAs) come last
   // launched with programmatic dependent launch: K1's logits / statistics are
-  // read only after the previous grid has completed
+  // read only after the previous grid has completed.  The plan kernel that
+  // follows may be scheduled during this grid's tail; it waits for completion
+  // before reading anything (and an attend launched right after select runs
+  // without its overlap flag, include/smallkv.h)
+  griddep_launch_dependents();
   griddep_wait();
   const int r = p.layer_off[p.layer_begin] + static_cast<int>(blockIdx.y);
   if (r >= p.layer_off[p.layer_end]) return;
