@@ -291,10 +291,12 @@ size_t smallkv_attend_workspace_size(const smallkv_cache* llm,
  *               completed.  With the flag it may also start BEFORE that, and
  *               then reads the selection outputs, head_map, seq_lens,
  *               budgets, block table and K/V pools during the previous
- *               kernel's tail — so the caller guarantees those were complete
- *               before the previous kernel started (true when another kernel,
- *               e.g. a previous smallkv_attend, separates this call from
- *               smallkv_select and from the K/V append).
+ *               kernel's tail — so the caller guarantees those (and `plan`)
+ *               were complete before the previous kernel started (true when
+ *               another kernel, e.g. a previous smallkv_attend, separates this
+ *               call from smallkv_select / smallkv_plan and from the K/V
+ *               append).  The first attend after smallkv_select or
+ *               smallkv_plan must therefore be called without the flag.
  *   ws          device workspace, >= smallkv_attend_workspace_size bytes (the
  *               split work is merged inside thread-block clusters; no
  *               initialisation needed).

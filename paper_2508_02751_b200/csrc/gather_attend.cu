@@ -289,6 +289,10 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const AttendParams p
   const int NC = p.max_chunks;
   const int G = p.heads / p.kv_heads;
   const uint32_t allc = (1u << G) - 1u;
+  // the first attend of the step may be scheduled during this grid's tail: it
+  // runs without the overlap flag, so it waits for our completion before
+  // reading the plan (include/smallkv.h, smallkv_attend `flags`)
+  griddep_launch_dependents();
   griddep_wait();
   build_layout(p, layer, b, g, L);
   uint8_t* rec = p.plan + ((static_cast<int64_t>(layer) * p.batch + b) * p.kv_heads + g) *
