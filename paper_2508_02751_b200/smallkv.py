@@ -422,7 +422,8 @@ class TieredKV:
         return int(c[0]), int(c[1])
 
 
-def from_problem(p, use_plan: bool = True, variant: str = "default") -> DecodeStep:
+def from_problem(p, use_plan: bool = True, variant: str = "default",
+                 overlap_select: bool = False) -> DecodeStep:
     """DecodeStep for a smallkv_synth.Problem already on the GPU."""
     return DecodeStep(slm_k=p.slm.k, slm_block_table=p.slm.block_table,
                       slm_q_heads=p.cfg.slm.q_heads, llm_k=p.llm.k, llm_v=p.llm.v,
@@ -430,7 +431,8 @@ def from_problem(p, use_plan: bool = True, variant: str = "default") -> DecodeSt
                       llm_layers=p.cfg.llm.layers, seq_lens=p.seq_lens,
                       max_seq_len=p.max_seq_len, head_map=p.head_map, k_crit=p.k_crit,
                       n_recent=p.n_recent, k_marg=p.k_marg, max_crit=p.max_crit,
-                      max_marg=p.max_marg, use_plan=use_plan, variant=variant)
+                      max_marg=p.max_marg, use_plan=use_plan, variant=variant,
+                      overlap_select=overlap_select)
 
 
 def match_window(n: int, w_min: int = 100, w_max: int = 200, keep_last: bool = True):
