@@ -342,7 +342,9 @@ int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
  * needs it (marginal rows stay V-only, R11); rows resident at the previous
  * step are not moved.  capacity must be a multiple of 4 and >= the list size
  * R' + (#distinct rows)·(K' + M') of every group, else the group is skipped
- * and counted as an overflow (its outputs are then undefined).
+ * and counted as an overflow: its hot pool is left unchanged and
+ * smallkv_plan_tiered / smallkv_attend_tiered read nothing for it and write
+ * NaN to its heads' outputs.
  * smallkv_plan_tiered: smallkv_plan over the hot-pool slots (after
  * smallkv_tier_update; plan size as smallkv_plan_size).
  * smallkv_attend_tiered: smallkv_attend reading the hot pool (plan: NULL or

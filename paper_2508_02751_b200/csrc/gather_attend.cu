@@ -299,6 +299,9 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const AttendParams p
                               plan_record_bytes(NC);
   if (threadIdx.x < sizeof(GroupLayout) / 4)
     reinterpret_cast<int*>(rec)[threadIdx.x] = reinterpret_cast<const int*>(&L)[threadIdx.x];
+  // variant f4: a list longer than the hot pool was skipped by tier_update (its
+  // entry slots are stale); the header alone tells the attend to write NaN
+  if (p.entry_slot && L.T > p.hot_cap) return;
   const int32_t* bt = p.block_table + static_cast<int64_t>(b) * p.max_blocks;
   // flattened over the group's list: entry x belongs to the rank whose
   // byte-balanced share contains it and is staged if it is in that rank's
@@ -474,6 +477,18 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
     build_layout(p, p.layer, b, g, L);
   }
   const int T = L.T;
+  if (p.entry_slot && T > p.hot_cap) {
+    // variant f4 capacity overflow: tier_update skipped this group, so its
+    // entry slots are stale; nothing is read and the outputs are NaN
+    cp_async_wait<0>();
+    griddep_wait();
+    griddep_launch_dependents();
+    if (c == 0) {
+      const int64_t bo = static_cast<int64_t>(b) * p.heads + g * G;
+      for (int i = tid; i < G * D; i += kThreads) p.out[bo * D + i] = __int_as_float(0x7fc00000);
+    }
+    return;
+  }
   const int e_lo = split_begin(L, c, NC);
   const int e_hi = split_begin(L, c + 1, NC);
   (void)T;

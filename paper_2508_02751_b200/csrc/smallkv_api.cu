@@ -334,7 +334,10 @@ int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm, const smallk
     const char* e = getenv("SMALLKV_SELECT_CHUNKS");   // tuning knob
     return e ? atoi(e) : 0;
   }();
-  const int want = chunks_env > 0 ? chunks_env : (aux_stream ? 4 : 1);
+  // at most kMaxChunks chunks (the fork/join events below live in a fixed array)
+  constexpr int kMaxChunks = 8;
+  int want = chunks_env > 0 ? chunks_env : (aux_stream ? 4 : 1);
+  if (want > kMaxChunks) want = kMaxChunks;
   const int nchunk = nl < want ? nl : want;
   cudaStream_t aux = static_cast<cudaStream_t>(aux_stream);
   auto chunk_lo = [&](int i) { return (nl * i) / nchunk; };
@@ -345,7 +348,7 @@ int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm, const smallk
     return skv::launch_select(se, rows_max < n_llm_heads ? rows_max : n_llm_heads,
                               batch->max_seq_len, true, st);
   };
-  cudaEvent_t evs[9] = {};
+  cudaEvent_t evs[kMaxChunks + 1] = {};
   const int nev = aux && nchunk > 1 ? nchunk + 1 : 0;
   for (int i = 0; i < nev; ++i) {
     e = cudaEventCreateWithFlags(&evs[i], cudaEventDisableTiming);

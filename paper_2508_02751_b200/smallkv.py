@@ -17,7 +17,7 @@ from typing import Optional, Sequence
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsmallkv.so")
+LIB_PATH = os.environ.get("SMALLKV_LIB") or os.path.join(_HERE, "libsmallkv.so")
 _lock = threading.Lock()
 _lib = None
 
