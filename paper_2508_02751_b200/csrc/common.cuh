@@ -116,6 +116,12 @@ SKV_DEV void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint64_t* bar, in
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+// Bulk prefetch of [p, p + bytes) into L2 (bytes a multiple of 16); no
+// destination, no completion: a later read of the range hits L2.
+SKV_DEV void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(reinterpret_cast<uint64_t>(p)), "r"(bytes)
+               : "memory");
+}
 SKV_DEV void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }

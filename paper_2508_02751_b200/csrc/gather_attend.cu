@@ -75,10 +75,11 @@ constexpr int stages_for() { return SKV_ATTEND_STAGES; }
 template <int D>
 constexpr int stage_bytes() { return 2 * kTile * D * 2; }
 
-// [row offset][mask][weight]: kBatch each | stages (kWarps x NSTAGE)
+// [row offset][mask][weight]: kBatch each (batch buffer 0) | stages (kWarps x
+// NSTAGE) | batch buffer 1 (the next batch is staged while this one streams)
 template <int D>
 constexpr size_t smem_bytes() {
-  return static_cast<size_t>(kBatch) * 12 +
+  return 2 * static_cast<size_t>(kBatch) * 12 +
          static_cast<size_t>(kWarps) * stages_for<D>() * stage_bytes<D>();
 }
 
@@ -306,7 +307,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const AttendParams p
   // flattened over the group's list: entry x belongs to the rank whose
   // byte-balanced share contains it and is staged if it is in that rank's
   // first batch
-  __shared__ int s_split[9];
+  __shared__ int s_split[17];
   if (threadIdx.x <= NC) s_split[threadIdx.x] = split_begin(L, threadIdx.x, NC);
   __syncthreads();
   if (threadIdx.x < NC) {   // each rank's first-batch tile table
@@ -379,9 +380,15 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
   uint32_t* smk = soff + kBatch;
   float* sw = reinterpret_cast<float*>(smk + kBatch);
   uint8_t* stages = reinterpret_cast<uint8_t*>(sw + kBatch);
+  // batch buffers: x & 1 selects [row offset | mask | weight] and the tile table
+  uint32_t* soff1 = reinterpret_cast<uint32_t*>(stages + static_cast<size_t>(kWarps) * NSTAGE * SB);
   __shared__ __align__(16) GroupLayout L;
-  __shared__ __align__(16) uint32_t s_tt[kTileTableBytes / 4];   // [count][tiles]
-  const uint32_t* s_tiles = s_tt + 1;
+  __shared__ __align__(16) uint32_t s_tt[kTileTableBytes / 4];    // [count][tiles], batch buffer 0
+  __shared__ __align__(16) uint32_t s_tt1[kTileTableBytes / 4];   // batch buffer 1
+  auto BOFF = [&](int x) { return (x & 1) ? soff1 : soff; };
+  auto BMK = [&](int x) { return (x & 1) ? soff1 + kBatch : smk; };
+  auto BW = [&](int x) { return reinterpret_cast<float*>((x & 1) ? soff1 + 2 * kBatch : smk + kBatch); };
+  auto BTT = [&](int x) { return (x & 1) ? s_tt1 : s_tt; };
 
   const int c = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
   const int NC = gridDim.x;
@@ -528,91 +535,121 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
   const int mi = lane >> 3;
   const int h0 = 2 * tq, h1 = 2 * tq + 1;
 
-  int tbase = 0;   // tiles this warp consumed in earlier batches (mbarrier phases)
-  for (int e_b = e_lo; e_b < e_hi; e_b += kBatch) {
-    const int E = min(kBatch, e_hi - e_b);
-    // ---- stage this batch (pre-staged by the plan kernel for the first one)
-    if (!(rec && e_b == e_lo)) stage_entries<D>(p, L, b, g, e_b, E, soff, smk, sw);
-    SKV_T(2);
-
-    // ---- tiles of this batch (from the plan for its first batch)
-    if (!(rec && e_b == e_lo) && tid == 0) build_tile_table(L, e_b, E, p.group_sel != 0, s_tt);
+  // ---- the share's entries in batches of kBatch, double-buffered: batch x+1
+  // is staged (list values, page table -> row offsets, tile table) into the
+  // other buffer at the start of batch x, while batch x's first tiles are in
+  // flight, and each warp's cp.async ring runs on into batch x+1's first tiles
+  // during batch x's last ones (no drain at the batch boundary).
+  const int nbatch = e_hi > e_lo ? (e_hi - e_lo + kBatch - 1) / kBatch : 0;
+  auto nmy_of = [&](int x) {
+    const int nt = static_cast<int>(BTT(x)[0]);
+    return nt > warp ? (nt - warp + kWarps - 1) / kWarps : 0;
+  };
+  // batch 0: pre-staged by the plan kernel (an empty share has an empty tile
+  // table there), or staged now
+  if (!rec) {
+    if (nbatch > 0) {
+      stage_entries<D>(p, L, b, g, e_lo, min(kBatch, e_hi - e_lo), soff, smk, sw);
+      if (tid == 0) build_tile_table(L, e_lo, min(kBatch, e_hi - e_lo), p.group_sel != 0, s_tt);
+    } else if (tid == 0) {
+      s_tt[0] = 0u;
+    }
     __syncthreads();
-    const int ntile = static_cast<int>(s_tt[0]);
-    const int nmy = ntile > warp ? (ntile - warp + kWarps - 1) / kWarps : 0;
+  }
+  SKV_T(2);
 
-    // Each cp.async instruction of the warp moves 4 rows x 128 contiguous bytes:
-    // lane l copies 16-byte chunk (l & 7) of entry 4*grp + (l >> 3); rows are
-    // XOR-swizzled in 16-byte chunks so ldmatrix is conflict-free.
-    auto issue = [&](int i) {
-      if (i < nmy) {
-        uint8_t* st = wst + ((tbase + i) % NSTAGE) * SB;
-        const uint32_t td = s_tiles[warp + i * kWarps];
-        const int e0 = static_cast<int>(td & 0xffffu), cnt = static_cast<int>((td >> 16) & 0xffu);
-        if (td >> 25) {
-          // f2 marginal tile: 16 V rows in the V half, their per-head weights
-          // [16][8] fp32 (512 B) at the start of the K half
+  auto issue = [&](int x, int j, int slot) {
+    if (x >= 0) {
+      uint8_t* st = wst + (slot % NSTAGE) * SB;
+      const uint32_t* xoff = BOFF(x);
+      const int e_b = e_lo + x * kBatch;
+      const uint32_t td = BTT(x)[1 + warp + j * kWarps];
+      const int e0 = static_cast<int>(td & 0xffffu), cnt = static_cast<int>((td >> 16) & 0xffu);
+      if (td >> 25) {
+        // f2 marginal tile: 16 V rows in the V half, their per-head weights
+        // [16][8] fp32 (512 B) at the start of the K half
 #pragma unroll
-          for (int grp = 0; grp < kTile / 4; ++grp) {
-            const int eo = grp * 4 + (lane >> 3);
-            const bool ev = eo < cnt;
-            const uint32_t ro = ev ? soff[e0 + eo] : 0u;
+        for (int grp = 0; grp < kTile / 4; ++grp) {
+          const int eo = grp * 4 + (lane >> 3);
+          const bool ev = eo < cnt;
+          const uint32_t ro = ev ? xoff[e0 + eo] : 0u;
 #pragma unroll
-            for (int hf = 0; hf < D / 64; ++hf) {
-              const int ch = hf * 8 + (lane & 7);
-              cp_async16(smem_u32(st + KV_BYTES + eo * ROWB + ((ch ^ (eo & 7)) << 4)), vpool + ro + ch * 8, ev);
-            }
+          for (int hf = 0; hf < D / 64; ++hf) {
+            const int ch = hf * 8 + (lane & 7);
+            cp_async16(smem_u32(st + KV_BYTES + eo * ROWB + ((ch ^ (eo & 7)) << 4)), vpool + ro + ch * 8, ev);
           }
-          const int eo = lane >> 1;
-          const int64_t m = static_cast<int64_t>(e_b + e0 + eo) - (L.Rc + L.rK[0]);
-          const float* src = p.marg_w + ((static_cast<int64_t>(L.rj[0]) * p.batch + b) * p.max_marg + m) * 8 +
-                             (lane & 1) * 4;
-          cp_async16(smem_u32(st + lane * 16), eo < cnt ? src : p.marg_w, eo < cnt);
-        } else if (td >> 24) {
-          // V-only tile: 32 V rows fill the stage
+        }
+        const int eo = lane >> 1;
+        const int64_t m = static_cast<int64_t>(e_b + e0 + eo) - (L.Rc + L.rK[0]);
+        const float* src = p.marg_w + ((static_cast<int64_t>(L.rj[0]) * p.batch + b) * p.max_marg + m) * 8 +
+                           (lane & 1) * 4;
+        cp_async16(smem_u32(st + lane * 16), eo < cnt ? src : p.marg_w, eo < cnt);
+      } else if (td >> 24) {
+        // V-only tile: 32 V rows fill the stage
 #pragma unroll
-          for (int grp = 0; grp < 2 * kTile / 4; ++grp) {
-            const int eo = grp * 4 + (lane >> 3);
-            const bool ev = eo < cnt;
-            const uint32_t ro = ev ? soff[e0 + eo] : 0u;
+        for (int grp = 0; grp < 2 * kTile / 4; ++grp) {
+          const int eo = grp * 4 + (lane >> 3);
+          const bool ev = eo < cnt;
+          const uint32_t ro = ev ? xoff[e0 + eo] : 0u;
 #pragma unroll
-            for (int hf = 0; hf < D / 64; ++hf) {
-              const int ch = hf * 8 + (lane & 7);
-              cp_async16(smem_u32(st + eo * ROWB + ((ch ^ (eo & 7)) << 4)), vpool + ro + ch * 8, ev);
-            }
+          for (int hf = 0; hf < D / 64; ++hf) {
+            const int ch = hf * 8 + (lane & 7);
+            cp_async16(smem_u32(st + eo * ROWB + ((ch ^ (eo & 7)) << 4)), vpool + ro + ch * 8, ev);
           }
-        } else {
+        }
+      } else {
 #pragma unroll
-          for (int grp = 0; grp < kTile / 4; ++grp) {
-            const int eo = grp * 4 + (lane >> 3);
-            const bool ev = eo < cnt;
-            const uint32_t ro = ev ? soff[e0 + eo] : 0u;
+        for (int grp = 0; grp < kTile / 4; ++grp) {
+          const int eo = grp * 4 + (lane >> 3);
+          const bool ev = eo < cnt;
+          const uint32_t ro = ev ? xoff[e0 + eo] : 0u;
 #pragma unroll
-            for (int hf = 0; hf < D / 64; ++hf) {
-              const int ch = hf * 8 + (lane & 7);
-              const int sw_ = (ch ^ (eo & 7)) << 4;
-              if (ev) cp_async16(smem_u32(st + eo * ROWB + sw_), kpool + ro + ch * 8, true);
-              cp_async16(smem_u32(st + KV_BYTES + eo * ROWB + sw_), vpool + ro + ch * 8, ev);
-            }
+          for (int hf = 0; hf < D / 64; ++hf) {
+            const int ch = hf * 8 + (lane & 7);
+            const int sw_ = (ch ^ (eo & 7)) << 4;
+            if (ev) cp_async16(smem_u32(st + eo * ROWB + sw_), kpool + ro + ch * 8, true);
+            cp_async16(smem_u32(st + KV_BYTES + eo * ROWB + sw_), vpool + ro + ch * 8, ev);
           }
         }
       }
-      cp_async_commit();
-    };
+    }
+    cp_async_commit();
+  };
 
+
+  int tbase = 0;   // tiles this warp consumed in earlier batches (ring slots)
+  {
+    const int nmy0 = nbatch > 0 ? nmy_of(0) : 0;
 #pragma unroll
     for (int i = 0; i < NSTAGE - 1; ++i)
-      if (!(e_b == e_lo && i < early)) issue(i);   // the early tiles are in flight already
-    if (!q_ready) wait_and_load_q();
+      if (!(i < early)) issue(i < nmy0 ? 0 : -1, i, i);   // the early tiles are in flight already
+  }
+  if (!q_ready) wait_and_load_q();
+  for (int x = 0; x < nbatch; ++x) {
+    if (x + 1 < nbatch) {
+      // stage batch x+1 into the other buffer (its previous batch, x-1, was
+      // fully consumed before the barrier that ended it)
+      const int eb1 = e_lo + (x + 1) * kBatch, E1 = min(kBatch, e_hi - eb1);
+      stage_entries<D>(p, L, b, g, eb1, E1, BOFF(x + 1), BMK(x + 1), BW(x + 1));
+      if (tid == 0) build_tile_table(L, eb1, E1, p.group_sel != 0, BTT(x + 1));
+      __syncthreads();
+    }
+    const int nmy = nmy_of(x);
+    const int nmy_next = x + 1 < nbatch ? nmy_of(x + 1) : 0;
+    const uint32_t* cmk = BMK(x);
+    const float* cw = BW(x);
     for (int i = 0; i < nmy; ++i) {
-      issue(i + NSTAGE - 1);
+      // ring slot of the tile NSTAGE-1 ahead: this batch's, else the next batch's
+      const int ti = i + NSTAGE - 1;
+      if (ti < nmy) issue(x, ti, tbase + ti);
+      else issue(ti - nmy < nmy_next ? x + 1 : -1, ti - nmy, tbase + ti);
       cp_async_wait<NSTAGE - 1>();
       __syncwarp();
       if (i == 0) { SKV_T(3); }
       const uint8_t* st = wst + ((tbase + i) % NSTAGE) * SB;
       const uint8_t* kb = st;
       const uint8_t* vb = st + KV_BYTES;
-      const uint32_t td = s_tiles[warp + i * kWarps];
+      const uint32_t td = BTT(x)[1 + warp + i * kWarps];
       const int e0 = static_cast<int>(td & 0xffffu), cnt = static_cast<int>((td >> 16) & 0xffu);
       if (td >> 25) {
         // ---- f2 marginal tile, 16 rows: O_m^T += V^T · A'^T with per-head
@@ -648,8 +685,8 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int tok = half * 16 + (u >> 1) * 8 + 2 * tq + (u & 1);
-            const uint32_t mk = tok < cnt ? smk[e0 + tok] : 0u;
-            wm[u] = ((mk >> (8 + gq)) & 1u) ? sw[e0 + tok] : 0.f;
+            const uint32_t mk = tok < cnt ? cmk[e0 + tok] : 0u;
+            wm[u] = ((mk >> (8 + gq)) & 1u) ? cw[e0 + tok] : 0.f;
           }
           uint32_t bh0_, bl0_, bh1_, bl1_;
           split_bf16x2(wm[0], wm[1], bh0_, bl0_);
@@ -682,8 +719,8 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
       float s4[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) s4[u] = (sc[0][u] + sc[1][u]) + (sc[2][u] + sc[3][u]);
-      const uint32_t mkA = gq < cnt ? smk[e0 + gq] : 0u;
-      const uint32_t mkB = gq + 8 < cnt ? smk[e0 + gq + 8] : 0u;
+      const uint32_t mkA = gq < cnt ? cmk[e0 + gq] : 0u;
+      const uint32_t mkB = gq + 8 < cnt ? cmk[e0 + gq + 8] : 0u;
       const float sv0 = ((mkA >> h0) & 1u) ? s4[0] * p.scale_log2 : -INFINITY;   // tok gq,   head h0
       const float sv1 = ((mkA >> h1) & 1u) ? s4[1] * p.scale_log2 : -INFINITY;   // tok gq,   head h1
       const float sv2 = ((mkB >> h0) & 1u) ? s4[2] * p.scale_log2 : -INFINITY;   // tok gq+8, head h0
@@ -742,10 +779,11 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
       }
       __syncwarp();
     }
-    cp_async_wait<0>();
     tbase += nmy;
-    __syncthreads();   // batch arrays and stages are free again
+    __syncthreads();   // batch x's buffer is free for batch x+2
   }
+  cp_async_wait<0>();
+  __syncthreads();   // the stages are free for the merge
   if (!q_ready) wait_and_load_q();   // empty share: still order the output writes
 #pragma unroll
   for (int sh = 4; sh < 32; sh <<= 1) {
@@ -1045,15 +1083,46 @@ extern "C" int skv_debug_set_trace(long long* buf) {
 }
 #endif
 
-// CTAs per (sequence, kv-group) = cluster size: as many as fill the GPU with
-// one 8-warp CTA per SM in a single wave, i.e. floor(#SMs / #groups), 1..8.
-// (Config 2: 128 groups -> 1; config 4 at one GPU: 64 groups -> 2.)
+// Largest cluster the GPU co-schedules `want` of at once (one attend CTA per SM),
+// from the occupancy calculator; clusters above 8 CTAs are non-portable.
+static int32_t clusters_fit(int nc) {
+  static int cache[17] = {0};
+  if (cache[nc]) return cache[nc] > 0 ? cache[nc] : 0;
+  auto kern = attend_kernel<128>;
+  const size_t sm = smem_bytes<128>();
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+  if (nc > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nc, 1, 1);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = sm;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = nc;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    n = nc <= 8 ? 148 / nc : 0;
+  }
+  cache[nc] = n > 0 ? n : -1;
+  return n;
+}
+
+// CTAs per (sequence, kv-group) = cluster size: the largest NC <= 16 with
+// NC * groups <= #SMs whose clusters the GPU co-schedules in a single wave
+// (one 8-warp CTA per SM), so a layer fills the GPU without a second wave.
+// (Config 2: 128 groups -> 1; config 4 at one GPU: 64 groups -> 2; at one
+// sequence per GPU: 8 groups -> up to 16.)
 int32_t attend_ctas_per_group(int32_t batch, int32_t kv_heads) {
   static const int32_t forced = [] {
     const char* e = getenv("SMALLKV_ATTEND_CTAS");   // tuning knob
     return e ? atoi(e) : 0;
   }();
-  if (forced > 0) return forced > 8 ? 8 : forced;
+  if (forced > 0) return forced > 16 ? 16 : forced;
   static const int32_t sms = [] {
     int dev = 0, n = 0;
     if (cudaGetDevice(&dev) != cudaSuccess ||
@@ -1064,8 +1133,11 @@ int32_t attend_ctas_per_group(int32_t batch, int32_t kv_heads) {
     return n;
   }();
   const int64_t groups = static_cast<int64_t>(batch) * kv_heads;
-  const int64_t nc = groups > 0 ? sms / groups : 1;
-  return nc < 1 ? 1 : (nc > 8 ? 8 : static_cast<int32_t>(nc));
+  int64_t nc = groups > 0 ? sms / groups : 1;
+  if (nc > 16) nc = 16;
+  for (; nc > 1; --nc)
+    if (static_cast<int64_t>(clusters_fit(static_cast<int>(nc))) >= groups) break;
+  return nc < 1 ? 1 : static_cast<int32_t>(nc);
 }
 
 template <int D>
@@ -1074,6 +1146,10 @@ static cudaError_t launch_d(const AttendParams& p, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(attend_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(sm));
   if (e != cudaSuccess) return e;
+  if (p.max_chunks > 8) {
+    e = cudaFuncSetAttribute(attend_kernel<D>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
   e = cudaFuncSetAttribute(attend_kernel<D>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};

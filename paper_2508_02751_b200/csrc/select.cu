@@ -36,6 +36,7 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include "select_long.cuh"
 #include "select_row.cuh"
 
 namespace skv {
@@ -52,12 +53,15 @@ constexpr int kSmemCap = 8192;   // rows staged in shared memory (40 KB); longer
 // before reading anything (and an attend launched right after select runs
 // without its overlap flag, include/smallkv.h)
 template <bool kInSmem, bool kLogBins, int kRegE>
-__global__ void __launch_bounds__(kThreads, kRegE > 0 ? SKV_SELECT_REG_MINB : 5) select_kernel(const SelectParams p) {
+__global__ void __launch_bounds__(kThreads, kRegE > 0 ? SKV_SELECT_REG_MINB : (kInSmem ? 5 : 4)) select_kernel(const SelectParams p) {
   griddep_launch_dependents();
   griddep_wait();
   const int r = p.layer_off[p.layer_begin] + static_cast<int>(blockIdx.y);
   if (r >= p.layer_off[p.layer_end]) return;
-  select_row<kInSmem, kLogBins, kRegE>(p, p.rows[r], blockIdx.x);
+  if constexpr (!kInSmem && kRegE == 0)
+    select_row_long<kLogBins>(p, p.rows[r], blockIdx.x);   // rows longer than kSmemCap
+  else
+    select_row<kInSmem, kLogBins, kRegE>(p, p.rows[r], blockIdx.x);
 }
 
 // ---------------------------------------------------------------------------

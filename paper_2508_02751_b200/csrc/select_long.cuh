@@ -1,0 +1,549 @@
+// select_long.cuh — K2's split of LONG rows (n > kSmemCap, e.g. 32K / 128K
+// contexts): one 256-thread CTA per (SLM row, sequence), the row read from
+// global memory (L2 / HBM) in every pass with 8 independent 16-byte loads in
+// flight per thread (32 KB per CTA), so the ~3 passes over a 512 KB row run
+// at memory speed instead of at the latency of 2 loads per thread.
+//
+// Same result as select_row (select_row.cuh; Eq. 4, Eq. 6
+// P:141-152, R1-R5, R10; variant f1's running sums, Eq. 1; variant
+// f2's log-coordinate bins, R16): exact lexicographic thresholds (T, I) on
+// (order-preserving key, index) per rank boundary, ascending lists, marg_w =
+// a' of the current step.
+//   1. (max, Σexp) from K1's chunk statistics -> lse'; ranked range [lo, hi]
+//      (f1: acc += a' first, range of the updated sums);
+//   2. one CTA-wide histogram of 2048 bins linear in the score (monotone) —
+//      at 128K tokens a boundary bin holds ~200 positions, so the sub-bin
+//      level of select_row is rarely needed; a boundary bin with more than
+//      kCap positions is refined with 2048 sub-bins, and a still-overfull one
+//      (massive exact ties) takes the exact 4-pass 8-bit radix select;
+//   3. one pass collects the boundary bins' (key, index) pairs and counts,
+//      per warp segment, the positions above them (the output offsets), the
+//      pair of exact rank is the threshold;
+//   4. one pass writes both ascending lists per warp segment.
+#pragma once
+
+#include <float.h>
+#include <math.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace skv {
+namespace {
+
+constexpr int kLongThreads = 256;
+constexpr int kLongWarps = kLongThreads / 32;
+constexpr int kLongBins = 2048;
+constexpr int kLongCap = 1024;
+constexpr int kLongU = 4;   // 16-byte loads in flight per thread and pass
+
+__device__ __forceinline__ int lclamp(int x, int lo, int hi) { return x < lo ? lo : (x > hi ? hi : x); }
+
+template <bool kLogBins>
+__device__ __forceinline__ void select_row_long(const SelectParams& p, const int j, const int b) {
+  __shared__ uint32_t hist[kLongBins];
+  __shared__ unsigned long long cand[2][kLongCap];
+  __shared__ float red[4][kLongWarps];
+  __shared__ int wab[kLongWarps][2];
+  __shared__ int wsel[kLongWarps][2];
+  __shared__ int s_i[16];            // [0,1] cell count, [2,3] bin, [4,5] above, [6,7] cand count
+  __shared__ uint32_t s_u[4];        // [0,1] radix prefix, [2,3] threshold key
+  __shared__ int s_ti[2], s_fb[2], s_rem[2];
+
+  const int n = p.seq_lens[b];
+  const int64_t rb = static_cast<int64_t>(j) * p.batch + b;
+  const float* row = p.logits + rb * p.row_stride;
+  const int Rc = lclamp(p.n_recent[b], 0, n);
+  const int Kc = min(lclamp(p.k_crit[b], 0, n - Rc), p.max_crit);
+  const int Mc = min(lclamp(p.k_marg[b], 0, n - Rc - Kc), p.max_marg);
+  const int N = n - Rc;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  float* accrow = p.acc ? p.acc + rb * p.row_stride : nullptr;
+  const float* score = accrow ? accrow : row;
+  const bool al = (p.row_stride & 3) == 0;
+  // kLongU float4 loads of positions base + stride*u (+0..3): unguarded when the
+  // last one is fully inside [0, lim)
+  auto loadU = [&](const float* src, int base, int stride, int lim, float4 (&v)[kLongU]) {
+    if (al && base + stride * (kLongU - 1) + 3 < lim) {
+#pragma unroll
+      for (int u = 0; u < kLongU; ++u) v[u] = __ldcg(reinterpret_cast<const float4*>(src + base + stride * u));
+    } else {
+#pragma unroll
+      for (int u = 0; u < kLongU; ++u) {
+        const int i = base + stride * u;
+        v[u].x = i < lim ? src[i] : 0.f;
+        v[u].y = i + 1 < lim ? src[i + 1] : 0.f;
+        v[u].z = i + 2 < lim ? src[i + 2] : 0.f;
+        v[u].w = i + 3 < lim ? src[i + 3] : 0.f;
+      }
+    }
+  };
+  // positions i..i+3 (i a multiple of 4, i < lim); lanes past lim read zeros
+  auto load4 = [&](const float* src, int i, int lim) -> float4 {
+    if (i >= lim) return make_float4(0.f, 0.f, 0.f, 0.f);
+    if (al && i + 3 < lim) return __ldcg(reinterpret_cast<const float4*>(src + i));
+    float4 v;
+    v.x = src[i];
+    v.y = i + 1 < lim ? src[i + 1] : 0.f;
+    v.z = i + 2 < lim ? src[i + 2] : 0.f;
+    v.w = i + 3 < lim ? src[i + 3] : 0.f;
+    return v;
+  };
+
+  // ---- 1. statistics: (max, Σexp) over [0, n) and the ranked range from K1's chunks
+  if (warp == 0) {
+    const int nch = (n + p.chunk_tokens - 1) / p.chunk_tokens;
+    const float4* st = p.stats + rb * p.n_chunks;
+    float m2 = -FLT_MAX, s2 = 0.f, l2 = FLT_MAX, h2 = -FLT_MAX;
+    for (int c = lane; c < nch; c += 32) {
+      const float4 v = st[c];
+      const float mm = fmaxf(m2, v.x);
+      s2 = s2 * __expf(m2 - mm) + v.y * __expf(v.x - mm);
+      m2 = mm;
+      l2 = fminf(l2, v.z);
+      h2 = fmaxf(h2, v.w);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float mo = __shfl_xor_sync(0xffffffffu, m2, o), so = __shfl_xor_sync(0xffffffffu, s2, o);
+      const float mm = fmaxf(m2, mo);
+      s2 = s2 * __expf(m2 - mm) + so * __expf(mo - mm);
+      m2 = mm;
+      l2 = fminf(l2, __shfl_xor_sync(0xffffffffu, l2, o));
+      h2 = fmaxf(h2, __shfl_xor_sync(0xffffffffu, h2, o));
+    }
+    if (lane == 0) {
+      red[0][0] = m2;
+      red[1][0] = s2;
+      red[2][0] = l2;
+      red[3][0] = h2;
+      p.lse[rb * 2] = m2;
+      p.lse[rb * 2 + 1] = m2 + logf(s2);
+      p.counts[rb * 2] = Kc;
+      p.counts[rb * 2 + 1] = Mc;
+    }
+  }
+  __syncthreads();
+  const float lse = red[0][0] + logf(red[1][0]);
+  float vlo = red[2][0], vhi = red[3][0];
+  if (accrow) {
+    // f1: acc[v] += a'_v for v < n (in place), rank on acc; range over [0, N)
+    float lo = FLT_MAX, hi = -FLT_MAX;
+    for (int base = 4 * tid; base < n; base += 4 * kLongThreads * kLongU) {
+      float4 a[kLongU], s[kLongU];
+#pragma unroll
+      for (int u = 0; u < kLongU; ++u) {
+        a[u] = load4(accrow, base + 4 * kLongThreads * u, n);
+        s[u] = load4(row, base + 4 * kLongThreads * u, n);
+      }
+#pragma unroll
+      for (int u = 0; u < kLongU; ++u) {
+        const int i = base + 4 * kLongThreads * u;
+        float av[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
+        const float sv[4] = {s[u].x, s[u].y, s[u].z, s[u].w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (i + k >= n) continue;
+          av[k] += __expf(sv[k] - lse);
+          accrow[i + k] = av[k];
+          if (i + k < N) {
+            lo = fminf(lo, av[k]);
+            hi = fmaxf(hi, av[k]);
+          }
+        }
+      }
+    }
+    lo = -warp_max(-lo);
+    hi = warp_max(hi);
+    __syncthreads();
+    if (lane == 0) {
+      red[2][warp] = lo;
+      red[3][warp] = hi;
+    }
+    __syncthreads();
+    vlo = FLT_MAX;
+    vhi = -FLT_MAX;
+    for (int w = 0; w < kLongWarps; ++w) {
+      vlo = fminf(vlo, red[2][w]);
+      vhi = fmaxf(vhi, red[3][w]);
+    }
+    __threadfence_block();
+  }
+  const int rA = Kc, rB = Kc + Mc;
+  if (rB == 0) return;
+
+  // per-warp contiguous segments of [0, N) (index order = output order),
+  // multiples of 128 positions (4 consecutive per lane per step)
+  const int seg = ((N + kLongWarps * 128 - 1) / (kLongWarps * 128)) * 128;
+  const int s0 = min(N, warp * seg), s1 = min(N, s0 + seg);
+
+  auto bv = [&](float v) {
+    return kLogBins ? static_cast<float>(__float_as_uint(fmaxf(v, 1e-30f))) : v;
+  };
+  const float blo = bv(vlo);
+  const float scale1 = (static_cast<float>(kLongBins) - 0.01f) / (bv(vhi) - blo);
+  const bool all_equal = !(vhi > vlo);
+  const bool bad_range = !all_equal && !isfinite(scale1);
+  constexpr float kTop = static_cast<float>(kLongBins) - 0.5f;
+  auto bin1 = [&](float v) { return static_cast<int>(fminf(fmaxf((bv(v) - blo) * scale1, 0.f), kTop)); };
+  // level-2 sub-bins inside boundary bin B of target t
+  float lo2[2] = {0.f, 0.f}, sc2[2] = {0.f, 0.f};
+  int b1[2] = {-1, -1}, b2[2] = {-1, -1};
+  bool lv2[2] = {false, false};
+  auto bin2 = [&](float v, int t) {
+    return static_cast<int>(fminf(fmaxf((bv(v) - lo2[t]) * sc2[t], 0.f), kTop));
+  };
+  // target t's cell: -1 below (worse), 0 inside, +1 above (better)
+  auto where = [&](float v, int t) -> int {
+    const int x = bin1(v);
+    if (x != b1[t]) return x > b1[t] ? 1 : -1;
+    if (!lv2[t]) return 0;
+    const int y = bin2(v, t);
+    return y == b2[t] ? 0 : (y > b2[t] ? 1 : -1);
+  };
+  int above_g[2] = {0, 0};
+  bool fallback = bad_range;
+  uint32_t TK[2] = {0u, 0u};
+  int TI[2] = {-1, -1};
+
+  // histogram of the positions in [0, N) that lie in cell t_src (t_src < 0:
+  // all) under bin function `fn`, then the boundary bin of each target in
+  // `tmask` from the top: s_i[t] count in the bin, s_i[2+t] bin, s_i[4+t] above
+  auto level = [&](int t_src, auto fn, uint32_t tmask, const int* want) {
+    for (int i = tid; i < kLongBins; i += kLongThreads) hist[i] = 0u;
+    __syncthreads();
+    const int bsrc = t_src >= 0 ? b1[t_src] : -1;
+    for (int base = 4 * tid; base < N; base += 4 * kLongThreads * kLongU) {
+      float4 v4[kLongU];
+      loadU(score, base, 4 * kLongThreads, N, v4);
+#pragma unroll
+      for (int u = 0; u < kLongU; ++u) {
+        const int i = base + 4 * kLongThreads * u;
+        const float vv[4] = {v4[u].x, v4[u].y, v4[u].z, v4[u].w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          // level 2: only positions inside the level-1 boundary bin
+          const bool take = i + k < N && (bsrc < 0 || bin1(vv[k]) == bsrc);
+          if (take) atomicAdd(&hist[fn(vv[k])], 1u);
+        }
+      }
+    }
+    __syncthreads();
+    if (warp < 2 && ((tmask >> warp) & 1u)) {
+      const int t = warp, rr = want[t];
+      constexpr int PER = kLongBins / 32;
+      int tot = 0;
+      for (int q = 0; q < PER; ++q) tot += static_cast<int>(hist[kLongBins - 1 - (lane * PER + q)]);
+      int incl = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int ab = incl - tot;
+      if (ab < rr && rr <= incl) {
+        for (int q = 0; q < PER; ++q) {
+          const int bi = kLongBins - 1 - (lane * PER + q);
+          const int c = static_cast<int>(hist[bi]);
+          if (ab < rr && rr <= ab + c) {
+            s_i[t] = c;
+            s_i[2 + t] = bi;
+            s_i[4 + t] = ab;
+          }
+          ab += c;
+        }
+      }
+    }
+    __syncthreads();
+  };
+
+  if (!all_equal && !fallback) {
+    const int want1[2] = {rA, rB};
+    level(-1, bin1, rA > 0 ? 3u : 2u, want1);
+    int cnt[2] = {0, 0};
+    for (int t = 0; t < 2; ++t) {
+      if (t == 0 && rA == 0) continue;
+      b1[t] = s_i[2 + t];
+      above_g[t] = s_i[4 + t];
+      cnt[t] = s_i[t];
+    }
+    __syncthreads();
+    for (int t = 0; t < 2; ++t) {
+      if ((t == 0 && rA == 0) || cnt[t] <= kLongCap) continue;
+      // level 2: sub-bins linear inside the boundary bin (outlier-stretched ranges)
+      lv2[t] = true;
+      lo2[t] = blo + static_cast<float>(b1[t]) / scale1;
+      sc2[t] = scale1 * static_cast<float>(kLongBins);
+      const int want2[2] = {rA - above_g[0], rB - above_g[1]};
+      const int tt = t;
+      level(t, [&](float v) { return bin2(v, tt); }, 1u << t, want2);
+      b2[t] = s_i[2 + t];
+      above_g[t] += s_i[4 + t];
+      cnt[t] = s_i[t];
+      __syncthreads();
+      if (cnt[t] > kLongCap) fallback = true;
+    }
+  }
+
+  if (fallback) {
+    // ---- massive exact ties: 4-pass 8-bit MSB radix select of the keys, then the tie index
+    uint32_t(*rh)[256] = reinterpret_cast<uint32_t(*)[256]>(&hist[0]);
+    uint32_t pref[2] = {0u, 0u};
+    int rem[2] = {rA, rB};
+#pragma unroll 1
+    for (int pass = 0; pass < 4; ++pass) {
+      const int shift = 24 - 8 * pass;
+      const uint32_t hmask = pass == 0 ? 0u : (0xffffffffu << (shift + 8));
+      for (int i = tid; i < 512; i += kLongThreads) rh[i >> 8][i & 255] = 0;
+      __syncthreads();
+      for (int base = warp * 32; base < N; base += kLongThreads) {
+        const int i = base + lane;
+        const bool valid = i < N;
+        const uint32_t k = valid ? desc_key(score[i]) : 0u;
+        const uint32_t dig = (k >> shift) & 255u;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const bool in = valid && (t == 1 || rA > 0) && (k & hmask) == pref[t];
+          const uint32_t grp = __match_any_sync(0xffffffffu, in ? dig : 0x100u);
+          if (in && lane == __ffs(grp) - 1) atomicAdd(&rh[t][dig], __popc(grp));
+        }
+      }
+      __syncthreads();
+      if (warp < 2 && (warp == 1 || rA > 0)) {
+        const int t = warp;
+        int c[8], tot = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          c[q] = static_cast<int>(rh[t][lane * 8 + q]);
+          tot += c[q];
+        }
+        int incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        int before = incl - tot;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (before < rem[t] && rem[t] <= before + c[q]) {
+            s_u[t] = pref[t] | (static_cast<uint32_t>(lane * 8 + q) << shift);
+            s_rem[t] = rem[t] - before;
+          }
+          before += c[q];
+        }
+      }
+      __syncthreads();
+      for (int t = 0; t < 2; ++t) {
+        if (t == 0 && rA == 0) continue;
+        pref[t] = s_u[t];
+        rem[t] = s_rem[t];
+      }
+      __syncthreads();
+    }
+    // the rem-th (1-based) position in index order whose key equals T
+    for (int t = 0; t < 2; ++t) {
+      if (t == 0 && rA == 0) continue;
+      const uint32_t T = pref[t];
+      int eq = 0;
+      for (int base = s0; base < s1; base += 32) {
+        const int i = base + lane;
+        eq += __popc(__ballot_sync(0xffffffffu, i < s1 && desc_key(score[i]) == T));
+      }
+      if (lane == 0) wab[warp][0] = eq;
+      __syncthreads();
+      int before = 0;
+      for (int w = 0; w < warp; ++w) before += wab[w][0];
+      if (before < rem[t] && rem[t] <= before + eq) {
+        for (int base = s0; base < s1; base += 32) {
+          const int i = base + lane;
+          const uint32_t bal = __ballot_sync(0xffffffffu, i < s1 && desc_key(score[i]) == T);
+          const int k = rem[t] - before;
+          if (k >= 1 && k <= __popc(bal)) {
+            if (lane == 0) {
+              uint32_t m = bal;
+              for (int q = 1; q < k; ++q) m &= m - 1;
+              s_ti[t] = base + __ffs(m) - 1;
+            }
+            break;
+          }
+          before += __popc(bal);
+        }
+      }
+      __syncthreads();
+      TK[t] = T;
+      TI[t] = s_ti[t];
+    }
+  } else if (!all_equal) {
+    // ---- candidates of the boundary cells, per-warp counts above them
+    if (tid < 2) s_i[6 + tid] = 0;
+    __syncthreads();
+    int ab[2] = {0, 0};
+    // targets' level-1 bins (rA == 0: target 0 never matches, bin above all)
+    const int c0 = rA > 0 ? b1[0] : kLongBins, c1 = b1[1];
+    const bool any2 = lv2[0] || lv2[1];
+    for (int base0 = s0; base0 < s1; base0 += 128 * kLongU) {
+      float4 v4[kLongU];
+      loadU(score, base0 + 4 * lane, 128, s1, v4);
+#pragma unroll
+      for (int u = 0; u < kLongU; ++u) {
+        const int i = base0 + 128 * u + 4 * lane;
+        const float vv[4] = {v4[u].x, v4[u].y, v4[u].z, v4[u].w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const bool valid = i + k < s1;
+          const int x = bin1(vv[k]);
+          ab[0] += (valid && x > c0) ? 1 : 0;
+          ab[1] += (valid && x > c1) ? 1 : 0;
+          if (valid && (x == c0 || x == c1)) {   // rare: a boundary bin
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+              if (x != (t == 0 ? c0 : c1)) continue;
+              int w = 0;
+              if (any2 && lv2[t]) {
+                const int y = bin2(vv[k], t);
+                w = y == b2[t] ? 0 : (y > b2[t] ? 1 : -1);
+              }
+              if (w > 0) {
+                ++ab[t];
+              } else if (w == 0) {
+                const int slot = atomicAdd(&s_i[6 + t], 1);
+                cand[t][slot] = (static_cast<unsigned long long>(desc_key(vv[k])) << 32) |
+                                static_cast<uint32_t>(i + k);
+              }
+            }
+          }
+        }
+      }
+    }
+    ab[0] = warp_sum_i(ab[0]);
+    ab[1] = warp_sum_i(ab[1]);
+    if (lane == 0) {
+      wab[warp][0] = ab[0];
+      wab[warp][1] = ab[1];
+    }
+    __syncthreads();
+    // the pair of exact rank (want - 1) among a cell's candidates (all distinct)
+    for (int t = 0; t < 2; ++t) {
+      if (t == 0 && rA == 0) continue;
+      const int nc = s_i[6 + t];
+      const int want = (t == 0 ? rA : rB) - above_g[t] - 1;
+      for (int c = tid; c < nc; c += kLongThreads) {
+        const unsigned long long v = cand[t][c];
+        int rank = 0;
+        for (int d = 0; d < nc; ++d) rank += cand[t][d] < v ? 1 : 0;
+        if (rank == want) {
+          s_u[2 + t] = static_cast<uint32_t>(v >> 32);
+          s_ti[t] = static_cast<int>(v & 0xffffffffu);
+        }
+      }
+    }
+    __syncthreads();
+    for (int t = 0; t < 2; ++t) {
+      if (t == 0 && rA == 0) continue;
+      TK[t] = s_u[2 + t];
+      TI[t] = s_ti[t];
+    }
+  }
+
+  // ---- per-warp output offsets
+  int cbase = 0, mbase = 0;
+  if (all_equal) {
+    cbase = min(s0, rA);
+    mbase = min(max(s0, rA), rB) - rA;
+  } else if (fallback) {
+    // (rare) count each warp segment's selections with the exact thresholds
+    const float XA = rA > 0 ? key_to_float(TK[0]) : __int_as_float(0x7fc00000), XB = key_to_float(TK[1]);
+    int cc = 0, cb = 0;
+    for (int i = s0 + lane; i < s1; i += 32) {
+      const float v = score[i];
+      const bool isC = v > XA || (v == XA && i <= TI[0]);
+      const bool inB = v > XB || (v == XB && i <= TI[1]);
+      cc += isC ? 1 : 0;
+      cb += inB ? 1 : 0;
+    }
+    cc = warp_sum_i(cc);
+    cb = warp_sum_i(cb);
+    if (lane == 0) {
+      wab[warp][0] = cc;
+      wab[warp][1] = cb;
+      wsel[warp][0] = wsel[warp][1] = 0;
+    }
+    __syncthreads();
+    for (int w = 0; w < warp; ++w) {
+      cbase += wab[w][0];
+      mbase += wab[w][1] - wab[w][0];
+    }
+  } else {
+    if (tid < 2 * kLongWarps) (&wsel[0][0])[tid] = 0;
+    __syncthreads();
+    for (int t = 0; t < 2; ++t) {
+      if (t == 0 && rA == 0) continue;
+      const unsigned long long thr = (static_cast<unsigned long long>(TK[t]) << 32) | static_cast<uint32_t>(TI[t]);
+      const int nc = s_i[6 + t];
+      for (int c = tid; c < nc; c += kLongThreads) {
+        const unsigned long long v = cand[t][c];
+        if (v <= thr) atomicAdd(&wsel[static_cast<int>(v & 0xffffffffu) / seg][t], 1);
+      }
+    }
+    __syncthreads();
+    int ia = 0, ib = 0;
+    for (int w = 0; w < warp; ++w) {
+      ia += wab[w][0] + wsel[w][0];
+      ib += wab[w][1] + wsel[w][1];
+    }
+    cbase = rA > 0 ? ia : 0;
+    mbase = ib - cbase;
+  }
+
+  // ---- emission: this warp's segment, 128 positions per step, kLongU steps in flight
+  const float XA = rA > 0 ? (all_equal ? vlo : key_to_float(TK[0])) : __int_as_float(0x7fc00000);
+  const float XB = all_equal ? vlo : key_to_float(TK[1]);
+  const int IA = all_equal ? rA - 1 : TI[0], IB = all_equal ? rB - 1 : TI[1];
+  int32_t* crit = p.crit_idx + rb * p.max_crit;
+  int32_t* marg = p.marg_idx + rb * p.max_marg;
+  float* mw = p.marg_w + rb * p.max_marg;
+  int oc = cbase, om = mbase;
+  for (int base0 = s0; base0 < s1; base0 += 128 * kLongU) {
+    float4 v4[kLongU];
+    loadU(score, base0 + 4 * lane, 128, s1, v4);
+#pragma unroll
+    for (int u = 0; u < kLongU; ++u) {
+      const int base = base0 + 128 * u + 4 * lane;
+      const float xs[4] = {v4[u].x, v4[u].y, v4[u].z, v4[u].w};
+      uint32_t cm = 0u, mm = 0u;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int ik = base + k;
+        const bool valid = ik < s1;
+        const bool isC = valid && (xs[k] > XA || (xs[k] == XA && ik <= IA));
+        const bool inB = valid && (xs[k] > XB || (xs[k] == XB && ik <= IB));
+        cm |= static_cast<uint32_t>(isC) << k;
+        mm |= static_cast<uint32_t>(inB && !isC) << k;
+      }
+      const int own = __popc(cm) | (__popc(mm) << 16);
+      int incl = own;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int ac = oc + ((incl - own) & 0xffff), am = om + ((incl - own) >> 16);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if ((cm >> k) & 1u) crit[ac++] = base + k;
+        if ((mm >> k) & 1u) {
+          marg[am] = base + k;
+          mw[am] = __expf((accrow ? row[base + k] : xs[k]) - lse);   // a' of the current step (Eq. 6)
+          ++am;
+        }
+      }
+      const int tot = __shfl_sync(0xffffffffu, incl, 31);
+      oc += tot & 0xffff;
+      om += tot >> 16;
+    }
+  }
+}
+
+}  // namespace
+}  // namespace skv

@@ -229,3 +229,25 @@ def compare_group(p, gpu, sel, layer_slot, out_gpu=None, llm_view=None):
         rep["max_out_err"] = float(err.max())
         assert err.max() <= OUT_TOL, f"f2 output error {err.max()}"
     return rep
+
+
+def attend_split(step) -> int:
+    """CTAs per (sequence, kv-group) the attend of a DecodeStep launches (its
+    cluster size), recovered from smallkv_plan_size: L*B*H_kv records of
+    256 + NC * (8 warps x 5 tiles x 272 B) bytes (gather_attend.cu)."""
+    import ctypes
+    L = step.llm_layers
+    nb = step.lib.smallkv_plan_size(ctypes.byref(step.llm), ctypes.byref(step.batch), L)
+    per = nb // (L * step.batch.batch * step.llm.num_kv_heads)
+    return (per - 256) // (8 * 5 * 272)
+
+
+def assert_same_outputs(a, b, same_split: bool):
+    """Bitwise when both runs split the groups' lists alike; otherwise equal up
+    to the fp32 rounding of the split-merge order, row-normwise <= 1e-5
+    (DESIGN.md §5)."""
+    if same_split:
+        assert torch.equal(a, b)
+    else:
+        err = row_normwise(a.double().cpu().numpy(), b.double().cpu().numpy()).max()
+        assert err <= 1e-5, err

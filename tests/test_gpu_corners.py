@@ -1,0 +1,183 @@
+"""GPU parity corners (round 2): per-sequence budget mixes through both attend
+launch shapes, variant f1 over a long decode chain against the fp64 oracle's
+chain, and BASELINE configs[4]'s long generation teacher-forced at sampled
+decode steps.  Bars as tests/test_gpu_parity.py."""
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+import pytest
+import torch
+
+import smallkv_synth as synth
+from tests import parity
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device (run with -m 'not gpu' on CPU)")
+    from paper_2508_02751_b200 import build
+    build.build()
+    torch.cuda.set_device(0)
+
+
+def _check(p, layers=None):
+    step, out_sel, outs = parity.run_gpu_step(p, layers=layers)
+    sel = parity.oracle_select(p)
+    rep = parity.compare_select(p, out_sel, sel)
+    sg = parity.sel_from_gpu(p, out_sel, sel)
+    errs = []
+    for i, slot in enumerate(range(p.llm.num_layers) if layers is None else layers):
+        e, _ = parity.compare_attend(p, slot, outs[i], sg)
+        errs.append(e)
+        assert e <= parity.OUT_TOL, f"layer slot {slot}: row-normwise err {e}"
+    rep["max_out_err"] = max(errs)
+    return rep, out_sel, outs
+
+
+# every sequence its own (K, R, M): K' = 0, M' = 0, R' = 0, all zero, over n
+# (clamp), and ordinary budgets side by side in one launch
+MIXED = [(150, 60, 200), (0, 40, 100), (120, 0, 0), (0, 0, 0), (3000, 900, 5000),
+         (50, 30, 0), (0, 0, 333), (99, 1, 1)]
+
+
+@pytest.mark.parametrize("map_kind", ["coherent", "random"])
+def test_per_sequence_budgets_clustered_attend(map_kind):
+    """8 sequences x 2 kv-groups = 16 groups -> clusters of 8 CTAs per group:
+    the plan kernel's byte-balanced shares see empty critical / marginal runs
+    on some sequences and not on others."""
+    from paper_2508_02751_b200 import smallkv
+    cfg = synth.small_config(llm=(2, 8, 2, 128), slm=(2, 8, 2, 64), seq_len=2600, batch=8,
+                             budget=(150, 60, 200))
+    p = synth.make_problem(cfg, seed=61, page_size=16, map_kind=map_kind,
+                           seq_lens=[2600, 2000, 1500, 900, 2600, 700, 1200, 5],
+                           budgets_per_seq=MIXED).to("cuda")
+    st = smallkv.from_problem(p)
+    assert st.lib is not None
+    rep, sel, outs = _check(p)
+    cnt = sel.counts.cpu()
+    rows = np.unique(p.head_map.cpu().numpy())
+    # the budgets really differ per sequence (K' = 0 and M' = 0 both occur)
+    assert (cnt[rows, 1, 0] == 0).all() and (cnt[rows, 2, 1] == 0).all()
+    assert (cnt[rows, 3] == 0).all()
+    print(map_kind, rep)
+
+
+def test_per_sequence_budgets_single_cta_attend():
+    """38 sequences x 4 kv-groups = 152 groups >= 148 SMs -> one CTA per group,
+    with per-sequence budget mixes (the 8 patterns repeated)."""
+    cfg = synth.small_config(llm=(1, 16, 4, 128), slm=(1, 8, 2, 64), seq_len=1300, batch=38,
+                             budget=(150, 60, 200))
+    B = 38
+    seqs = [1300 - 29 * i for i in range(B)]
+    buds = [MIXED[i % len(MIXED)] for i in range(B)]
+    p = synth.make_problem(cfg, seed=62, page_size=64, map_kind="random", seq_lens=seqs,
+                           budgets_per_seq=buds).to("cuda")
+    rep, _, _ = _check(p)
+    print("single-CTA groups", rep)
+
+
+def test_f1_long_chain_qwen14b_dims():
+    """Variant f1 (Eq. 1 running sums) over 1024 decode steps at
+    BASELINE configs[4]'s SLM dims (Qwen2.5-1.5B: 12 q / 2 kv heads, d = 128),
+    context growing from 8193 by one token per step with the per-step tau
+    budgets: the GPU's fp32 running sums track the fp64 oracle chain,
+    and at sampled steps the sets agree outside the A18 band (relative 1e-6
+    of the boundary sum) with every actual flip within fp32 rounding of it."""
+    import oracle
+    from paper_2508_02751_b200 import smallkv
+    base = synth.CONFIGS["qwen14b"]
+    steps = 1024
+    n0 = 8193
+    n_max = n0 + steps - 1
+    cfg = dataclasses.replace(base, llm=synth.ModelDims(1, 40, 8, 128),
+                              slm=synth.ModelDims(1, 12, 2, 128), seq_len=n_max, batch=1,
+                              budget=(n_max // 10, n_max // 20, n_max // 10))
+    p = synth.make_problem(cfg, seed=71, device="cuda", seq_lens=[n_max])
+    step = smallkv.from_problem(p)
+    acc = torch.zeros_like(step.out.logits)
+    pc = p.to("cpu")
+    slm_view, _ = parity.views(pc)
+    rows = oracle.image_rows(pc.head_map)
+    oacc = np.zeros((len(rows), 1, p.max_seq_len), np.float64)
+    checks = {0, 1, 255, 511, 767, steps - 1}
+    worst = {"acc_rel": 0.0, "flips": 0, "exempt": 0}
+    for t in range(steps):
+        n = n0 + t
+        bud = (n // 10, n // 20, n // 10)
+        p.seq_lens.fill_(n)
+        p.k_crit.fill_(bud[0])
+        p.n_recent.fill_(bud[1])
+        p.k_marg.fill_(bud[2])
+        sel_gpu = step.select(p.slm_q, acc=acc, plan=False)
+        sl = torch.tensor([n], dtype=torch.int32)
+        kc, nr, km = (torch.tensor([x], dtype=torch.int32) for x in bud)
+        sel = oracle.select_acc(pc.slm_q, slm_view, sl, rows, kc, nr, km, p.max_crit,
+                                p.max_marg, p.max_seq_len, oacc)
+        if t in checks:
+            torch.cuda.synchronize()
+            ga = acc.cpu().double().numpy()[rows][:, 0, :n]
+            rel = np.abs(ga - oacc[:, 0, :n]) / np.maximum(np.abs(oacc[:, 0, :n]), 1e-30)
+            worst["acc_rel"] = max(worst["acc_rel"], float(rel.max()))
+            assert rel.max() <= 5e-5, (t, rel.max())
+            pcs = dataclasses.replace(pc, seq_lens=sl, k_crit=kc, n_recent=nr, k_marg=km)
+            rep = parity.compare_select(pcs, sel_gpu, sel, rank_score=oacc)
+            worst["flips"] += rep["flips"]
+            worst["exempt"] += rep["exempt_tokens"]
+    print("f1 chain", steps, "steps:", worst)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("t", [0, 1, 1023, 4095, 8191])
+def test_qwen14b_teacher_forced_decode_steps(t):
+    """BASELINE configs[4] long generation (8K prompt + 8K decode, per-step
+    reselection, Alg. 1 decode loop P:196-209), teacher-forced: the pools hold
+    the final 16384-token context and decode step t sees n = 8193 + t tokens
+    with the tau = 0.2 budgets at that n; every SLM layer is scored, sampled
+    rows / sequences are checked against the oracle, and the outputs of the
+    first and last LLM layer for the sampled sequences."""
+    base = synth.CONFIGS["qwen14b"]
+    cfg = dataclasses.replace(base, seq_len=16384, batch=4)
+    n = 8193 + t
+    bud = (n // 10, n // 20, n // 10)
+    key = ("p",)
+    cache = test_qwen14b_teacher_forced_decode_steps.__dict__.setdefault("cache", {})
+    if key not in cache:
+        cache.clear()
+        cache[key] = synth.make_problem(cfg, seed=81, device="cuda", llm_layers=[0, 47],
+                                        budget=(16384 // 10, 16384 // 20, 16384 // 10))
+    p = cache[key]
+    p.seq_lens.fill_(n)
+    p.k_crit.fill_(bud[0])
+    p.n_recent.fill_(bud[1])
+    p.k_marg.fill_(bud[2])
+    step, sel_gpu, outs = parity.run_gpu_step(p)
+    sb = [0, 3]
+    sub = dataclasses.replace(
+        p, seq_lens=p.seq_lens[sb].contiguous(), slm_q=p.slm_q[:, sb].contiguous(),
+        llm_q=p.llm_q[:, sb].contiguous(),
+        slm=dataclasses.replace(p.slm, block_table=p.slm.block_table[sb].contiguous()),
+        llm=dataclasses.replace(p.llm, block_table=p.llm.block_table[sb].contiguous()),
+        k_crit=p.k_crit[sb].contiguous(), n_recent=p.n_recent[sb].contiguous(),
+        k_marg=p.k_marg[sb].contiguous()).to("cpu")
+
+    class _SubSel:
+        pass
+    gs = _SubSel()
+    for name in ("logits", "lse", "crit", "marg", "marg_w", "counts"):
+        setattr(gs, name, getattr(sel_gpu, name)[:, sb])
+    H = cfg.llm.q_heads
+    used = np.unique(np.concatenate(
+        [sub.head_map.numpy()[l * H:(l + 1) * H] for l in (0, 47)])).astype(np.int32)
+    slm_view, llm_view = parity.views(sub)
+    sel_used = parity.oracle_select(sub, rows=used, slm_view=slm_view)
+    rep = parity.compare_select(sub, gs, sel_used)
+    sg = parity.sel_from_gpu(sub, gs, sel_used)
+    for slot in range(2):
+        e, _ = parity.compare_attend(sub, slot, outs[slot][sb].cpu(), sg, llm_view=llm_view)
+        assert e <= parity.OUT_TOL
+    print("qwen14b decode step", t, "n", n, rep)
