@@ -172,6 +172,9 @@ size_t smallkv_select_workspace_size(const smallkv_cache* slm,
  *               chunks on `stream` while the split of each finished chunk runs
  *               on aux_stream (Alg. 1 l.8-9 "in parallel"); `stream`
  *               waits for the last split before returning work to the caller.
+ *               A chunk holds as many SLM layers as keep its score rows
+ *               (H_s * B * max_seq_len * 4 bytes per layer) within 48 MB, at
+ *               least one, so the split re-reads them from L2 (long contexts).
  *               Both streams must be on the current device; capturable.
  * Errors: NULL pointers, H_s % H_kv_s != 0, head_dim not in {64,128},
  * page_size not a power of two in [1,256], misaligned pointers, small ws,

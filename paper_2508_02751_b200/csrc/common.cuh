@@ -175,6 +175,33 @@ SKV_DEV float4 ld_dsmem_f32x4(uint32_t local, uint32_t rank) {
   return v;
 }
 
+SKV_DEV uint32_t dsmem_addr(uint32_t local, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(local), "r"(rank));
+  return remote;
+}
+SKV_DEV uint32_t ld_dsmem_u32(uint32_t local, uint32_t rank) {
+  uint32_t v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];\n" : "=r"(v) : "r"(dsmem_addr(local, rank)) : "memory");
+  return v;
+}
+SKV_DEV uint4 ld_dsmem_u32x4(uint32_t local, uint32_t rank) {
+  uint4 v;
+  asm volatile("ld.shared::cluster.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(dsmem_addr(local, rank))
+               : "memory");
+  return v;
+}
+SKV_DEV unsigned long long ld_dsmem_u64(uint32_t local, uint32_t rank) {
+  unsigned long long v;
+  asm volatile("ld.shared::cluster.u64 %0, [%1];\n" : "=l"(v) : "r"(dsmem_addr(local, rank)) : "memory");
+  return v;
+}
+SKV_DEV void st_dsmem_u64(uint32_t local, uint32_t rank, unsigned long long v) {
+  asm volatile("st.shared::cluster.u64 [%0], %1;\n" ::"r"(dsmem_addr(local, rank)), "l"(v) : "memory");
+}
+
 SKV_DEV float warp_max(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));

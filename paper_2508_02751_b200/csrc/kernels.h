@@ -29,10 +29,11 @@ struct SlmScoreParams {
 cudaError_t launch_slm_score(const SlmScoreParams& p, const CUtensorMap& map, int max_seq_len,
                              cudaStream_t s);
 
-// row flags + compact list of the head map's image
+// row flags + compact list of the head map's image (+ zeroes the long split's to-do count)
 cudaError_t launch_row_flags(const int32_t* head_map, int32_t n_llm_heads, int32_t n_slm_heads,
                              int32_t heads_per_layer, uint8_t* row_needed, int32_t* rows,
-                             int32_t* n_rows, int32_t* layer_off, cudaStream_t s);
+                             int32_t* n_rows, int32_t* layer_off, int32_t* todo_count,
+                             cudaStream_t s);
 
 // ---------------------------------------------------------------- K2 select
 struct SelectParams {
@@ -52,9 +53,17 @@ struct SelectParams {
   int32_t n_chunks, chunk_tokens;
   int32_t batch, row_stride, max_crit, max_marg;
   int32_t log_bins;           // histogram on log(score) (variant f2's group scores)
+  int32_t* todo;              // rows (row * B + b) the cluster split hands to the single-CTA split
+  int32_t* todo_count;        // zeroed by row_flags at the start of each select call
 };
 cudaError_t launch_select(const SelectParams& p, int32_t max_rows, int32_t max_seq_len,
                           bool overlap_previous, cudaStream_t s);
+// long rows with few (row, sequence) pairs: one thread-block cluster of
+// `cluster` CTAs (2, 4, 8 or 16) per pair (select_cluster.cu), then the rows it
+// handed over (usually none)
+constexpr int32_t kClusterSplitMinLen = 16384;
+cudaError_t launch_select_cluster(const SelectParams& p, int32_t max_rows, int32_t cluster,
+                                  cudaStream_t s);
 
 // ---------------------------------------------------------------- variant f2 (R16)
 // Group score rows F_g = Σ_{h in group} a'_{f(l,h)} (+ their ranked-range

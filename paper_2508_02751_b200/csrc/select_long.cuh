@@ -39,6 +39,91 @@ constexpr int kLongU = 4;   // 16-byte loads in flight per thread and pass
 
 __device__ __forceinline__ int lclamp(int x, int lo, int hi) { return x < lo ? lo : (x > hi ? hi : x); }
 
+// U float4 loads of positions base + stride*u (+0..3) of src: unguarded when
+// the last one is fully inside [0, lim) (and the row is 16-byte aligned)
+template <int U>
+__device__ __forceinline__ void long_loadU(const float* src, int base, int stride, int lim, bool al,
+                                           float4 (&v)[U]) {
+  if (al && base + stride * (U - 1) + 3 < lim) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = __ldcg(reinterpret_cast<const float4*>(src + base + stride * u));
+  } else {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + stride * u;
+      v[u].x = i < lim ? src[i] : 0.f;
+      v[u].y = i + 1 < lim ? src[i + 1] : 0.f;
+      v[u].z = i + 2 < lim ? src[i + 2] : 0.f;
+      v[u].w = i + 3 < lim ? src[i + 3] : 0.f;
+    }
+  }
+}
+
+// One warp writes the ascending lists of its segment [s0, s1) of the ranked
+// range: position i is critical iff (score, i) <= (XA, IA) lexicographically
+// (score > XA, or == XA and i <= IA), in the inclusive set iff <= (XB, IB),
+// marginal iff inclusive and not critical.  oc / om: the warp's first slots
+// in crit / marg.  score = the ranking value (logits, or f1's sums: then
+// `row` holds the logits, whose a' is marg_w).
+__device__ __forceinline__ void long_emit(const float* score, const float* row, int s0, int s1, int lane,
+                                          float XA, int IA, float XB, int IB, float lse, bool al,
+                                          int32_t* crit, int32_t* marg, float* mw, int oc, int om) {
+  for (int base0 = s0; base0 < s1; base0 += 128 * kLongU) {
+    float4 v4[kLongU];
+    long_loadU<kLongU>(score, base0 + 4 * lane, 128, s1, al, v4);
+#pragma unroll
+    for (int u = 0; u < kLongU; ++u) {
+      const int base = base0 + 128 * u + 4 * lane;
+      const float xs[4] = {v4[u].x, v4[u].y, v4[u].z, v4[u].w};
+      uint32_t cm = 0u, mm = 0u;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int ik = base + k;
+        const bool valid = ik < s1;
+        const bool isC = valid && (xs[k] > XA || (xs[k] == XA && ik <= IA));
+        const bool inB = valid && (xs[k] > XB || (xs[k] == XB && ik <= IB));
+        cm |= static_cast<uint32_t>(isC) << k;
+        mm |= static_cast<uint32_t>(inB && !isC) << k;
+      }
+      const int own = __popc(cm) | (__popc(mm) << 16);
+      int incl = own;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int32_t* cp = crit + oc + ((incl - own) & 0xffff);
+      int32_t* mp = marg + om + ((incl - own) >> 16);
+      float* wp = mw + om + ((incl - own) >> 16);
+      if (cm | mm) {
+        float wv[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) wv[k] = xs[k];
+        if (row)   // f1: the weight is the current step's a', not the running sum
+#pragma unroll
+          for (int k = 0; k < 4; ++k) wv[k] = (mm >> k) & 1u ? row[base + k] : 0.f;
+        // predicated stores, no per-position branches
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t cc = (cm >> k) & 1u, m = (mm >> k) & 1u;
+          const float a = __expf(wv[k] - lse);   // a' of the current step (Eq. 6)
+          if (cc) *cp = base + k;
+          if (m) {
+            *mp = base + k;
+            *wp = a;
+          }
+          cp += cc;
+          mp += m;
+          wp += m;
+        }
+      }
+      const int tot = __shfl_sync(0xffffffffu, incl, 31);
+      oc += tot & 0xffff;
+      om += tot >> 16;
+    }
+  }
+}
+
 template <bool kLogBins>
 __device__ __forceinline__ void select_row_long(const SelectParams& p, const int j, const int b) {
   __shared__ uint32_t hist[kLongBins];
@@ -213,6 +298,7 @@ __device__ __forceinline__ void select_row_long(const SelectParams& p, const int
     for (int i = tid; i < kLongBins; i += kLongThreads) hist[i] = 0u;
     __syncthreads();
     const int bsrc = t_src >= 0 ? b1[t_src] : -1;
+    const uint32_t hist_s = smem_u32(hist);
     for (int base = 4 * tid; base < N; base += 4 * kLongThreads * kLongU) {
       float4 v4[kLongU];
       loadU(score, base, 4 * kLongThreads, N, v4);
@@ -224,7 +310,9 @@ __device__ __forceinline__ void select_row_long(const SelectParams& p, const int
         for (int k = 0; k < 4; ++k) {
           // level 2: only positions inside the level-1 boundary bin
           const bool take = i + k < N && (bsrc < 0 || bin1(vv[k]) == bsrc);
-          if (take) atomicAdd(&hist[fn(vv[k])], 1u);
+          // shared-window reduction (the lambda sees `hist` through a generic
+          // reference; the explicit .shared address avoids a generic atomic)
+          if (take) asm volatile("red.shared.add.u32 [%0], 1;\n" ::"r"(hist_s + 4u * static_cast<uint32_t>(fn(vv[k]))) : "memory");
         }
       }
     }
@@ -496,53 +584,13 @@ __device__ __forceinline__ void select_row_long(const SelectParams& p, const int
     mbase = ib - cbase;
   }
 
-  // ---- emission: this warp's segment, 128 positions per step, kLongU steps in flight
+  // ---- emission: this warp's segment
   const float XA = rA > 0 ? (all_equal ? vlo : key_to_float(TK[0])) : __int_as_float(0x7fc00000);
   const float XB = all_equal ? vlo : key_to_float(TK[1]);
   const int IA = all_equal ? rA - 1 : TI[0], IB = all_equal ? rB - 1 : TI[1];
-  int32_t* crit = p.crit_idx + rb * p.max_crit;
-  int32_t* marg = p.marg_idx + rb * p.max_marg;
-  float* mw = p.marg_w + rb * p.max_marg;
-  int oc = cbase, om = mbase;
-  for (int base0 = s0; base0 < s1; base0 += 128 * kLongU) {
-    float4 v4[kLongU];
-    loadU(score, base0 + 4 * lane, 128, s1, v4);
-#pragma unroll
-    for (int u = 0; u < kLongU; ++u) {
-      const int base = base0 + 128 * u + 4 * lane;
-      const float xs[4] = {v4[u].x, v4[u].y, v4[u].z, v4[u].w};
-      uint32_t cm = 0u, mm = 0u;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int ik = base + k;
-        const bool valid = ik < s1;
-        const bool isC = valid && (xs[k] > XA || (xs[k] == XA && ik <= IA));
-        const bool inB = valid && (xs[k] > XB || (xs[k] == XB && ik <= IB));
-        cm |= static_cast<uint32_t>(isC) << k;
-        mm |= static_cast<uint32_t>(inB && !isC) << k;
-      }
-      const int own = __popc(cm) | (__popc(mm) << 16);
-      int incl = own;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      int ac = oc + ((incl - own) & 0xffff), am = om + ((incl - own) >> 16);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if ((cm >> k) & 1u) crit[ac++] = base + k;
-        if ((mm >> k) & 1u) {
-          marg[am] = base + k;
-          mw[am] = __expf((accrow ? row[base + k] : xs[k]) - lse);   // a' of the current step (Eq. 6)
-          ++am;
-        }
-      }
-      const int tot = __shfl_sync(0xffffffffu, incl, 31);
-      oc += tot & 0xffff;
-      om += tot >> 16;
-    }
-  }
+  long_emit(score, accrow ? row : nullptr, s0, s1, lane, XA, IA, XB, IB, lse, al,
+            p.crit_idx + rb * p.max_crit, p.marg_idx + rb * p.max_marg, p.marg_w + rb * p.max_marg,
+            cbase, mbase);
 }
 
 }  // namespace

@@ -224,9 +224,11 @@ slm_score_kernel(const __grid_constant__ CUtensorMap map, const SlmScoreParams p
 __global__ void row_flags_kernel(const int32_t* __restrict__ head_map, int32_t n_llm,
                                  int32_t n_slm, int32_t heads_per_layer,
                                  uint8_t* __restrict__ needed, int32_t* __restrict__ rows,
-                                 int32_t* __restrict__ n_rows, int32_t* __restrict__ layer_off) {
+                                 int32_t* __restrict__ n_rows, int32_t* __restrict__ layer_off,
+                                 int32_t* __restrict__ todo_count) {
   extern __shared__ uint8_t flags[];
   griddep_launch_dependents();   // K1 may be scheduled now; it waits for our completion
+  if (threadIdx.x == 0) *todo_count = 0;
   for (int i = threadIdx.x; i < n_slm; i += blockDim.x) flags[i] = 0;
   __syncthreads();
   for (int i = threadIdx.x; i < n_llm; i += blockDim.x) {
@@ -258,10 +260,11 @@ __global__ void row_flags_kernel(const int32_t* __restrict__ head_map, int32_t n
 
 cudaError_t launch_row_flags(const int32_t* head_map, int32_t n_llm_heads, int32_t n_slm_heads,
                              int32_t heads_per_layer, uint8_t* row_needed, int32_t* rows,
-                             int32_t* n_rows, int32_t* layer_off, cudaStream_t s) {
+                             int32_t* n_rows, int32_t* layer_off, int32_t* todo_count,
+                             cudaStream_t s) {
   row_flags_kernel<<<1, 1024, n_slm_heads, s>>>(head_map, n_llm_heads, n_slm_heads,
                                                heads_per_layer, row_needed, rows, n_rows,
-                                               layer_off);
+                                               layer_off, todo_count);
   return cudaGetLastError();
 }
 

@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "kernels.h"
 #include "smallkv.h"
@@ -110,7 +111,7 @@ int check_budgets(const smallkv_budgets* bu) {
 constexpr int kScoreChunk = 1024;   // tokens per K1 CTA = per row-statistics chunk (512/2048 measured no better)
 
 struct SelectWs {
-  size_t flags, rows, nrows, layer_off, stats, total;
+  size_t flags, rows, nrows, layer_off, todo_count, todo, stats, total;
 };
 SelectWs select_ws_layout(int32_t n_slm, int32_t n_layers, int32_t batch, int32_t max_seq_len) {
   SelectWs w;
@@ -118,7 +119,9 @@ SelectWs select_ws_layout(int32_t n_slm, int32_t n_layers, int32_t batch, int32_
   w.rows = round256(static_cast<size_t>(n_slm));
   w.nrows = w.rows + round256(static_cast<size_t>(n_slm) * 4);
   w.layer_off = w.nrows + 256;
-  w.stats = w.layer_off + round256(static_cast<size_t>(n_layers + 1) * 4);
+  w.todo_count = w.layer_off + round256(static_cast<size_t>(n_layers + 1) * 4);
+  w.todo = w.todo_count + 256;
+  w.stats = w.todo + round256(static_cast<size_t>(n_slm) * batch * 4);
   const size_t nch = (static_cast<size_t>(max_seq_len) + kScoreChunk - 1) / kScoreChunk;
   w.total = w.stats + round256(static_cast<size_t>(n_slm) * batch * nch * 16);
   return w;
@@ -128,7 +131,7 @@ SelectWs select_ws_layout(int32_t n_slm, int32_t n_layers, int32_t batch, int32_
 // (identity row list, layer offsets, one statistics chunk per row) and scratch
 // for the split's single-weight outputs (replaced by the per-head weights).
 struct GroupWs {
-  size_t rows, layer_off, gstats, lse, mw, total;
+  size_t rows, layer_off, gstats, lse, mw, todo, total;
 };
 GroupWs group_ws_layout(const smallkv_cache* slm, const smallkv_batch* b, int32_t max_marg,
                         int32_t n_llm_layers, int32_t llm_kv_heads) {
@@ -141,7 +144,8 @@ GroupWs group_ws_layout(const smallkv_cache* slm, const smallkv_batch* b, int32_
   w.gstats = w.layer_off + 256;
   w.lse = w.gstats + round256(ng * b->batch * 16);
   w.mw = w.lse + round256(ng * b->batch * 8);
-  w.total = w.mw + round256(ng * b->batch * static_cast<size_t>(max_marg) * 4);
+  w.todo = w.mw + round256(ng * b->batch * static_cast<size_t>(max_marg) * 4);
+  w.total = w.todo + round256(ng * b->batch * 4);
   return w;
 }
 
@@ -248,8 +252,9 @@ int setup_scoring(const uint16_t* slm_q, const smallkv_cache* slm, const smallkv
   int32_t* rows = reinterpret_cast<int32_t*>(wsb + L.rows);
   int32_t* nrows = reinterpret_cast<int32_t*>(wsb + L.nrows);
   int32_t* layer_off = reinterpret_cast<int32_t*>(wsb + L.layer_off);
+  int32_t* todo_count = reinterpret_cast<int32_t*>(wsb + L.todo_count);
   cudaError_t e = skv::launch_row_flags(head_map, n_llm_heads, n_slm, slm->num_q_heads, flags,
-                                        rows, nrows, layer_off, s);
+                                        rows, nrows, layer_off, todo_count, s);
   if (e != cudaSuccess) return cuda_fail(e, "row_flags launch");
 
   skv::SlmScoreParams& sp = S.sp;
@@ -292,7 +297,23 @@ int setup_scoring(const uint16_t* slm_q, const smallkv_cache* slm, const smallkv
   se.stats = sp.stats;
   se.n_chunks = sp.n_chunks;
   se.chunk_tokens = kScoreChunk;
+  se.todo_count = todo_count;
+  se.todo = reinterpret_cast<int32_t*>(wsb + L.todo);
   return SMALLKV_OK;
+}
+
+// K2 over SLM layers [se.layer_begin, se.layer_end): long rows by thread-block
+// clusters (select_cluster.cu; f1's in-place running sums stay on the
+// single-CTA split), others by one CTA per row
+cudaError_t launch_split(const skv::SelectParams& se, int32_t max_rows, int32_t max_seq_len,
+                         bool overlap_previous, cudaStream_t s) {
+  // measured on B200 (config 4, 131072 tokens): with >= 1024 (row, sequence)
+  // pairs one CTA per pair fills the GPU (B = 8: 3.13 ms vs 3.29 with clusters
+  // of 4); with fewer, clusters of 2 halve the split (B = 1: 0.58 vs 1.05 ms)
+  const int64_t pairs = static_cast<int64_t>(max_rows) * se.batch;
+  if (!se.acc && max_seq_len > skv::kClusterSplitMinLen && pairs < 1024)
+    return skv::launch_select_cluster(se, max_rows, pairs < 256 ? 4 : 2, s);
+  return skv::launch_select(se, max_rows, max_seq_len, overlap_previous, s);
 }
 }  // namespace
 
@@ -334,10 +355,16 @@ int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm, const smallk
     const char* e = getenv("SMALLKV_SELECT_CHUNKS");   // tuning knob
     return e ? atoi(e) : 0;
   }();
-  // at most kMaxChunks chunks (the fork/join events below live in a fixed array)
-  constexpr int kMaxChunks = 8;
-  int want = chunks_env > 0 ? chunks_env : (aux_stream ? 4 : 1);
-  if (want > kMaxChunks) want = kMaxChunks;
+  // With an auxiliary stream the chunks are sized so that a chunk's score rows
+  // stay L2-resident until its split reads them (kChunkRowBytes of rows per
+  // chunk, at least one SLM layer): K2 then re-reads them from L2 while K1
+  // streams the next chunk's K' from HBM.
+  constexpr size_t kChunkRowBytes = size_t(48) << 20;
+  const size_t layer_rows = static_cast<size_t>(slm->num_q_heads) * batch->batch * batch->max_seq_len * 4;
+  int per_chunk = static_cast<int>(kChunkRowBytes / (layer_rows > 0 ? layer_rows : 1));
+  if (per_chunk < 1) per_chunk = 1;
+  int want = chunks_env > 0 ? chunks_env : (aux_stream ? (nl + per_chunk - 1) / per_chunk : 1);
+  if (want < 1) want = 1;
   const int nchunk = nl < want ? nl : want;
   cudaStream_t aux = static_cast<cudaStream_t>(aux_stream);
   auto chunk_lo = [&](int i) { return (nl * i) / nchunk; };
@@ -345,11 +372,11 @@ int smallkv_select(const uint16_t* slm_q, const smallkv_cache* slm, const smallk
     se.layer_begin = chunk_lo(i);
     se.layer_end = chunk_lo(i + 1);
     const int rows_max = (se.layer_end - se.layer_begin) * slm->num_q_heads;
-    return skv::launch_select(se, rows_max < n_llm_heads ? rows_max : n_llm_heads,
-                              batch->max_seq_len, true, st);
+    return launch_split(se, rows_max < n_llm_heads ? rows_max : n_llm_heads, batch->max_seq_len,
+                        true, st);
   };
-  cudaEvent_t evs[kMaxChunks + 1] = {};
   const int nev = aux && nchunk > 1 ? nchunk + 1 : 0;
+  std::vector<cudaEvent_t> evs(static_cast<size_t>(nev), nullptr);
   for (int i = 0; i < nev; ++i) {
     e = cudaEventCreateWithFlags(&evs[i], cudaEventDisableTiming);
     if (e != cudaSuccess) {
@@ -469,8 +496,8 @@ int smallkv_select_group(const uint16_t* slm_q, const smallkv_cache* slm, const 
   se.n_chunks = 1;
   se.chunk_tokens = batch->max_seq_len;
   se.log_bins = 1;
-  if ((e = skv::launch_select(se, n_llm_layers * llm_kv_heads, batch->max_seq_len, false, s)) !=
-      cudaSuccess)
+  se.todo = reinterpret_cast<int32_t*>(wsb + W.todo);
+  if ((e = launch_split(se, n_llm_layers * llm_kv_heads, batch->max_seq_len, false, s)) != cudaSuccess)
     return cuda_fail(e, "select launch");
   if ((e = skv::launch_group_weights(gp, s)) != cudaSuccess) return cuda_fail(e, "group_weights launch");
   return SMALLKV_OK;

@@ -422,9 +422,35 @@ class TieredKV:
         return int(c[0]), int(c[1])
 
 
+# score rows per SLM layer above which smallkv_select splits on an auxiliary
+# stream in L2-sized SLM-layer chunks (include/smallkv.h, aux_stream)
+AUX_SELECT_LAYER_BYTES = 16 << 20
+
+
+def auto_overlap_select(slm_q_heads: int, batch: int, max_seq_len: int) -> bool:
+    """Long contexts: one SLM layer's score rows are too large to stay in L2
+    across the whole select (config 2: 7 MB per layer, no; config 4: 59 MB, yes)."""
+    return slm_q_heads * batch * max_seq_len * 4 > AUX_SELECT_LAYER_BYTES
+
+
+def select_chunks(slm_layers: int, slm_q_heads: int, batch: int, max_seq_len: int,
+                  aux: bool) -> int:
+    """SLM-layer chunks smallkv_select launches (mirrors smallkv_api.cu)."""
+    if not aux:
+        return 1
+    env = int(os.environ.get("SMALLKV_SELECT_CHUNKS", "0") or 0)
+    if env > 0:
+        return min(slm_layers, env)
+    per = max(1, (48 << 20) // max(1, slm_q_heads * batch * max_seq_len * 4))
+    return min(slm_layers, -(-slm_layers // per))
+
+
 def from_problem(p, use_plan: bool = True, variant: str = "default",
-                 overlap_select: bool = False) -> DecodeStep:
-    """DecodeStep for a smallkv_synth.Problem already on the GPU."""
+                 overlap_select=None) -> DecodeStep:
+    """DecodeStep for a smallkv_synth.Problem already on the GPU.  overlap_select
+    None: automatic (auto_overlap_select)."""
+    if overlap_select is None:
+        overlap_select = False
     return DecodeStep(slm_k=p.slm.k, slm_block_table=p.slm.block_table,
                       slm_q_heads=p.cfg.slm.q_heads, llm_k=p.llm.k, llm_v=p.llm.v,
                       llm_block_table=p.llm.block_table, llm_q_heads=p.cfg.llm.q_heads,
@@ -624,7 +650,8 @@ class DecodeGraph:
         # row_flags + (slm_score + select) per SLM-layer chunk (+ plan), then one
         # attend kernel per layer
         nl = self.step.slm.num_layers
-        chunks = min(4, nl) if self.step.aux_stream is not None else 1
+        chunks = select_chunks(nl, self.step.slm.num_q_heads, self.step.batch.batch,
+                               self.step.batch.max_seq_len, self.step.aux_stream is not None)
         sel = 2 * chunks if self.step.variant == "default" else 4   # f2: + group score, weights
         tier = 0 if self.tier is None else (2 if self.tier.plan_buf is not None else 1)  # f4
         return (1 + sel + tier + (1 if self.step.plan_buf is not None else 0)

@@ -181,3 +181,33 @@ def test_qwen14b_teacher_forced_decode_steps(t):
         e, _ = parity.compare_attend(sub, slot, outs[slot][sb].cpu(), sg, llm_view=llm_view)
         assert e <= parity.OUT_TOL
     print("qwen14b decode step", t, "n", n, rep)
+
+
+@pytest.mark.parametrize("n,page", [(16385, 64), (40000, 64), (70000, 64), (20000, 16)])
+def test_cluster_split_long_rows(n, page):
+    """Rows longer than 16384 tokens are split by a thread-block cluster (8
+    CTAs, 16 beyond 65536 tokens) cooperating over distributed shared memory;
+    ragged lengths put the second sequence's rows in fewer, partly empty
+    segments.  Exact sets against the oracle."""
+    cfg = synth.small_config(llm=(1, 8, 2, 128), slm=(1, 4, 1, 64), seq_len=n, batch=2,
+                             budget=(n // 10, n // 20, n // 10))
+    p = synth.make_problem(cfg, seed=63, page_size=page, seq_lens=[n, n // 3 + 7],
+                           map_kind="random").to("cuda")
+    rep, _, _ = _check(p)
+    print("cluster split", n, rep)
+
+
+def test_cluster_split_massive_ties_handover():
+    """Two distinct logit values over a 20000-token row: the boundary bins hold
+    thousands of exact ties, the cluster hands the row to the single-CTA long
+    split (exact radix select + index tie-break)."""
+    n = 20000
+    cfg = synth.small_config(llm=(1, 8, 2, 128), slm=(1, 4, 1, 64), seq_len=n, batch=1,
+                             budget=(n // 10, 20, n // 10))
+    p = synth.make_problem(cfg, seed=64, page_size=256, seq_lens=[n])
+    k = p.slm.k.clone()
+    k[:, 0::2] = p.slm.k[:, :1, :, :1]
+    k[:, 1::2] = p.slm.k[:, 1:2, :, :1]
+    p = dataclasses.replace(p, slm=dataclasses.replace(p.slm, k=k)).to("cuda")
+    rep, _, _ = _check(p)
+    print("cluster ties", rep)
