@@ -69,6 +69,7 @@ constexpr int kTile = 16;      // rows (tokens) per warp tile
 constexpr int kWarps = SKV_ATTEND_WARPS;      // one CTA per SM (8 warps x 3-stage rings = 192 KB)
 constexpr int kThreads = kWarps * 32;
 constexpr int kBatch = 1024;   // entries whose positions/pages/weights are staged at once
+constexpr int kAsyncStageMinLen = 8192;   // contexts above this stage their batches asynchronously
 
 template <int D>
 constexpr int stages_for() { return SKV_ATTEND_STAGES; }
@@ -76,10 +77,11 @@ template <int D>
 constexpr int stage_bytes() { return 2 * kTile * D * 2; }
 
 // [row offset][mask][weight]: kBatch each (batch buffer 0) | stages (kWarps x
-// NSTAGE) | batch buffer 1 (the next batch is staged while this one streams)
+// NSTAGE) | batch buffer 1 (the next batch is staged while this one streams) |
+// page-table scratch of the batch being staged
 template <int D>
 constexpr size_t smem_bytes() {
-  return 2 * static_cast<size_t>(kBatch) * 12 +
+  return 2 * static_cast<size_t>(kBatch) * 12 + static_cast<size_t>(kBatch) * 4 +
          static_cast<size_t>(kWarps) * stages_for<D>() * stage_bytes<D>();
 }
 
@@ -368,7 +370,10 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const AttendParams p
   }
 }
 
-template <int D>
+// kAsync: batch x+1 is staged asynchronously during batch x (long lists);
+// otherwise CTA-synchronously at the start of batch x (short lists rarely have
+// a second batch, and the leaner kernel keeps fewer registers live)
+template <int D, bool kAsync>
 __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const AttendParams p) {
   constexpr int NSTAGE = stages_for<D>();
   constexpr int ROWB = D * 2;                // bytes per K or V row
@@ -385,6 +390,8 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
   __shared__ __align__(16) GroupLayout L;
   __shared__ __align__(16) uint32_t s_tt[kTileTableBytes / 4];    // [count][tiles], batch buffer 0
   __shared__ __align__(16) uint32_t s_tt1[kTileTableBytes / 4];   // batch buffer 1
+  __shared__ __align__(8) uint64_t bar_staged[2];                  // batch buffer b staged
+  int32_t* spg = reinterpret_cast<int32_t*>(soff1 + 3 * kBatch);   // [kBatch] pages / slots
   auto BOFF = [&](int x) { return (x & 1) ? soff1 : soff; };
   auto BMK = [&](int x) { return (x & 1) ? soff1 + kBatch : smk; };
   auto BW = [&](int x) { return reinterpret_cast<float*>((x & 1) ? soff1 + 2 * kBatch : smk + kBatch); };
@@ -472,6 +479,11 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
       cp_async_commit();
       ++early;
     }
+  }
+  if (tid == 0) {
+    mbar_init(&bar_staged[0], kThreads);
+    mbar_init(&bar_staged[1], kThreads);
+    fence_barrier_init();
   }
   if (rec) {
     // wait for the plan group only (the oldest); the early tiles stay in flight
@@ -625,24 +637,132 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
       if (!(i < early)) issue(i < nmy0 ? 0 : -1, i, i);   // the early tiles are in flight already
   }
   if (!q_ready) wait_and_load_q();
+  // ---- asynchronous staging of batch x+1: every thread stages its entries
+  // tid + k*kThreads in three steps interleaved with its warp's batch-x tiles —
+  // A list values and weights (4-byte cp.async) + masks, B page-table entries
+  // (cp.async into spg), C row offsets (+ thread 0: the tile table) and an
+  // arrive on the buffer's mbarrier; a warp waits on it only when its ring
+  // reaches batch x+1, so no warp stops for the staging round trips.
+  const int32_t* es = p.entry_slot
+      ? p.entry_slot + ((static_cast<int64_t>(p.layer) * p.batch + b) * p.kv_heads + g) * p.hot_cap
+      : nullptr;
+  const int64_t grp_row0 = (static_cast<int64_t>(b) * p.kv_heads + g) * p.hot_cap;   // f4
+  const int32_t* btg = p.block_table + static_cast<int64_t>(b) * p.max_blocks;
+  const bool gs = p.group_sel != 0;
+  const uint32_t allc = (1u << G) - 1u;
+  int sstep = 3;   // steps of the staged batch this thread has done (3: all)
+  auto stage_step = [&](int y) {
+    const int eb = e_lo + y * kBatch, E = min(kBatch, e_hi - eb);
+    uint32_t* yoff = BOFF(y);
+    uint32_t* ymk = BMK(y);
+    float* yw = BW(y);
+    if (sstep == 0) {
+      for (int k = 0; k < kBatch / kThreads; ++k) {
+        const int i = tid + k * kThreads;
+        if (i >= E) break;
+        const int xv = eb + i;
+        if (es) cp_async4(smem_u32(spg + i), es + xv);
+        if (xv < L.Rc) {
+          yoff[i] = static_cast<uint32_t>(L.n - L.Rc + xv);
+          ymk[i] = allc;
+          yw[i] = 0.f;
+          continue;
+        }
+        int xr = xv - L.Rc, kk = 0;
+        while (kk < L.nrows - 1 && xr >= L.rK[kk] + L.rM[kk]) {
+          xr -= L.rK[kk] + L.rM[kk];
+          ++kk;
+        }
+        const int64_t rbk = static_cast<int64_t>(L.rj[kk]) * p.batch + b;
+        if (xr < L.rK[kk]) {
+          cp_async4(smem_u32(yoff + i), p.crit_idx + rbk * p.max_crit + xr);
+          ymk[i] = L.rhm[kk];
+          yw[i] = 0.f;
+        } else {
+          const int m = xr - L.rK[kk];
+          cp_async4(smem_u32(yoff + i), p.marg_idx + rbk * p.max_marg + m);
+          ymk[i] = L.rhm[kk] << 8;
+          if (!gs) cp_async4(smem_u32(yw + i), p.marg_w + rbk * p.max_marg + m);
+          else yw[i] = 0.f;
+        }
+      }
+    } else if (sstep == 1) {
+      if (!es)
+        for (int k = 0; k < kBatch / kThreads; ++k) {
+          const int i = tid + k * kThreads;
+          if (i >= E) break;
+          cp_async4(smem_u32(spg + i), btg + (static_cast<int>(yoff[i]) >> p.ps_shift));
+        }
+    } else if (sstep == 2) {
+      for (int k = 0; k < kBatch / kThreads; ++k) {
+        const int i = tid + k * kThreads;
+        if (i >= E) break;
+        const int pos = static_cast<int>(yoff[i]);
+        yoff[i] = es ? static_cast<uint32_t>((grp_row0 + spg[i]) * D)
+                     : static_cast<uint32_t>(((static_cast<int64_t>(spg[i]) * p.kv_heads + g) * p.page_size +
+                                              (pos & (p.page_size - 1))) * D);
+        // the weight arrived by this thread's cp.async, which the wait made
+        // visible to this thread only: an ordinary store publishes it with the
+        // arrive below (the other warps read it after their wait)
+        const float wv = yw[i];
+        asm volatile("st.shared.f32 [%0], %1;\n" ::"r"(smem_u32(yw + i)), "f"(wv) : "memory");
+      }
+      if (tid == 0) build_tile_table(L, eb, E, gs, BTT(y));
+      mbar_arrive(&bar_staged[y & 1]);
+    }
+    ++sstep;
+  };
   for (int x = 0; x < nbatch; ++x) {
-    if (x + 1 < nbatch) {
-      // stage batch x+1 into the other buffer (its previous batch, x-1, was
-      // fully consumed before the barrier that ended it)
+    const bool more = x + 1 < nbatch;
+    sstep = more ? 0 : 3;
+    if (more && (!kAsync || p.sync_stage == 1)) {
+      // diagnostics: the whole staging of batch x+1 now, CTA-synchronously
       const int eb1 = e_lo + (x + 1) * kBatch, E1 = min(kBatch, e_hi - eb1);
       stage_entries<D>(p, L, b, g, eb1, E1, BOFF(x + 1), BMK(x + 1), BW(x + 1));
-      if (tid == 0) build_tile_table(L, eb1, E1, p.group_sel != 0, BTT(x + 1));
-      __syncthreads();
+      if (tid == 0) build_tile_table(L, eb1, E1, gs, BTT(x + 1));
+      mbar_arrive(&bar_staged[(x + 1) & 1]);
+      sstep = 3;
     }
     const int nmy = nmy_of(x);
-    const int nmy_next = x + 1 < nbatch ? nmy_of(x + 1) : 0;
+    int nmy_next = -1;   // known once batch x+1 is staged
+    auto wait_next = [&]() {   // batch x+1's entries and tile table are in place
+      if (nmy_next >= 0) return;
+      while (sstep < 3) {   // this thread's remaining steps first (drains its copies;
+        cp_async_commit();  // wait_group covers committed groups only)
+        cp_async_wait<0>();
+        stage_step(x + 1);
+      }
+      mbar_wait(&bar_staged[(x + 1) & 1], static_cast<uint32_t>((x >> 1) & 1));
+      nmy_next = nmy_of(x + 1);
+    };
     const uint32_t* cmk = BMK(x);
     const float* cw = BW(x);
+    if (kAsync && more && p.sync_stage == 2) {
+      // diagnostics: this thread's three steps now (full waits), barrier hand-off kept
+      while (sstep < 3) {
+        cp_async_commit();
+        cp_async_wait<0>();
+        stage_step(x + 1);
+      }
+    }
     for (int i = 0; i < nmy; ++i) {
+      if (kAsync && more && i == 0 && sstep == 0) stage_step(x + 1);   // A: joins this iteration's commit group
       // ring slot of the tile NSTAGE-1 ahead: this batch's, else the next batch's
       const int ti = i + NSTAGE - 1;
-      if (ti < nmy) issue(x, ti, tbase + ti);
-      else issue(ti - nmy < nmy_next ? x + 1 : -1, ti - nmy, tbase + ti);
+      if (ti < nmy) {
+        issue(x, ti, tbase + ti);
+      } else if (more) {
+        wait_next();
+        issue(ti - nmy < nmy_next ? x + 1 : -1, ti - nmy, tbase + ti);
+      } else {
+        issue(-1, 0, tbase + ti);
+      }
+      if (kAsync && more && sstep < 3 && (i == 1 || i == 3)) {
+        // B at iteration 1, C at 3: the previous step's group (one iteration
+        // older than the ring needs) is waited for here
+        cp_async_wait<NSTAGE - 2>();
+        stage_step(x + 1);
+      }
       cp_async_wait<NSTAGE - 1>();
       __syncwarp();
       if (i == 0) { SKV_T(3); }
@@ -779,6 +899,7 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
       }
       __syncwarp();
     }
+    if (more) wait_next();   // (a warp with few tiles in batch x)
     tbase += nmy;
     __syncthreads();   // batch x's buffer is free for batch x+2
   }
@@ -1088,7 +1209,7 @@ extern "C" int skv_debug_set_trace(long long* buf) {
 static int32_t clusters_fit(int nc) {
   static int cache[17] = {0};
   if (cache[nc]) return cache[nc] > 0 ? cache[nc] : 0;
-  auto kern = attend_kernel<128>;
+  auto kern = attend_kernel<128, true>;
   const size_t sm = smem_bytes<128>();
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
   if (nc > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -1140,17 +1261,17 @@ int32_t attend_ctas_per_group(int32_t batch, int32_t kv_heads) {
   return nc < 1 ? 1 : static_cast<int32_t>(nc);
 }
 
-template <int D>
+template <int D, bool kAsync>
 static cudaError_t launch_d(const AttendParams& p, cudaStream_t s) {
   const size_t sm = smem_bytes<D>();
-  cudaError_t e = cudaFuncSetAttribute(attend_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(attend_kernel<D, kAsync>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(sm));
   if (e != cudaSuccess) return e;
   if (p.max_chunks > 8) {
-    e = cudaFuncSetAttribute(attend_kernel<D>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaFuncSetAttribute(attend_kernel<D, kAsync>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
-  e = cudaFuncSetAttribute(attend_kernel<D>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  e = cudaFuncSetAttribute(attend_kernel<D, kAsync>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.max_chunks, p.kv_heads, p.batch);
@@ -1166,7 +1287,7 @@ static cudaError_t launch_d(const AttendParams& p, cudaStream_t s) {
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, attend_kernel<D>, p);
+  return cudaLaunchKernelEx(&cfg, attend_kernel<D, kAsync>, p);
 }
 
 int64_t plan_bytes(int32_t n_layers, int32_t batch, int32_t kv_heads, int32_t max_seq_len) {
@@ -1202,7 +1323,9 @@ cudaError_t launch_tier_update(const TierParams& t, cudaStream_t s) {
 }
 
 cudaError_t launch_attend(const AttendParams& p, cudaStream_t s) {
-  cudaError_t e = p.head_dim == 64 ? launch_d<64>(p, s) : launch_d<128>(p, s);
+  const bool async = p.row_stride > kAsyncStageMinLen;
+  cudaError_t e = p.head_dim == 64 ? (async ? launch_d<64, true>(p, s) : launch_d<64, false>(p, s))
+                                   : (async ? launch_d<128, true>(p, s) : launch_d<128, false>(p, s));
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }

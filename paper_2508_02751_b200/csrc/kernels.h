@@ -122,6 +122,7 @@ struct AttendParams {
   // entry_slot[((layer*B + b)*H_kv + g)*hot_cap + e]
   const int32_t* entry_slot;  // nullptr: the paged pool
   int32_t hot_cap;
+  int32_t sync_stage;         // diagnostics: stage batch x+1 synchronously at the start of batch x
 };
 
 // variant f4: keep each group's needed rows in an HBM hot pool, fetching only

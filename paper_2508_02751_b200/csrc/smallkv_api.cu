@@ -560,6 +560,11 @@ int fill_attend_params(skv::AttendParams& ap, const smallkv_cache* llm, const sm
   ap.row_stride = batch->max_seq_len;
   ap.max_crit = budgets->max_crit;
   ap.max_marg = budgets->max_marg;
+  static const int sync_stage_env = [] {
+    const char* e = getenv("SMALLKV_ATTEND_SYNC_STAGE");   // diagnostics
+    return e ? atoi(e) : 0;
+  }();
+  ap.sync_stage = sync_stage_env;
   ap.max_chunks = skv::attend_ctas_per_group(batch->batch, llm->num_kv_heads);
   ap.scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(llm->head_dim));
   return SMALLKV_OK;

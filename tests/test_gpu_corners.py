@@ -211,3 +211,23 @@ def test_cluster_split_massive_ties_handover():
     p = dataclasses.replace(p, slm=dataclasses.replace(p.slm, k=k)).to("cuda")
     rep, _, _ = _check(p)
     print("cluster ties", rep)
+
+
+def test_attend_many_staging_batches():
+    """Long lists (n = 65536, 8 sequences x 8 kv-groups -> 2 CTAs per group,
+    ~8 staging batches of 1024 entries per CTA, the marginal ones V-only with
+    few tiles per warp): batch x+1 is staged asynchronously while batch x
+    streams; outputs against the oracle on the GPU's sets, and equal to the
+    synchronous staging path up to nothing (the same arithmetic)."""
+    n = 65536
+    cfg = synth.small_config(llm=(1, 64, 8, 128), slm=(1, 14, 2, 64), seq_len=n, batch=8,
+                             budget=(n // 10, n // 20, n // 10))
+    p = synth.make_problem(cfg, seed=65, page_size=64).to("cuda")
+    step, sel_gpu, outs = parity.run_gpu_step(p)
+    assert parity.attend_split(step) <= 2   # several batches per CTA
+    pc = p.to("cpu")
+    sel = parity.oracle_select(pc)
+    sg = parity.sel_from_gpu(pc, sel_gpu, sel)
+    e, _ = parity.compare_attend(pc, 0, outs[0].cpu(), sg)
+    assert e <= 1e-4, e
+    print("many staging batches: row-normwise err", e)
