@@ -300,9 +300,13 @@ size_t smallkv_attend_workspace_size(const smallkv_cache* llm,
  *               call from smallkv_select / smallkv_plan and from the K/V
  *               append).  The first attend after smallkv_select or
  *               smallkv_plan must therefore be called without the flag.
- *   ws          device workspace, >= smallkv_attend_workspace_size bytes (the
- *               split work is merged inside thread-block clusters; no
- *               initialisation needed).
+ *   ws          device workspace, >= smallkv_attend_workspace_size bytes,
+ *               zero-filled once by the caller (smallkv_workspace_init) and
+ *               left zeroed by every call: when a group's list is split over
+ *               more CTAs than the GPU co-schedules as one thread-block
+ *               cluster, the CTAs merge their partial states through it (a
+ *               per-group arrival counter + partial rows, merged in rank
+ *               order: deterministic); otherwise it is unused.
  *               SMALLKV_ATTEND_GROUP_SELECTION (variant f2, R16): the
  *               selection inputs are smallkv_select_group's group-indexed
  *               outputs; every head of group g attends over the group's

@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const AttendParams p
   // flattened over the group's list: entry x belongs to the rank whose
   // byte-balanced share contains it and is staged if it is in that rank's
   // first batch
-  __shared__ int s_split[17];
+  __shared__ int s_split[33];
   if (threadIdx.x <= NC) s_split[threadIdx.x] = split_begin(L, threadIdx.x, NC);
   __syncthreads();
   if (threadIdx.x < NC) {   // each rank's first-batch tile table
@@ -1041,6 +1041,47 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
 #endif
   if (NC == 1) return;
 
+  if (p.global_merge) {
+    // ---- K4 without a cluster: every rank stores its state, the last rank of
+    // the group to arrive merges all of them in rank order (deterministic)
+    __syncthreads();   // the state was written by all threads
+    const int64_t grp = static_cast<int64_t>(b) * p.kv_heads + g;
+    float* part = p.partials + (grp * NC + c) * kAttendPartFloats;
+    constexpr int kPart4 = (16 + 16 * D) / 4;
+    for (int i = tid; i < kPart4; i += kThreads)
+      reinterpret_cast<float4*>(part)[i] = reinterpret_cast<const float4*>(cst)[i];
+    __threadfence();
+    __syncthreads();
+    __shared__ int s_last;
+    if (tid == 0) s_last = atomicAdd(p.tickets + grp, 1) == NC - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const float* gp = p.partials + grp * NC * kAttendPartFloats;
+    for (int it = tid; it < G * (D / 4); it += kThreads) {
+      const int h = it / (D / 4), c4 = (it % (D / 4)) * 4;
+      float M = -INFINITY;
+      for (int q = 0; q < NC; ++q) M = fmaxf(M, __ldcg(gp + q * kAttendPartFloats + h));
+      const float Mu = M == -INFINITY ? 0.f : M;
+      float L = 0.f;
+      float4 oc = make_float4(0.f, 0.f, 0.f, 0.f), om = oc;
+      for (int q = 0; q < NC; ++q) {
+        const float* pq = gp + q * kAttendPartFloats;
+        const float f = exp2f(__ldcg(pq + h) - Mu);
+        L += __ldcg(pq + 8 + h) * f;
+        const float4 a = __ldcg(reinterpret_cast<const float4*>(pq + 16 + h * D + c4));
+        const float4 m = __ldcg(reinterpret_cast<const float4*>(pq + 16 + 8 * D + h * D + c4));
+        oc.x += a.x * f; oc.y += a.y * f; oc.z += a.z * f; oc.w += a.w * f;
+        om.x += m.x; om.y += m.y; om.z += m.z; om.w += m.w;
+      }
+      const float li = L > 0.f ? 1.f / L : 0.f;
+      *reinterpret_cast<float4*>(p.out + (bh0 + h) * D + c4) =
+          make_float4(oc.x * li + om.x, oc.y * li + om.y, oc.z * li + om.z, oc.w * li + om.w);
+    }
+    if (tid == 0) p.tickets[grp] = 0;   // ready for the next launch
+    return;
+  }
+
   // ---- fused K4: the group's CTAs form one thread-block cluster; the ranks
   // merge every rank's state in rank order through distributed shared memory.
   cluster_sync();
@@ -1238,12 +1279,7 @@ static int32_t clusters_fit(int nc) {
 // (one 8-warp CTA per SM), so a layer fills the GPU without a second wave.
 // (Config 2: 128 groups -> 1; config 4 at one GPU: 64 groups -> 2; at one
 // sequence per GPU: 8 groups -> up to 16.)
-int32_t attend_ctas_per_group(int32_t batch, int32_t kv_heads) {
-  static const int32_t forced = [] {
-    const char* e = getenv("SMALLKV_ATTEND_CTAS");   // tuning knob
-    return e ? atoi(e) : 0;
-  }();
-  if (forced > 0) return forced > 16 ? 16 : forced;
+static int32_t num_sms() {
   static const int32_t sms = [] {
     int dev = 0, n = 0;
     if (cudaGetDevice(&dev) != cudaSuccess ||
@@ -1253,12 +1289,38 @@ int32_t attend_ctas_per_group(int32_t batch, int32_t kv_heads) {
     }
     return n;
   }();
+  return sms;
+}
+
+// CTAs per (sequence, kv-group): NC = #SMs / #groups (capped at 32), so a
+// layer fills the GPU in one wave of one 8-warp CTA per SM.  When the GPU
+// co-schedules a cluster of NC CTAs for every group at once (occupancy
+// calculator; non-portable above 8), the ranks merge in distributed shared
+// memory; otherwise the CTAs are launched without a cluster and merge through
+// a global workspace (attend_split_in_cluster false).
+// (Config 2: 128 groups -> 1; config 4 at one GPU: 64 groups -> 2, cluster;
+// at one sequence per GPU: 8 groups -> 18, global merge.)
+int32_t attend_ctas_per_group(int32_t batch, int32_t kv_heads) {
+  static const int32_t forced = [] {
+    const char* e = getenv("SMALLKV_ATTEND_CTAS");   // tuning knob
+    return e ? atoi(e) : 0;
+  }();
+  if (forced > 0) return forced > 32 ? 32 : forced;
   const int64_t groups = static_cast<int64_t>(batch) * kv_heads;
-  int64_t nc = groups > 0 ? sms / groups : 1;
-  if (nc > 16) nc = 16;
-  for (; nc > 1; --nc)
-    if (static_cast<int64_t>(clusters_fit(static_cast<int>(nc))) >= groups) break;
-  return nc < 1 ? 1 : static_cast<int32_t>(nc);
+  const int64_t nc = groups > 0 ? num_sms() / groups : 1;
+  return nc < 1 ? 1 : (nc > 32 ? 32 : static_cast<int32_t>(nc));
+}
+
+bool attend_split_in_cluster(int32_t batch, int32_t kv_heads) {
+  static const int32_t force_global = [] {
+    const char* e = getenv("SMALLKV_ATTEND_GLOBAL_MERGE");   // tuning knob
+    return e ? atoi(e) : 0;
+  }();
+  const int32_t nc = attend_ctas_per_group(batch, kv_heads);
+  if (nc <= 1) return true;
+  if (force_global || nc > 16) return false;
+  const int64_t groups = static_cast<int64_t>(batch) * kv_heads;
+  return static_cast<int64_t>(clusters_fit(nc)) >= groups;
 }
 
 template <int D, bool kAsync>
@@ -1267,7 +1329,7 @@ static cudaError_t launch_d(const AttendParams& p, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(attend_kernel<D, kAsync>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(sm));
   if (e != cudaSuccess) return e;
-  if (p.max_chunks > 8) {
+  if (p.max_chunks > 8 && !p.global_merge) {
     e = cudaFuncSetAttribute(attend_kernel<D, kAsync>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
@@ -1279,14 +1341,14 @@ static cudaError_t launch_d(const AttendParams& p, cudaStream_t s) {
   cfg.dynamicSmemBytes = sm;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = p.max_chunks;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = p.max_chunks;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = p.global_merge ? 1 : 2;   // the global merge needs no cluster
   return cudaLaunchKernelEx(&cfg, attend_kernel<D, kAsync>, p);
 }
 

@@ -123,7 +123,14 @@ struct AttendParams {
   const int32_t* entry_slot;  // nullptr: the paged pool
   int32_t hot_cap;
   int32_t sync_stage;         // diagnostics: stage batch x+1 synchronously at the start of batch x
+  // split without a cluster (max_chunks > the clusters the GPU co-schedules):
+  // every CTA writes its partial state, the last one of the group merges
+  int32_t global_merge;
+  float* partials;            // [B][H_kv][max_chunks][kAttendPartFloats]
+  int32_t* tickets;           // [B][H_kv], zero between launches
 };
+// floats of one CTA's partial state: (m, l) of 8 heads, O_c and O_m of 8 heads x 128
+constexpr int kAttendPartFloats = 16 + 16 * 128;
 
 // variant f4: keep each group's needed rows in an HBM hot pool, fetching only
 // rows that were not resident at the previous step from the host-resident pool.
@@ -146,6 +153,7 @@ cudaError_t launch_attend(const AttendParams& p, cudaStream_t s);
 cudaError_t launch_plan(const AttendParams& p, int32_t n_layers, cudaStream_t s);
 int64_t plan_bytes(int32_t n_layers, int32_t batch, int32_t kv_heads, int32_t max_seq_len);
 int32_t attend_ctas_per_group(int32_t batch, int32_t kv_heads);
+bool attend_split_in_cluster(int32_t batch, int32_t kv_heads);   // else the global merge
 
 // ---------------------------------------------------------------- variant f3 prefill scores (R17)
 struct PrefillParams {

@@ -150,16 +150,23 @@ GroupWs group_ws_layout(const smallkv_cache* slm, const smallkv_batch* b, int32_
 }
 
 struct AttendWs {
-  size_t total;
+  size_t partials, tickets, total;
   int32_t ctas;
+  bool cluster;
 };
-// The attend kernel merges its split work inside thread-block clusters
-// (distributed shared memory), so it needs no global scratch; the workspace
-// argument is kept for ABI stability and future variants.
+// The attend kernel merges a group's split work inside a thread-block cluster
+// (distributed shared memory) when the GPU co-schedules it; otherwise through
+// per-CTA partial states in the workspace and a per-group ticket (zeroed once
+// by the caller, left zeroed by every launch).
 AttendWs attend_ws_layout(const smallkv_cache* llm, const smallkv_batch* b) {
   AttendWs w;
   w.ctas = skv::attend_ctas_per_group(b->batch, llm->num_kv_heads);
-  w.total = 256;
+  w.cluster = skv::attend_split_in_cluster(b->batch, llm->num_kv_heads);
+  const size_t groups = static_cast<size_t>(b->batch) * llm->num_kv_heads;
+  w.tickets = 0;
+  w.partials = round256(groups * 4);
+  w.total = w.cluster ? 256
+                      : w.partials + round256(groups * w.ctas * skv::kAttendPartFloats * sizeof(float));
   return w;
 }
 
@@ -566,6 +573,7 @@ int fill_attend_params(skv::AttendParams& ap, const smallkv_cache* llm, const sm
   }();
   ap.sync_stage = sync_stage_env;
   ap.max_chunks = skv::attend_ctas_per_group(batch->batch, llm->num_kv_heads);
+  ap.global_merge = skv::attend_split_in_cluster(batch->batch, llm->num_kv_heads) ? 0 : 1;
   ap.scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(llm->head_dim));
   return SMALLKV_OK;
 }
@@ -648,6 +656,8 @@ int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
   ap.overlap_prologue = (flags & SMALLKV_ATTEND_OVERLAP_PROLOGUE) ? 1 : 0;
   ap.group_sel = (flags & SMALLKV_ATTEND_GROUP_SELECTION) ? 1 : 0;
   ap.plan = const_cast<uint8_t*>(static_cast<const uint8_t*>(plan));
+  ap.tickets = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(ws) + L.tickets);
+  ap.partials = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + L.partials);
   cudaError_t e = skv::launch_attend(ap, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "attend launch");
   return SMALLKV_OK;
@@ -803,6 +813,8 @@ int smallkv_attend_tiered(int32_t llm_layer, const uint16_t* q, const smallkv_ca
     return fail(SMALLKV_ERR_WORKSPACE, "attend workspace %zu < %zu bytes", ws_bytes, W.total);
   if ((rc = check_device()) != SMALLKV_OK) return rc;
   const TierState T = tier_layout(host_llm, batch, n_llm_layers, capacity);
+  ap.tickets = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(ws) + W.tickets);
+  ap.partials = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + W.partials);
   ap.q = q;
   ap.out = out;
   ap.layer = llm_layer;

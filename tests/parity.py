@@ -232,14 +232,14 @@ def compare_group(p, gpu, sel, layer_slot, out_gpu=None, llm_view=None):
 
 
 def attend_split(step) -> int:
-    """CTAs per (sequence, kv-group) the attend of a DecodeStep launches (its
-    cluster size), recovered from smallkv_plan_size: L*B*H_kv records of
-    256 + NC * (8 warps x 5 tiles x 272 B) bytes (gather_attend.cu)."""
+    """CTAs per (sequence, kv-group) the attend of a DecodeStep launches,
+    recovered from smallkv_plan_size: L*B*H_kv records of 256 + NC * (384 +
+    1024 x 12) bytes (gather_attend.cu plan_record_bytes)."""
     import ctypes
     L = step.llm_layers
     nb = step.lib.smallkv_plan_size(ctypes.byref(step.llm), ctypes.byref(step.batch), L)
     per = nb // (L * step.batch.batch * step.llm.num_kv_heads)
-    return (per - 256) // (8 * 5 * 272)
+    return (per - 256) // (384 + 1024 * 12)
 
 
 def assert_same_outputs(a, b, same_split: bool):

@@ -231,3 +231,16 @@ def test_attend_many_staging_batches():
     e, _ = parity.compare_attend(pc, 0, outs[0].cpu(), sg)
     assert e <= 1e-4, e
     print("many staging batches: row-normwise err", e)
+
+
+@pytest.mark.parametrize("B,n", [(1, 9000), (2, 2600)])
+def test_attend_split_without_cluster(B, n):
+    """Few groups (B x 2 kv-groups): each group's list is split over #SMs /
+    #groups CTAs, more than one cluster the GPU co-schedules, so the CTAs merge
+    their partial states through the workspace (arrival counter, rank-order
+    merge); two layers back to back (PDL overlap) reuse the counters."""
+    cfg = synth.small_config(llm=(2, 8, 2, 128), slm=(2, 8, 2, 64), seq_len=n, batch=B,
+                             budget=(n // 10, n // 20, n // 10))
+    p = synth.make_problem(cfg, seed=66, page_size=16, map_kind="random").to("cuda")
+    rep, _, _ = _check(p)
+    print("split without cluster", B, n, rep)

@@ -75,9 +75,10 @@ def guard_step(st, fill: int) -> Guarded:
         st.gout = smallkv.SelectOut(
             g.make(go.logits.shape, go.logits.dtype), st.out.lse,
             *(g.make(t.shape, t.dtype) for t in (go.crit, go.marg, go.marg_w, go.counts)))
-    # workspaces carry no initialisation requirement (include/smallkv.h): poisoned too
+    # the select workspace carries no initialisation requirement: poisoned too;
+    # the attend workspace is zeroed once by contract (include/smallkv.h)
     st.ws_select = g.make(st.ws_select.shape, torch.uint8)
-    st.ws_attend = g.make(st.ws_attend.shape, torch.uint8)
+    st.ws_attend = g.make(st.ws_attend.shape, torch.uint8).zero_()
     if st.plan_buf is not None:
         st.plan_buf = g.make(st.plan_buf.shape, torch.uint8)
     return g
