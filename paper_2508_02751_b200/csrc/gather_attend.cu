@@ -49,13 +49,19 @@ __device__ __forceinline__ long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-#define SKV_T(i)                                                                         \
+// record of CTA `cta` of layer `skv_tl`: kTraceSlots int64 (tools/attend_trace.py):
+// 0-8 globaltimer ns at the SKV_T points, 10 entries of the share, 11 SM id,
+// 12 ns thread 0 spent in CTA-synchronous batch staging, 13 batches
+constexpr int kTraceSlots = 16;
+#define SKV_TS(i, v)                                                                     \
   if (g_trace && threadIdx.x == 0) {                                                     \
     const int cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;      \
-    g_trace[(skv_tl * 4096 + cta) * 10 + (i)] = gtimer();                                \
+    g_trace[(static_cast<int64_t>(skv_tl) * 4096 + cta) * kTraceSlots + (i)] = (v);      \
   }
+#define SKV_T(i) SKV_TS(i, gtimer())
 #else
 #define SKV_T(i)
+#define SKV_TS(i, v)
 #endif
 
 namespace {
@@ -312,29 +318,43 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const AttendParams p
   __shared__ int s_split[33];
   if (threadIdx.x <= NC) s_split[threadIdx.x] = split_begin(L, threadIdx.x, NC);
   __syncthreads();
+  // only the staged entries are visited: flattened over the ranks' first
+  // batches (s_pre[c] = staged entries of ranks < c)
+  // (thread 32: the tile-table builders below are threads < NC <= 32, and
+  // their serial builds overlap the staging loop)
+  __shared__ int s_pre[33];
+  if (threadIdx.x == 32) {
+    int a = 0;
+    for (int c = 0; c < NC; ++c) {
+      s_pre[c] = a;
+      a += min(kBatch, s_split[c + 1] - s_split[c]);
+    }
+    s_pre[NC] = a;
+  }
+  __syncthreads();
   if (threadIdx.x < NC) {   // each rank's first-batch tile table
     const int c = threadIdx.x, e0 = s_split[c];
     build_tile_table(L, e0, min(kBatch, s_split[c + 1] - e0), p.group_sel != 0,
                      reinterpret_cast<uint32_t*>(rec + kHdrBytes + c * kTileTableBytes));
   }
   constexpr int U = 1024 / kPlanThreads;
-  const int T = L.T;
-  for (int base = threadIdx.x; base < T; base += U * kPlanThreads) {
+  const int F = s_pre[NC];
+  for (int base = threadIdx.x; base < F; base += U * kPlanThreads) {
     int pos[U], slot_i[U];
     uint32_t mk[U];
     float wt[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int x0 = base + u * kPlanThreads;
+      const int f = base + u * kPlanThreads;
       slot_i[u] = -1;
       pos[u] = 0;
       mk[u] = 0u;
       wt[u] = 0.f;
-      if (x0 >= T) continue;
+      if (f >= F) continue;
       int c = 0;
-      while (c < NC - 1 && x0 >= s_split[c + 1]) ++c;
-      const int i = x0 - s_split[c];
-      if (i >= kBatch) continue;
+      while (c < NC - 1 && f >= s_pre[c + 1]) ++c;
+      const int i = f - s_pre[c];
+      const int x0 = s_split[c] + i;
       slot_i[u] = c * kBatch + i;
       const ListEntry le = list_entry(p, L, b, x0, allc);
       pos[u] = le.pos;
@@ -348,7 +368,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const AttendParams p
 #pragma unroll
       for (int u = 0; u < U; ++u)
         ro[u] = slot_i[u] < 0 ? 0u : static_cast<uint32_t>(
-            ((static_cast<int64_t>(b) * p.kv_heads + g) * p.hot_cap + __ldg(es + base + u * kPlanThreads)) * D);
+            ((static_cast<int64_t>(b) * p.kv_heads + g) * p.hot_cap + __ldg(es + s_split[slot_i[u] / kBatch] + slot_i[u] % kBatch)) * D);
     } else {
       int page[U];
 #pragma unroll
@@ -404,6 +424,7 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
   // outputs, page tables, K/V tiles) may run during that kernel's tail.
 #ifdef SKV_TRACE
   const int skv_tl = p.layer;   // trace slot (diagnostic builds only)
+  long long skv_stage_ns = 0;
 #endif
   SKV_T(7);
   if (!p.overlap_prologue) griddep_wait();
@@ -717,11 +738,17 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
     sstep = more ? 0 : 3;
     if (more && (!kAsync || p.sync_stage == 1)) {
       // diagnostics: the whole staging of batch x+1 now, CTA-synchronously
+#ifdef SKV_TRACE
+      const long long t_st = gtimer();
+#endif
       const int eb1 = e_lo + (x + 1) * kBatch, E1 = min(kBatch, e_hi - eb1);
       stage_entries<D>(p, L, b, g, eb1, E1, BOFF(x + 1), BMK(x + 1), BW(x + 1));
       if (tid == 0) build_tile_table(L, eb1, E1, gs, BTT(x + 1));
       mbar_arrive(&bar_staged[(x + 1) & 1]);
       sstep = 3;
+#ifdef SKV_TRACE
+      skv_stage_ns += gtimer() - t_st;
+#endif
     }
     const int nmy = nmy_of(x);
     int nmy_next = -1;   // known once batch x+1 is staged
@@ -912,6 +939,16 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
     l1 += __shfl_xor_sync(0xffffffffu, l1, sh);
   }
   SKV_T(4);
+#ifdef SKV_TRACE
+  {
+    int smid;
+    asm("mov.u32 %0, %%smid;" : "=r"(smid));
+    SKV_TS(10, e_hi - e_lo);
+    SKV_TS(11, smid);
+    SKV_TS(12, skv_stage_ns);
+    SKV_TS(13, nbatch);
+  }
+#endif
 
   // ---- merge warps (fixed order)
   float* wm_s = reinterpret_cast<float*>(stages);              // [kWarps][8]
@@ -1030,15 +1067,6 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
     }
   }
   SKV_T(5);
-#ifdef SKV_TRACE
-  if (g_trace && tid == 0) {
-    const int cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-    int smid;
-    asm("mov.u32 %0, %%smid;" : "=r"(smid));
-    g_trace[(skv_tl * 4096 + cta) * 10 + 8] = e_hi - e_lo;
-    g_trace[(skv_tl * 4096 + cta) * 10 + 9] = smid;
-  }
-#endif
   if (NC == 1) return;
 
   if (p.global_merge) {

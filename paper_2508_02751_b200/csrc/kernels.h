@@ -53,8 +53,8 @@ struct SelectParams {
   int32_t n_chunks, chunk_tokens;
   int32_t batch, row_stride, max_crit, max_marg;
   int32_t log_bins;           // histogram on log(score) (variant f2's group scores)
-  int32_t* todo;              // rows (row * B + b) the cluster split hands to the single-CTA split
-  int32_t* todo_count;        // zeroed by row_flags at the start of each select call
+  int32_t* todo;              // rows (row * B + b) the cluster / register splits hand to the long split
+  int32_t* todo_count;        // [count, consumer ticket]: zeroed by row_flags, emptied by each to-do launch
 };
 cudaError_t launch_select(const SelectParams& p, int32_t max_rows, int32_t max_seq_len,
                           bool overlap_previous, cudaStream_t s);
@@ -62,6 +62,9 @@ cudaError_t launch_select(const SelectParams& p, int32_t max_rows, int32_t max_s
 // `cluster` CTAs (2, 4, 8 or 16) per pair (select_cluster.cu), then the rows it
 // handed over (usually none)
 constexpr int32_t kClusterSplitMinLen = 16384;
+// the long split over the to-do list the cluster / register splits filled (a
+// fixed small grid; returns at once when the list is empty), then empties it
+cudaError_t launch_select_todo(const SelectParams& p, cudaStream_t s);
 cudaError_t launch_select_cluster(const SelectParams& p, int32_t max_rows, int32_t cluster,
                                   cudaStream_t s);
 

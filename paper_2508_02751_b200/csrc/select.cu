@@ -32,12 +32,14 @@
 // passes).  All reductions use a fixed order.
 #include <float.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.h"
 
 #include "select_long.cuh"
 #include "select_row.cuh"
+#include "select_reg.cuh"
 
 namespace skv {
 
@@ -62,6 +64,20 @@ __global__ void __launch_bounds__(kThreads, kRegE > 0 ? SKV_SELECT_REG_MINB : (k
     select_row_long<kLogBins>(p, p.rows[r], blockIdx.x);   // rows longer than kSmemCap
   else
     select_row<kInSmem, kLogBins, kRegE>(p, p.rows[r], blockIdx.x);
+}
+
+#ifndef SKV_SELECT_REGK_MINB
+#define SKV_SELECT_REGK_MINB 5
+#endif
+// Rows of <= 4096 tokens without f1's running sums: the register split
+// (select_reg.cuh); the rows it hands over are finished by the to-do launch.
+template <bool kLogBins>
+__global__ void __launch_bounds__(kRegThreads, SKV_SELECT_REGK_MINB) select_reg_kernel(const SelectParams p) {
+  griddep_launch_dependents();
+  griddep_wait();
+  const int r = p.layer_off[p.layer_begin] + static_cast<int>(blockIdx.y);
+  if (r >= p.layer_off[p.layer_end]) return;
+  select_row_reg<kLogBins>(p, p.rows[r], blockIdx.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -244,6 +260,15 @@ __global__ void __launch_bounds__(kGroupThreads) group_weights_kernel(const Grou
 // run alongside the immediately preceding kernel (the next chunk's K1).  The
 // caller guarantees that this grid's inputs were complete before that kernel
 // started (they come from an earlier launch on the stream).
+// tuning knob: SMALLKV_SELECT_REG=generic keeps short rows on select_row's register variant
+static bool reg_generic() {
+  static const bool g = [] {
+    const char* e = getenv("SMALLKV_SELECT_REG");
+    return e && e[0] == 'g';
+  }();
+  return g;
+}
+
 cudaError_t launch_select(const SelectParams& p, int32_t max_rows, int32_t max_seq_len,
                           bool overlap_previous, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
@@ -256,7 +281,11 @@ cudaError_t launch_select(const SelectParams& p, int32_t max_rows, int32_t max_s
   cfg.attrs = attr;
   cfg.numAttrs = overlap_previous ? 1 : 0;
   cudaError_t e;
-  if (max_seq_len <= kThreads * kRegRow) {
+  if (max_seq_len <= kThreads * kRegRow && !p.acc && !reg_generic()) {
+    e = cudaLaunchKernelEx(&cfg, p.log_bins ? select_reg_kernel<true> : select_reg_kernel<false>, p);
+    if (e != cudaSuccess) return e;
+    return launch_select_todo(p, s);
+  } else if (max_seq_len <= kThreads * kRegRow) {
     e = cudaLaunchKernelEx(&cfg, p.log_bins ? select_kernel<false, true, kRegRow> : select_kernel<false, false, kRegRow>, p);
   } else if (max_seq_len <= kSmemCap) {
     cfg.dynamicSmemBytes = static_cast<size_t>(max_seq_len) * 5 + 16;

@@ -391,6 +391,12 @@ __global__ void __launch_bounds__(kLongThreads, 4) select_todo_kernel(const Sele
     select_row_long<kLogBins>(p, rbi / p.batch, rbi % p.batch);
     __syncthreads();
   }
+  // the last CTA (every CTA has read the count by then) empties the list for
+  // the next split launch of the same call (SLM-layer chunks)
+  if (threadIdx.x == 0 && atomicAdd(p.todo_count + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+    p.todo_count[0] = 0;
+    p.todo_count[1] = 0;
+  }
 }
 }  // namespace
 
@@ -422,13 +428,21 @@ cudaError_t launch_select_cluster(const SelectParams& p, int32_t max_rows, int32
   cudaError_t e = cudaLaunchKernelEx(&cfg, k, p);
   if (e != cudaSuccess) return e;
   // the rows it handed over (usually none)
+  return launch_select_todo(p, s);
+}
+
+cudaError_t launch_select_todo(const SelectParams& p, cudaStream_t s) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
   cudaLaunchConfig_t c2 = {};
   c2.gridDim = dim3(kTodoCtas);
   c2.blockDim = dim3(kLongThreads);
   c2.stream = s;
-  c2.attrs = &attr[1];
+  c2.attrs = attr;
   c2.numAttrs = 1;
-  e = cudaLaunchKernelEx(&c2, p.log_bins ? select_todo_kernel<true> : select_todo_kernel<false>, p);
+  const cudaError_t e =
+      cudaLaunchKernelEx(&c2, p.log_bins ? select_todo_kernel<true> : select_todo_kernel<false>, p);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }

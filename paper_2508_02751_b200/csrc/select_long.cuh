@@ -133,7 +133,7 @@ __device__ __forceinline__ void select_row_long(const SelectParams& p, const int
   __shared__ int wsel[kLongWarps][2];
   __shared__ int s_i[16];            // [0,1] cell count, [2,3] bin, [4,5] above, [6,7] cand count
   __shared__ uint32_t s_u[4];        // [0,1] radix prefix, [2,3] threshold key
-  __shared__ int s_ti[2], s_fb[2], s_rem[2];
+  __shared__ int s_ti[2], s_rem[2];
 
   const int n = p.seq_lens[b];
   const int64_t rb = static_cast<int64_t>(j) * p.batch + b;

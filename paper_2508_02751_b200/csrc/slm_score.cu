@@ -228,7 +228,10 @@ __global__ void row_flags_kernel(const int32_t* __restrict__ head_map, int32_t n
                                  int32_t* __restrict__ todo_count) {
   extern __shared__ uint8_t flags[];
   griddep_launch_dependents();   // K1 may be scheduled now; it waits for our completion
-  if (threadIdx.x == 0) *todo_count = 0;
+  if (threadIdx.x == 0) {
+    todo_count[0] = 0;   // to-do list of the split (count, consumer ticket)
+    todo_count[1] = 0;
+  }
   for (int i = threadIdx.x; i < n_slm; i += blockDim.x) flags[i] = 0;
   __syncthreads();
   for (int i = threadIdx.x; i < n_llm; i += blockDim.x) {

@@ -445,6 +445,19 @@ def select_chunks(slm_layers: int, slm_q_heads: int, batch: int, max_seq_len: in
     return min(slm_layers, -(-slm_layers // per))
 
 
+def split_launches(max_rows: int, batch: int, max_seq_len: int, acc: bool = False) -> int:
+    """Kernels one K2 split launches (mirrors launch_split / launch_select): the
+    register split (rows <= 4096 tokens, no f1 sums) and the cluster split (long
+    rows, < 1024 pairs) are followed by the to-do launch."""
+    if acc:
+        return 1
+    if max_seq_len <= 4096:
+        return 1 if os.environ.get("SMALLKV_SELECT_REG", "").startswith("g") else 2
+    if max_seq_len > 16384 and max_rows * batch < 1024:
+        return 2
+    return 1
+
+
 def from_problem(p, use_plan: bool = True, variant: str = "default",
                  overlap_select=None) -> DecodeStep:
     """DecodeStep for a smallkv_synth.Problem already on the GPU.  overlap_select
@@ -652,7 +665,15 @@ class DecodeGraph:
         nl = self.step.slm.num_layers
         chunks = select_chunks(nl, self.step.slm.num_q_heads, self.step.batch.batch,
                                self.step.batch.max_seq_len, self.step.aux_stream is not None)
-        sel = 2 * chunks if self.step.variant == "default" else 4   # f2: + group score, weights
+        B, S = self.step.batch.batch, self.step.batch.max_seq_len
+        n_llm = int(self.step.head_map.numel())
+        if self.step.variant == "default":
+            # per chunk: slm_score + the split (+ its to-do launch)
+            sel = sum(1 + split_launches(min(n_llm, (hi - lo) * self.step.slm.num_q_heads), B, S)
+                      for lo, hi in ((nl * i // chunks, nl * (i + 1) // chunks) for i in range(chunks)))
+        else:   # f2: slm_score, group score, the split (+ to-do), group weights
+            H_kv = self.step.llm.num_kv_heads
+            sel = 3 + split_launches(self.step.llm_layers * H_kv, B, S)
         tier = 0 if self.tier is None else (2 if self.tier.plan_buf is not None else 1)  # f4
         return (1 + sel + tier + (1 if self.step.plan_buf is not None else 0)
                 + len(self.plan))
