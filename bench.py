@@ -122,7 +122,26 @@ def workload(args):
     return cfg
 
 
-def build_problem(cfg, rank: int, world: int, shard: str, device):
+def f4_capacity(cfg) -> int:
+    """f4 hot-pool slots per group: the largest list R' + (#distinct SLM rows of
+    the group) * (K'+M') under the config's head map and budgets."""
+    import smallkv_synth as synth
+    L, H, Hkv = cfg.llm.layers, cfg.llm.q_heads, cfg.llm.kv_heads
+    hm = synth.head_map_coherent(cfg.llm, cfg.slm).view(L, Hkv, H // Hkv)
+    rows_max = max(len(set(hm[l, g].tolist())) for l in range(L) for g in range(Hkv))
+    K, R, M = cfg.budget
+    return -(-(R + rows_max * (K + M)) // 4) * 4
+
+
+def f4_device_bytes(cfg, B: int) -> int:
+    """HBM the f4 hot pools (K and V) and tier state take."""
+    cap = f4_capacity(cfg)
+    groups = cfg.llm.layers * B * cfg.llm.kv_heads
+    return groups * cap * cfg.llm.head_dim * 2 * 2 + groups * (cfg.seq_len * 4 + cap * 21)
+
+
+def build_problem(cfg, rank: int, world: int, shard: str, device, reserve: int = 0,
+                  max_resident: int = 0):
     """Rank `rank`'s inputs of a `world`-rank job over the config's GLOBAL batch
     (strong scaling).  batch sharding: the sequences batch_shard(B, world, rank)
     (drawn with seed = rank; every rank holds both models' caches of its own
@@ -141,10 +160,12 @@ def build_problem(cfg, rank: int, world: int, shard: str, device):
     per_layer = B * kv_share * cfg.seq_len * cfg.llm.head_dim * 2 * 2
     free = torch.cuda.mem_get_info(device)[0]
     slm_bytes = cfg.slm.layers * B * cfg.slm.kv_heads * cfg.seq_len * cfg.slm.head_dim * 2
-    budget = int(0.8 * free) - slm_bytes - (4 << 30)
+    budget = int(0.8 * free) - slm_bytes - (4 << 30) - reserve
     if heads:   # the full LLM pool is generated once, then sliced (a copy of the slice)
         budget = budget * kv_share // (cfg.llm.kv_heads + kv_share)
     resident = max(1, min(cfg.llm.layers, budget // per_layer))
+    if max_resident:
+        resident = min(resident, max_resident)
     p = synth.make_problem(cfg, seed=0 if heads else rank, device=device, batch=B,
                            llm_layers=list(range(resident)))
     if heads:
@@ -198,13 +219,24 @@ def run_ours(args, world, rank, local):
     cfg = workload(args)
     heads = args.shard in ("heads", "heads-slm") and jw > 1
     slm_part = args.shard == "heads-slm" and jw > 1
-    p, resident = build_problem(cfg, jr, jw, args.shard, device)
+    if args.variant == "f4":
+        # the hot pools and tier state stay in HBM; the host copy of the resident
+        # layer slots must fit pinned host memory (half of it at most)
+        import psutil
+        B0 = len(pdist.batch_shard(cfg.batch, jw, jr))
+        per_layer = B0 * cfg.llm.kv_heads * cfg.seq_len * cfg.llm.head_dim * 2 * 2
+        p, resident = build_problem(cfg, jr, jw, args.shard, device, reserve=f4_device_bytes(cfg, B0),
+                                    max_resident=max(1, psutil.virtual_memory().total // 2 // per_layer))
+    else:
+        p, resident = build_problem(cfg, jr, jw, args.shard, device)
     L = cfg.llm.layers
     tier = None
     if args.variant == "f4":
         # host-tiered pool: the LLM K/V in pinned host memory,
-        # each group's needed rows in an HBM hot pool refreshed per layer
-        assert resident == L, "f4 keeps one hot-pool slot per LLM layer"
+        # each group's needed rows in an HBM hot pool refreshed per layer.  The
+        # host pool holds the problem's resident layer slots (LLM layer l reads
+        # slot l mod resident, as the HBM path's rotation); the hot pool has a
+        # slot per LLM layer.
         step = smallkv.from_problem(p, use_plan=False)
         host_k = torch.empty(p.llm.k.shape, dtype=p.llm.k.dtype, pin_memory=True)
         host_v = torch.empty(p.llm.v.shape, dtype=p.llm.v.dtype, pin_memory=True)
@@ -215,7 +247,10 @@ def run_ours(args, world, rank, local):
         hm = p.head_map.cpu().view(L, Hkv, H // Hkv)
         rows_max = max(len(set(hm[l, g].tolist())) for l in range(L) for g in range(Hkv))
         cap = -(-(int(p.n_recent.max()) + rows_max * (p.max_crit + p.max_marg)) // 4) * 4
-        tier = smallkv.TieredKV(step, host_k, host_v, capacity=cap)
+        assert cap <= f4_capacity(cfg), (cap, f4_capacity(cfg))
+        per_layer = args.f4_refresh == "per-layer"
+        tier = smallkv.TieredKV(step, host_k, host_v, capacity=cap, use_plan=not per_layer,
+                                per_layer=per_layer)
     else:
         step = smallkv.from_problem(p, variant=args.variant)
     H_loc, d = p.cfg.llm.q_heads, cfg.llm.head_dim
@@ -631,11 +666,28 @@ def f4_report(p, cfg, graph, tier, steps: int = 20):
     s.synchronize()
     ms = e0.elapsed_time(e1) / steps
     per = (f3 - f2) / steps
+    # the host link's copy peak on this box: pinned host -> device, 1 GiB
+    hb = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
+    db = torch.empty(1 << 30, dtype=torch.uint8, device=p.slm_q.device)
+    db.copy_(hb, non_blocking=True)
+    torch.cuda.synchronize()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record()
+    for _ in range(3):
+        db.copy_(hb, non_blocking=True)
+    c1.record()
+    c1.synchronize()
+    link_peak = 3 * (1 << 30) / (c0.elapsed_time(c1) / 1e3) / 1e9
+    del hb, db
     return {"steady_rows_fetched_per_step": (f1 - f0) / 3,
+            "refresh": "per-layer (side stream, overlaps the attends)" if tier.per_layer
+                       else "all layers in one launch after select",
+            "host_link_peak_gbs": round(link_peak, 2),
             "drift": {"value": round(cfg.llm.layers / (ms / 1e3), 2), "unit": "layer-steps/s",
                       "ms_per_step": round(ms, 4), "rows_fetched_per_step": per,
                       "host_link_bytes_per_step": int(per * row_bytes),
                       "host_link_gbs": round(per * row_bytes / (ms / 1e3) / 1e9, 2),
+                      "host_link_frac": round(per * row_bytes / (ms / 1e3) / 1e9 / link_peak, 3),
                       "note": "SLM query alternating between two inputs each step"},
             "capacity_overflows": ov,
             "hot_pool_bytes": int(tier.hot_k.numel() * 4),
@@ -779,6 +831,9 @@ def main():
     ap.add_argument("--variant", choices=["default", "f2", "f4"], default="default",
                     help="f2: per-KV-group shared selection (SURVEY §8(f) f2, DESIGN.md R16); "
                          "f4: host-tiered KV pool (SURVEY §8(f) f4, DESIGN.md R18)")
+    ap.add_argument("--f4-refresh", choices=["per-layer", "all"], default="all",
+                    help="f4: refresh layer l+1's hot pool on a side stream during attend l "
+                         "(per-layer), or every layer in one launch after select (all)")
     ap.add_argument("--shard", choices=["batch", "heads", "heads-slm"], default="batch",
                     help="N>1 partition of the global batch: sequences or LLM kv-head groups")
     ap.add_argument("--emulate-world", type=int, default=1,

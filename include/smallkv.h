@@ -333,7 +333,8 @@ int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
  * lives in HOST memory (pinned, UVA-addressable: `host_llm.k/v`); each
  * (layer, sequence, kv-group) keeps the rows its current list needs in an HBM
  * hot pool of `capacity` slots:
- *   host_llm       layer l of its pools holds LLM layer l (num_layers >= L).
+ *   host_llm       LLM layer l reads layer slot l mod host_llm.num_layers of its
+ *                  pools (num_layers = L: every layer; fewer: a rotated subset).
  *   hot_k / hot_v  device bf16 [L][B][H_kv][capacity][d] (caller-owned).
  *   state          device bytes >= smallkv_tier_state_size(): per group the
  *                  position->slot and slot->position maps, residency flags, the
@@ -357,8 +358,9 @@ int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
  * smallkv_attend_tiered: smallkv_attend reading the hot pool (plan: NULL or
  * smallkv_plan_tiered's).
  * flags: SMALLKV_ATTEND_GROUP_SELECTION for variant f2 selections.
- * Errors: as smallkv_attend, plus max_seq_len > 32768 or bad capacity
- * (SMALLKV_ERR_SHAPE), small state (SMALLKV_ERR_WORKSPACE).
+ * Errors: as smallkv_attend, plus max_seq_len > 524288 or a capacity that is
+ * not a multiple of 4 in [4, 2^24] (SMALLKV_ERR_SHAPE), small state
+ * (SMALLKV_ERR_WORKSPACE).
  */
 size_t smallkv_tier_state_size(const smallkv_cache* llm, const smallkv_batch* batch,
                                int32_t n_llm_layers, int32_t capacity);

@@ -1153,18 +1153,17 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
 // Rows resident at the previous step are not moved (migrate the
 // change, in parallel with the forward).
 constexpr int kTierThreads = 256;
-constexpr int kTierMaxSeq = 32768;   // bitmaps in shared memory
-
 template <int D>
 __global__ void __launch_bounds__(kTierThreads) tier_update_kernel(const TierParams t) {
   const AttendParams& p = t.a;
   __shared__ __align__(16) GroupLayout L;
-  __shared__ uint32_t need_v[kTierMaxSeq / 32], need_k[kTierMaxSeq / 32], claimed[kTierMaxSeq / 32];
   __shared__ int s_nfree, s_nmiss;
-  extern __shared__ int dyn[];   // [cap] entry positions | [cap] free slots | [cap] missing positions
-  int* s_pos = dyn;
-  int* s_free = dyn + t.cap;
-  int* s_miss = dyn + 2 * t.cap;
+  // per-position bitmaps (3 x ceil(max_seq_len / 32) words: 48 KB at 128K tokens)
+  extern __shared__ uint32_t bitmaps[];
+  const int nw = (t.max_seq_len + 31) / 32;
+  uint32_t* need_v = bitmaps;
+  uint32_t* need_k = bitmaps + nw;
+  uint32_t* claimed = bitmaps + 2 * nw;
   const int g = blockIdx.x, b = blockIdx.y, layer = t.layer_begin + blockIdx.z, tid = threadIdx.x;
   build_layout(p, layer, b, g, L);
   const int n = L.n, T = L.T;
@@ -1173,12 +1172,19 @@ __global__ void __launch_bounds__(kTierThreads) tier_update_kernel(const TierPar
     return;
   }
   const int64_t grp = (static_cast<int64_t>(layer) * p.batch + b) * p.kv_heads + g;
+  // per-entry scratch in global memory (L2): [cap] entry positions | [cap]
+  // free slots | [cap] missing positions
+  int* s_pos = t.scratch + grp * 3 * t.cap;
+  int* s_free = s_pos + t.cap;
+  int* s_miss = s_pos + 2 * t.cap;
   int32_t* sop = t.slot_of_pos + grp * t.max_seq_len;
   int32_t* pos_of = t.pos_of_slot + grp * t.cap;
   uint8_t* flags = t.slot_flags + grp * t.cap;
   int32_t* es = t.entry_slot + grp * t.cap;
-  const uint16_t* host_k = t.host_k + static_cast<int64_t>(layer) * t.host_layer_stride;
-  const uint16_t* host_v = t.host_v + static_cast<int64_t>(layer) * t.host_layer_stride;
+  // host layer slot: layer mod the host pool's layers (a caller may rotate a subset)
+  const int64_t hl = layer % t.host_layers;
+  const uint16_t* host_k = t.host_k + hl * t.host_layer_stride;
+  const uint16_t* host_v = t.host_v + hl * t.host_layer_stride;
   const int64_t hot0 = (static_cast<int64_t>(layer) * p.batch + b) * p.kv_heads + g;
   uint16_t* hot_k = t.hot_k + hot0 * t.cap * D;
   uint16_t* hot_v = t.hot_v + hot0 * t.cap * D;
@@ -1248,21 +1254,37 @@ __global__ void __launch_bounds__(kTierThreads) tier_update_kernel(const TierPar
     s_jpos[j] = pos;
   }
   __syncthreads();
-  // (5) the copies: 16-byte chunks over the host link, spread over all threads
+  // (5) the copies over the host link: 16-byte chunks, consecutive threads on
+  // consecutive chunks of a row (V then K: 2 x D*2 contiguous bytes per job),
+  // kTierU chunk loads in flight per thread before their stores
   const int njob = s_nmiss;
   const int32_t* bt = p.block_table + static_cast<int64_t>(b) * p.max_blocks;
   constexpr int CH = D / 8;
-  for (int it = tid; it < njob * 2 * CH; it += kTierThreads) {
-    const int j = it / (2 * CH), which = (it / CH) & 1, c = it % CH;   // which: 0 V, 1 K
-    const uint32_t job = static_cast<uint32_t>(s_job[j]);
-    if (!((job >> (30 + which)) & 1u)) continue;
-    const int pos = s_jpos[j], sl = static_cast<int>(job & 0x3fffffffu);
-    const int64_t src = ((static_cast<int64_t>(__ldg(bt + (pos >> p.ps_shift))) * p.kv_heads + g) *
-                             p.page_size + (pos & (p.page_size - 1))) * D;
-    const uint4 v = reinterpret_cast<const uint4*>((which ? host_k : host_v) + src)[c];
-    reinterpret_cast<uint4*>((which ? hot_k : hot_v) + static_cast<int64_t>(sl) * D)[c] = v;
-    if (c == 0) atomicAdd(t.counters, 1ull);
+  constexpr int kTierU = 4;
+  unsigned long long rows = 0;
+  for (int it0 = tid; it0 < njob * 2 * CH; it0 += kTierU * kTierThreads) {
+    uint4 v[kTierU];
+    uint4* dst[kTierU];
+#pragma unroll
+    for (int u = 0; u < kTierU; ++u) {
+      const int it = it0 + u * kTierThreads;
+      dst[u] = nullptr;
+      if (it >= njob * 2 * CH) continue;
+      const int j = it / (2 * CH), which = (it / CH) & 1, c = it % CH;   // which: 0 V, 1 K
+      const uint32_t job = static_cast<uint32_t>(s_job[j]);
+      if (!((job >> (30 + which)) & 1u)) continue;
+      const int pos = s_jpos[j], sl = static_cast<int>(job & 0x3fffffffu);
+      const int64_t src = ((static_cast<int64_t>(__ldg(bt + (pos >> p.ps_shift))) * p.kv_heads + g) *
+                               p.page_size + (pos & (p.page_size - 1))) * D;
+      v[u] = reinterpret_cast<const uint4*>((which ? host_k : host_v) + src)[c];
+      dst[u] = reinterpret_cast<uint4*>((which ? hot_k : hot_v) + static_cast<int64_t>(sl) * D) + c;
+      if (c == 0) ++rows;
+    }
+#pragma unroll
+    for (int u = 0; u < kTierU; ++u)
+      if (dst[u]) *dst[u] = v[u];
   }
+  if (rows) atomicAdd(t.counters, rows);
 }
 
 }  // namespace
@@ -1403,7 +1425,7 @@ cudaError_t launch_plan(const AttendParams& p, int32_t n_layers, cudaStream_t s)
 }
 
 cudaError_t launch_tier_update(const TierParams& t, cudaStream_t s) {
-  const size_t sm = static_cast<size_t>(t.cap) * 3 * sizeof(int);
+  const size_t sm = static_cast<size_t>((t.max_seq_len + 31) / 32) * 3 * sizeof(uint32_t);
   dim3 grid(t.a.kv_heads, t.a.batch, t.layer_count);
   auto k = t.a.head_dim == 64 ? tier_update_kernel<64> : tier_update_kernel<128>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));

@@ -144,11 +144,13 @@ struct TierParams {
   uint16_t* hot_k;            // [L][B][H_kv][cap][d]
   uint16_t* hot_v;
   int64_t host_layer_stride;  // elements
+  int32_t host_layers;        // host pool layer slots: LLM layer l reads slot l mod host_layers
   int32_t* slot_of_pos;       // [L][B][H_kv][max_seq_len]  (-1: not resident)
   int32_t* pos_of_slot;       // [L][B][H_kv][cap]          (-1: free)
   uint8_t* slot_flags;        // [L][B][H_kv][cap]          bit0 V resident, bit1 K resident
   int32_t* entry_slot;        // [L][B][H_kv][cap]
   unsigned long long* counters;   // [0] rows fetched (K or V), [1] capacity overflows
+  int32_t* scratch;           // [L][B][H_kv][3][cap] per-entry work lists
   int32_t cap, max_seq_len, layer_begin, layer_count;
 };
 cudaError_t launch_tier_update(const TierParams& p, cudaStream_t s);

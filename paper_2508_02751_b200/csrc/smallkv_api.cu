@@ -665,7 +665,7 @@ int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
 
 namespace {
 struct TierState {
-  size_t sop, pos_of, entry, flags, counters, total;
+  size_t sop, pos_of, entry, flags, counters, scratch, total;
 };
 TierState tier_layout(const smallkv_cache* llm, const smallkv_batch* b, int32_t L, int32_t cap) {
   TierState t;
@@ -674,15 +674,21 @@ TierState tier_layout(const smallkv_cache* llm, const smallkv_batch* b, int32_t 
   t.pos_of = round256(groups * b->max_seq_len * 4);
   t.entry = t.pos_of + round256(groups * cap * 4);
   t.flags = t.entry + round256(groups * cap * 4);
-  t.counters = t.flags + round256(groups * cap);
+  t.scratch = t.flags + round256(groups * cap);
+  t.counters = t.scratch + round256(groups * cap * 3 * 4);   // last 256 bytes (TieredKV.counters)
   t.total = t.counters + 256;
   return t;
 }
+// the update's position bitmaps (3 bits per position) live in shared memory
+constexpr int32_t kTierMaxSeq = 524288;
+constexpr int32_t kTierMaxCap = 1 << 24;
 int check_tier(const smallkv_cache* llm, const smallkv_batch* batch, int32_t L, int32_t cap) {
   if (!llm || !batch) return fail(SMALLKV_ERR_NULL, "tier: NULL cache/batch");
-  if (L < 1 || cap < 4 || cap % 4 != 0 || cap > 65536)
-    return fail(SMALLKV_ERR_SHAPE, "tier: layers %d / capacity %d (multiple of 4 in [4,65536])", L, cap);
-  if (batch->max_seq_len > 32768) return fail(SMALLKV_ERR_SHAPE, "tier: max_seq_len > 32768");
+  if (L < 1 || cap < 4 || cap % 4 != 0 || cap > kTierMaxCap)
+    return fail(SMALLKV_ERR_SHAPE, "tier: layers %d / capacity %d (multiple of 4 in [4,%d])", L, cap,
+                kTierMaxCap);
+  if (batch->max_seq_len > kTierMaxSeq)
+    return fail(SMALLKV_ERR_SHAPE, "tier: max_seq_len %d > %d", batch->max_seq_len, kTierMaxSeq);
   return SMALLKV_OK;
 }
 }  // namespace
@@ -724,7 +730,7 @@ int smallkv_tier_update(int32_t layer_begin, int32_t layer_count, const smallkv_
   if (!hot_k || !hot_v) return fail(SMALLKV_ERR_NULL, "tier: NULL hot pool");
   if (flags & ~SMALLKV_ATTEND_GROUP_SELECTION) return fail(SMALLKV_ERR_SHAPE, "tier: unknown flags");
   if (layer_begin < 0 || layer_count < 1 || layer_begin + layer_count > n_llm_layers ||
-      host_llm->num_layers < n_llm_layers || layer_count > 65535)
+      host_llm->num_layers < 1 || layer_count > 65535)
     return fail(SMALLKV_ERR_SHAPE, "tier: layers [%d,%d) vs %d LLM / %d pool layers", layer_begin,
                 layer_begin + layer_count, n_llm_layers, host_llm->num_layers);
   const TierState T = tier_layout(host_llm, batch, n_llm_layers, capacity);
@@ -738,6 +744,8 @@ int smallkv_tier_update(int32_t layer_begin, int32_t layer_count, const smallkv_
   tp.host_v = host_llm->v;
   tp.host_layer_stride = static_cast<int64_t>(host_llm->num_pages) * host_llm->num_kv_heads *
                          host_llm->page_size * host_llm->head_dim;
+  tp.host_layers = host_llm->num_layers;
+  tp.scratch = reinterpret_cast<int32_t*>(st + T.scratch);
   tp.hot_k = hot_k;
   tp.hot_v = hot_v;
   tp.slot_of_pos = reinterpret_cast<int32_t*>(st + T.sop);

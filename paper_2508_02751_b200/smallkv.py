@@ -344,11 +344,15 @@ class TieredKV:
     host link) and read by smallkv_attend_tiered."""
 
     def __init__(self, step: DecodeStep, host_k: torch.Tensor, host_v: torch.Tensor,
-                 capacity: int, use_plan: bool = True):
-        """host_k / host_v: pinned CPU pools [L][pages][kv][ps][d] (layer l = LLM layer l)."""
+                 capacity: int, use_plan: bool = True, per_layer: bool = False):
+        """host_k / host_v: pinned CPU pools [Lh][pages][kv][ps][d]; LLM layer l reads
+        host layer slot l mod Lh.  per_layer: a decode graph refreshes layer by layer
+        on a side stream, the refresh of layer l+1 overlapping the attend of layer l
+        (no plan: the attends stage their lists themselves)."""
         assert host_k.device.type == "cpu" and host_k.is_pinned() and host_v.is_pinned()
-        assert host_k.shape[0] >= step.llm_layers
+        assert not (per_layer and use_plan), "the per-layer refresh runs without a plan"
         self.step = step
+        self.per_layer = per_layer
         self.lib = step.lib
         bt_keep = step._keep[4]   # llm block table (device)
         self.host = make_cache(host_k, host_v, bt_keep, step.llm.num_q_heads)
@@ -576,12 +580,15 @@ class DecodeGraph:
         if self.host_io is not None:
             return self._calls_host_io()
         if self.tier is not None:
-            # f4: one refresh of every layer's hot pool right after select (ahead
+            # f4: the refresh of every layer's hot pool right after select (ahead
             # of the attends), then the attends; the first attend reads
             # what the refresh wrote, so only later ones overlap their prologue
+            main = torch.cuda.current_stream()
             self.step.select(self.slm_q)
-            self.tier.update()
+            evs = self._tier_refresh(main)
             for i, (layer, slot, q, out) in enumerate(self.plan):
+                if evs:
+                    main.wait_event(evs[i])
                 self.tier.attend(layer, q, out, overlap_prologue=i > 0)
             return
         if record:
@@ -595,6 +602,29 @@ class DecodeGraph:
             self.step.attend(layer, slot, q, out, overlap_prologue=i > 0)
             if record:
                 self.events[2 + i].record()
+
+    def _tier_refresh(self, main):
+        """f4 refresh after select: one launch for every layer, or (per-layer tier)
+        one launch per layer on a high-priority side stream, so the refresh of
+        layer l+1 crosses the host link while layer l attends; returns the
+        per-layer completion events (None: all refreshed in order on `main`)."""
+        t = self.tier
+        if not t.per_layer:
+            t.update()
+            return None
+        if not hasattr(self, "tier_stream"):
+            self.tier_stream = torch.cuda.Stream(priority=-1)
+        done = torch.cuda.Event()
+        done.record(main)
+        self.tier_stream.wait_event(done)
+        evs = []
+        with torch.cuda.stream(self.tier_stream):
+            for layer, _, _, _ in self.plan:
+                t.update(layer, 1)
+                e = torch.cuda.Event()
+                e.record(self.tier_stream)
+                evs.append(e)
+        return evs
 
     def _calls_host_io(self):
         """select + attends with the host copies on side streams (see __init__)."""
@@ -614,8 +644,9 @@ class DecodeGraph:
             q_ready = torch.cuda.Event()
             q_ready.record(self.h2d_stream)
         self.step.select(self.slm_q)
+        evs = None
         if self.tier is not None:
-            self.tier.update()   # f4: refresh every layer's hot pool after select
+            evs = self._tier_refresh(main)   # f4: refresh the hot pools after select
         main.wait_event(q_ready)
         # outputs read back in pairs of layers: one fork per pair (each fork
         # costs the attend chain more than a pair's copy delay; measured 0.665
@@ -624,6 +655,8 @@ class DecodeGraph:
         for i, (layer, slot, q, out) in enumerate(self.plan):
             if self.tier is not None:
                 # the first attend reads what the refresh wrote (no overlap)
+                if evs:
+                    main.wait_event(evs[i])
                 self.tier.attend(layer, q, out, overlap_prologue=i > 0)
             else:
                 self.step.attend(layer, slot, q, out, overlap_prologue=i > 0)
@@ -674,6 +707,7 @@ class DecodeGraph:
         else:   # f2: slm_score, group score, the split (+ to-do), group weights
             H_kv = self.step.llm.num_kv_heads
             sel = 3 + split_launches(self.step.llm_layers * H_kv, B, S)
-        tier = 0 if self.tier is None else (2 if self.tier.plan_buf is not None else 1)  # f4
+        tier = (0 if self.tier is None else len(self.plan) if self.tier.per_layer
+                else (2 if self.tier.plan_buf is not None else 1))   # f4
         return (1 + sel + tier + (1 if self.step.plan_buf is not None else 0)
                 + len(self.plan))

@@ -541,16 +541,19 @@ def test_f3_head_matching_end_to_end():
 
 # ---------------------------------------------------------------- variant f4 (R18)
 
-def _tiered_step(p, variant="default"):
+def _tiered_step(p, variant="default", per_layer=False, host_layers=None):
     from paper_2508_02751_b200 import smallkv
     step = smallkv.from_problem(p, use_plan=False, variant=variant)
-    host_k = torch.empty(p.llm.k.shape, dtype=p.llm.k.dtype, pin_memory=True)
-    host_v = torch.empty(p.llm.v.shape, dtype=p.llm.v.dtype, pin_memory=True)
-    host_k.copy_(p.llm.k)
-    host_v.copy_(p.llm.v)
+    src_k = p.llm.k if host_layers is None else p.llm.k[:host_layers]
+    src_v = p.llm.v if host_layers is None else p.llm.v[:host_layers]
+    host_k = torch.empty(src_k.shape, dtype=p.llm.k.dtype, pin_memory=True)
+    host_v = torch.empty(src_v.shape, dtype=p.llm.v.dtype, pin_memory=True)
+    host_k.copy_(src_k)
+    host_v.copy_(src_v)
     G = p.cfg.llm.q_heads // p.cfg.llm.kv_heads
     cap = -(-(int(p.n_recent.max()) + G * (p.max_crit + p.max_marg)) // 4) * 4
-    tier = smallkv.TieredKV(step, host_k, host_v, capacity=cap)
+    tier = smallkv.TieredKV(step, host_k, host_v, capacity=cap, use_plan=not per_layer,
+                            per_layer=per_layer)
     return step, tier
 
 
@@ -605,6 +608,72 @@ def test_f4_tiered_pool_bitwise(variant, map_kind):
         for slot, (ref, got) in enumerate(both):
             e, _ = parity.compare_attend(p, slot, got, sg)
             assert e <= parity.OUT_TOL
+
+
+def test_f4_long_context_and_rotated_host_pool():
+    """f4 past the former 32768-token limit (bitmaps sized by max_seq_len, work
+    lists in global memory): n = 40000 with a ragged second sequence, bitwise
+    equal to the HBM-resident path and to the oracle; and a host pool of ONE
+    layer slot serving both LLM layers (slot l mod 1), against the HBM path
+    reading cache slot 0 for both."""
+    cfg = _cfg(llm=(2, 8, 2, 128), slm=(2, 8, 2, 64), n=40000, B=2, budget=(4000, 2000, 4000))
+    p = synth.make_problem(cfg, seed=45, page_size=64, seq_lens=[40000, 9001]).to("cuda")
+    step, tier = _tiered_step(p)
+    both = _run_both(p, step, tier, p.slm_q)
+    for ref, got in both:
+        assert torch.equal(ref, got)
+    f1, ov = tier.counters()
+    assert ov == 0 and f1 > 0
+    sel = parity.oracle_select(p)
+    parity.compare_select(p, step.out, sel)
+    sg = parity.sel_from_gpu(p, step.out, sel)
+    for slot, (ref, got) in enumerate(both):
+        e, _ = parity.compare_attend(p, slot, got, sg)
+        assert e <= parity.OUT_TOL
+    # rotation: host slot l mod 1
+    step1, tier1 = _tiered_step(p, host_layers=1)
+    step1.select(p.slm_q)
+    tier1.update()
+    for layer in range(2):
+        ref = torch.empty(p.batch, p.cfg.llm.q_heads, p.cfg.llm.head_dim, device="cuda")
+        got = torch.empty_like(ref)
+        step1.attend(layer, 0, p.llm_q[layer], ref)
+        tier1.attend(layer, p.llm_q[layer], got)
+        torch.cuda.synchronize()
+        assert torch.equal(ref, got), layer
+
+
+def test_decode_graph_tier_per_layer_refresh():
+    """DecodeGraph with the per-layer f4 refresh (each layer's tier update on a
+    high-priority side stream, attend l waiting only for refresh l): outputs
+    bitwise equal to the eager all-layer refresh, over a repeated step (nothing
+    fetched) and a drifted one (only non-resident rows fetched)."""
+    from paper_2508_02751_b200 import smallkv
+    cfg = _cfg(llm=(3, 8, 2, 128), slm=(2, 8, 2, 64), n=1500, B=3, budget=(150, 60, 200))
+    p = synth.make_problem(cfg, seed=47, page_size=16, seq_lens=[1500, 700, 1]).to("cuda")
+    step, tier = _tiered_step(p)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    q2 = (p.slm_q.float() + 0.5 * torch.randn(p.slm_q.shape, device="cuda", generator=g)).to(torch.bfloat16)
+    refs1 = [ref for ref, _ in _run_both(p, step, tier, p.slm_q)]
+    refs2 = [ref for ref, _ in _run_both(p, step, tier, q2)]
+    stepg, tierg = _tiered_step(p, per_layer=True)
+    L = p.llm.num_layers
+    shape = (p.batch, cfg.llm.q_heads, cfg.llm.head_dim)
+    outs = torch.empty((L,) + shape, dtype=torch.float32, device="cuda")
+    slm_q = p.slm_q.clone()
+    plan = [(l, l, p.llm_q[l], outs[l]) for l in range(L)]
+    graph = smallkv.DecodeGraph(stepg, slm_q, plan, tier=tierg)
+    assert graph.kernels_per_step >= 2 * L
+    for q, refs in ((p.slm_q, refs1), (p.slm_q, refs1), (q2, refs2)):
+        slm_q.copy_(q)
+        graph.replay()
+        graph.stream.synchronize()
+        if q is p.slm_q:
+            f_before, _ = tierg.counters()
+        for l in range(L):
+            assert torch.equal(outs[l], refs[l]), l
+    f_after, ov = tierg.counters()
+    assert ov == 0 and f_after > f_before
 
 
 def test_f3b_partitioned_slm_virtual_ranks_bit_identical():
