@@ -1192,16 +1192,21 @@ __global__ void __launch_bounds__(kTierThreads) tier_update_kernel(const TierPar
   if (tid == 0) s_nfree = s_nmiss = 0;
   __syncthreads();
   // (1) the list's positions (decoded once) and their needs: K+V for recent /
-  // critical entries, V for marginal ones
+  // critical entries, V for marginal ones.  s_pos keeps (position | K needed
+  // << 31) of the last refresh: an identical list leaves nothing to do (the
+  // steady state), which one comparison per entry detects.
+  int changed = T != t.prev_T[grp];
   for (int x = tid; x < T; x += kTierThreads) {
     const ListEntry le = list_entry(p, L, b, x, 0xffu);
     const int pos = le.pos;
     const bool k = (le.mask & 0xffu) != 0u;   // critical / recent: K needed
-    s_pos[x] = pos;
+    const int code = pos | (k ? static_cast<int>(0x80000000u) : 0);
+    changed |= s_pos[x] != code;
+    s_pos[x] = code;
     atomicOr(&need_v[pos >> 5], 1u << (pos & 31));
     if (k) atomicOr(&need_k[pos >> 5], 1u << (pos & 31));
   }
-  __syncthreads();
+  if (!__syncthreads_or(changed)) return;
   // (2) free the slots of positions no longer needed; collect free slots
   for (int sl = tid; sl < t.cap; sl += kTierThreads) {
     int pos = pos_of[sl];
@@ -1216,13 +1221,16 @@ __global__ void __launch_bounds__(kTierThreads) tier_update_kernel(const TierPar
   __syncthreads();
   // (3) newly needed positions (each once), then their slots
   for (int x = tid; x < T; x += kTierThreads) {
-    const int pos = s_pos[x];
+    const int pos = s_pos[x] & 0x7fffffff;
     if (sop[pos] < 0 && !((atomicOr(&claimed[pos >> 5], 1u << (pos & 31)) >> (pos & 31)) & 1u))
       s_miss[atomicAdd(&s_nmiss, 1)] = pos;
   }
   __syncthreads();
   const int nmiss = s_nmiss, nfree = s_nfree;
-  if (tid == 0 && nmiss > nfree) atomicAdd(t.counters + 1, 1ull);
+  if (tid == 0) {
+    if (nmiss > nfree) atomicAdd(t.counters + 1, 1ull);
+    t.prev_T[grp] = nmiss > nfree ? -1 : T;   // (an overflow: refresh in full next time)
+  }
   for (int i = tid; i < min(nmiss, nfree); i += kTierThreads) {
     const int pos = s_miss[i], sl = s_free[i];
     pos_of[sl] = pos;
@@ -1239,7 +1247,7 @@ __global__ void __launch_bounds__(kTierThreads) tier_update_kernel(const TierPar
   int* s_job = s_free;   // slot | getv << 30 | getk << 31
   int* s_jpos = s_miss;  // its position
   for (int x = tid; x < T; x += kTierThreads) {
-    const int pos = s_pos[x];
+    const int pos = s_pos[x] & 0x7fffffff;
     const int sl = sop[pos];
     es[x] = sl < 0 ? 0 : sl;
     if (sl < 0) continue;
