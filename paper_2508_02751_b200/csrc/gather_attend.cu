@@ -474,10 +474,26 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
     const int n = p.seq_lens[b];
     const int Rc = min(max(p.n_recent[b], 0), n);
     const int32_t* bt = p.block_table + static_cast<int64_t>(b) * p.max_blocks;
+    constexpr int NE = NSTAGE - 1;
+    int ne = 0;   // early stages of this warp: tiles warp + i*kWarps of the recent run
 #pragma unroll
-    for (int i = 0; i < NSTAGE - 1; ++i) {
-      const int j = warp + i * kWarps;   // tile j = entries [16j, 16j+16) of the recent run
-      if (kTile * j >= Rc || early != i) break;
+    for (int i = 0; i < NE; ++i)
+      if (kTile * (warp + i * kWarps) < Rc && ne == i) ne = i + 1;
+    // every page-table entry first (one round trip), then the copies
+    int page[NE][kTile / 4];
+#pragma unroll
+    for (int i = 0; i < NE; ++i)
+#pragma unroll
+      for (int grp = 0; grp < kTile / 4; ++grp) {
+        const int j = warp + i * kWarps;
+        const int eo = grp * 4 + (lane >> 3);
+        const int pos = n - Rc + kTile * j + eo;
+        page[i][grp] = (i < ne && kTile * j + eo < Rc) ? __ldg(bt + (pos >> p.ps_shift)) : 0;
+      }
+#pragma unroll
+    for (int i = 0; i < NE; ++i) {
+      if (i >= ne) break;
+      const int j = warp + i * kWarps;
       const int cnt = min(kTile, Rc - kTile * j);
       uint8_t* st = wst + i * SB;
 #pragma unroll
@@ -486,8 +502,8 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
         const bool ev = eo < cnt;
         const int pos = n - Rc + kTile * j + eo;
         const uint32_t ro = ev ? static_cast<uint32_t>(
-                                     ((static_cast<int64_t>(__ldg(bt + (pos >> p.ps_shift))) * p.kv_heads + g) *
-                                          p.page_size + (pos & (p.page_size - 1))) * D)
+                                     ((static_cast<int64_t>(page[i][grp]) * p.kv_heads + g) * p.page_size +
+                                      (pos & (p.page_size - 1))) * D)
                                : 0u;
 #pragma unroll
         for (int hf = 0; hf < D / 64; ++hf) {
