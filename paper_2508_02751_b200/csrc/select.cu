@@ -44,7 +44,14 @@
 namespace skv {
 
 namespace {
-constexpr int kSmemCap = 8192;   // rows staged in shared memory (40 KB); longer rows read L2 directly
+#ifndef SKV_SMEM_CAP
+#define SKV_SMEM_CAP 8192
+#endif
+#ifndef SKV_REG_MAX_LEN
+#define SKV_REG_MAX_LEN 12288
+#endif
+constexpr int kRegMaxLen = SKV_REG_MAX_LEN;   // rows the register split holds (f1: the splits below)
+constexpr int kSmemCap = SKV_SMEM_CAP;   // rows staged in shared memory (5 B per token); longer rows read L2 directly
                                  // (measured faster from 16K tokens up: more CTAs per SM)
 
 // grid (B, max_rows): the CTAs of a row are consecutive and the rows past the
@@ -71,13 +78,13 @@ __global__ void __launch_bounds__(kThreads, kRegE > 0 ? SKV_SELECT_REG_MINB : (k
 #endif
 // Rows of <= 4096 tokens without f1's running sums: the register split
 // (select_reg.cuh); the rows it hands over are finished by the to-do launch.
-template <bool kLogBins>
-__global__ void __launch_bounds__(kRegThreads, SKV_SELECT_REGK_MINB) select_reg_kernel(const SelectParams p) {
+template <bool kLogBins, int kT, int kE>
+__global__ void __launch_bounds__(kT, kT == 256 ? SKV_SELECT_REGK_MINB : 2) select_reg_kernel(const SelectParams p) {
   griddep_launch_dependents();
   griddep_wait();
   const int r = p.layer_off[p.layer_begin] + static_cast<int>(blockIdx.y);
   if (r >= p.layer_off[p.layer_end]) return;
-  select_row_reg<kLogBins>(p, p.rows[r], blockIdx.x);
+  select_row_reg<kLogBins, kT, kE>(p, p.rows[r], blockIdx.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -281,8 +288,16 @@ cudaError_t launch_select(const SelectParams& p, int32_t max_rows, int32_t max_s
   cfg.attrs = attr;
   cfg.numAttrs = overlap_previous ? 1 : 0;
   cudaError_t e;
-  if (max_seq_len <= kThreads * kRegRow && !p.acc && !reg_generic()) {
-    e = cudaLaunchKernelEx(&cfg, p.log_bins ? select_reg_kernel<true> : select_reg_kernel<false>, p);
+  if (max_seq_len <= kRegMaxLen && !p.acc && !reg_generic()) {
+    if (max_seq_len <= 4096) {
+      e = cudaLaunchKernelEx(&cfg, p.log_bins ? select_reg_kernel<true, 256, 16> : select_reg_kernel<false, 256, 16>, p);
+    } else if (max_seq_len <= 8192) {
+      cfg.blockDim = dim3(512);
+      e = cudaLaunchKernelEx(&cfg, p.log_bins ? select_reg_kernel<true, 512, 16> : select_reg_kernel<false, 512, 16>, p);
+    } else {
+      cfg.blockDim = dim3(512);
+      e = cudaLaunchKernelEx(&cfg, p.log_bins ? select_reg_kernel<true, 512, 24> : select_reg_kernel<false, 512, 24>, p);
+    }
     if (e != cudaSuccess) return e;
     return launch_select_todo(p, s);
   } else if (max_seq_len <= kThreads * kRegRow) {

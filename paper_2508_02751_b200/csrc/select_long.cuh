@@ -60,67 +60,67 @@ __device__ __forceinline__ void long_loadU(const float* src, int base, int strid
 }
 
 // One warp writes the ascending lists of its segment [s0, s1) of the ranked
-// range: position i is critical iff (score, i) <= (XA, IA) lexicographically
-// (score > XA, or == XA and i <= IA), in the inclusive set iff <= (XB, IB),
-// marginal iff inclusive and not critical.  oc / om: the warp's first slots
-// in crit / marg.  score = the ranking value (logits, or f1's sums: then
-// `row` holds the logits, whose a' is marg_w).
+// range (s0 a multiple of 4): position i is critical iff (score, i) <= (XA, IA)
+// lexicographically (score > XA, or == XA and i <= IA), in the inclusive set
+// iff <= (XB, IB), marginal iff inclusive and not critical.  oc / om: the
+// warp's first slots in crit / marg.  score = the ranking value (logits, or
+// f1's sums: then `row` holds the logits, whose a' is marg_w).
+// Each lane takes 16 consecutive positions per step (four 16-byte loads, L1
+// allocating: the halves of a sector two loads apart are one L1 line), so one
+// packed warp scan serves 512 positions and the lists are written per set bit.
 __device__ __forceinline__ void long_emit(const float* score, const float* row, int s0, int s1, int lane,
                                           float XA, int IA, float XB, int IB, float lse, bool al,
                                           int32_t* crit, int32_t* marg, float* mw, int oc, int om) {
-  for (int base0 = s0; base0 < s1; base0 += 128 * kLongU) {
-    float4 v4[kLongU];
-    long_loadU<kLongU>(score, base0 + 4 * lane, 128, s1, al, v4);
+  for (int base = s0; base < s1; base += 512) {
+    const int p0 = base + 16 * lane;
+    float v[16];
+    if (al && p0 + 15 < s1) {
 #pragma unroll
-    for (int u = 0; u < kLongU; ++u) {
-      const int base = base0 + 128 * u + 4 * lane;
-      const float xs[4] = {v4[u].x, v4[u].y, v4[u].z, v4[u].w};
-      uint32_t cm = 0u, mm = 0u;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int ik = base + k;
-        const bool valid = ik < s1;
-        const bool isC = valid && (xs[k] > XA || (xs[k] == XA && ik <= IA));
-        const bool inB = valid && (xs[k] > XB || (xs[k] == XB && ik <= IB));
-        cm |= static_cast<uint32_t>(isC) << k;
-        mm |= static_cast<uint32_t>(inB && !isC) << k;
+      for (int u = 0; u < 4; ++u) {
+        const float4 t = *reinterpret_cast<const float4*>(score + p0 + 4 * u);
+        v[4 * u] = t.x;
+        v[4 * u + 1] = t.y;
+        v[4 * u + 2] = t.z;
+        v[4 * u + 3] = t.w;
       }
-      const int own = __popc(cm) | (__popc(mm) << 16);
-      int incl = own;
+    } else {
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      int32_t* cp = crit + oc + ((incl - own) & 0xffff);
-      int32_t* mp = marg + om + ((incl - own) >> 16);
-      float* wp = mw + om + ((incl - own) >> 16);
-      if (cm | mm) {
-        float wv[4];
+      for (int e = 0; e < 16; ++e) v[e] = p0 + e < s1 ? score[p0 + e] : 0.f;
+    }
+    uint32_t cm = 0u, bm = 0u;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) wv[k] = xs[k];
-        if (row)   // f1: the weight is the current step's a', not the running sum
+    for (int e = 0; e < 16; ++e) {
+      const int i = p0 + e;
+      const bool valid = i < s1;
+      const bool isC = valid && (v[e] > XA || (v[e] == XA && i <= IA));
+      const bool inB = valid && (v[e] > XB || (v[e] == XB && i <= IB));
+      cm |= static_cast<uint32_t>(isC) << e;
+      bm |= static_cast<uint32_t>(inB) << e;
+    }
+    const uint32_t mm = bm & ~cm;
+    const int own = __popc(cm) | (__popc(mm) << 16);
+    int incl = own;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) wv[k] = (mm >> k) & 1u ? row[base + k] : 0.f;
-        // predicated stores, no per-position branches
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int ac = oc + ((incl - own) & 0xffff), am = om + ((incl - own) >> 16);
+    for (uint32_t m = cm; m; m &= m - 1u) crit[ac++] = p0 + __ffs(m) - 1;
+    if (mm) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint32_t cc = (cm >> k) & 1u, m = (mm >> k) & 1u;
-          const float a = __expf(wv[k] - lse);   // a' of the current step (Eq. 6)
-          if (cc) *cp = base + k;
-          if (m) {
-            *mp = base + k;
-            *wp = a;
-          }
-          cp += cc;
-          mp += m;
-          wp += m;
+      for (int e = 0; e < 16; ++e) {
+        if ((mm >> e) & 1u) {
+          marg[am] = p0 + e;
+          // a' of the current step (Eq. 6); f1: from the logits, not the running sum
+          mw[am] = __expf((row ? row[p0 + e] : v[e]) - lse);
+          ++am;
         }
       }
-      const int tot = __shfl_sync(0xffffffffu, incl, 31);
-      oc += tot & 0xffff;
-      om += tot >> 16;
     }
+    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+    oc += tot & 0xffff;
+    om += tot >> 16;
   }
 }
 

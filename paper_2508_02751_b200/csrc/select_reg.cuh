@@ -1,6 +1,7 @@
-// select_reg.cuh — K2's split of SHORT rows (n <= 4096 tokens, the 4K-context
-// configurations) with the row held in registers: one 256-thread CTA per
-// (SLM row, sequence), 16 consecutive positions per thread.
+// select_reg.cuh — K2's split of SHORT rows (n <= 12288 tokens: the 4K and 8K
+// contexts) with the row held in registers: one CTA per (SLM row, sequence),
+// kRegE consecutive positions per thread (256 x 16 up to 4096 tokens, 512 x 16
+// up to 8192, 512 x 24 up to 12288).
 //
 // Same result as select_row (select_row.cuh; Eq. 4, Eq. 6
 // P:141-152, R1-R5, R10; f2's log-coordinate bins, R16): exact lexicographic
@@ -32,11 +33,7 @@
 
 namespace skv {
 namespace {
-constexpr int kRegThreads = 256;
-constexpr int kRegWarps = kRegThreads / 32;
 constexpr int kRegBins = 256;
-constexpr int kRegE = 16;        // positions per thread
-constexpr int kRegCap = 256;     // boundary-bin pairs held per boundary
 
 __device__ __forceinline__ int rclamp(int x, int lo, int hi) { return x < lo ? lo : (x > hi ? hi : x); }
 // 0xff in byte k iff k < r (r positions left in a 4-position word; r <= 0: none)
@@ -51,8 +48,12 @@ __device__ __forceinline__ void rlse_combine(float& m, float& s, float m2, float
   m = mm;
 }
 
-template <bool kLogBins>
+// kRegThreads threads x kRegE positions per thread (rows up to their product)
+template <bool kLogBins, int kRegThreads, int kRegE>
 __device__ __forceinline__ void select_row_reg(const SelectParams& p, const int j, const int b) {
+  constexpr int kRegWarps = kRegThreads / 32;
+  constexpr int kRegCap = kRegThreads * kRegE / 16;   // boundary-bin pairs held per boundary
+  static_assert(kRegE % 4 == 0 && kRegE <= 32, "16-bit packed counts, 32-bit masks");
   __shared__ __align__(16) uint32_t hist[kRegWarps][kRegBins];
   __shared__ unsigned long long cand[2][kRegCap];
   __shared__ float red[4];

@@ -451,12 +451,14 @@ def select_chunks(slm_layers: int, slm_q_heads: int, batch: int, max_seq_len: in
 
 def split_launches(max_rows: int, batch: int, max_seq_len: int, acc: bool = False) -> int:
     """Kernels one K2 split launches (mirrors launch_split / launch_select): the
-    register split (rows <= 4096 tokens, no f1 sums) and the cluster split (long
-    rows, < 1024 pairs) are followed by the to-do launch."""
+    register split (rows <= 12288 tokens, no f1 sums) and the cluster split
+    (long rows, < 1024 pairs) are followed by the to-do launch."""
     if acc:
         return 1
-    if max_seq_len <= 4096:
-        return 1 if os.environ.get("SMALLKV_SELECT_REG", "").startswith("g") else 2
+    if max_seq_len <= 12288:   # kernels.h / select.cu kRegMaxLen
+        if os.environ.get("SMALLKV_SELECT_REG", "").startswith("g"):
+            return 1
+        return 2
     if max_seq_len > 16384 and max_rows * batch < 1024:
         return 2
     return 1
