@@ -394,11 +394,13 @@ def test_qwen14b_full_size_sampled():
     print("qwen14b n=16384", _full_size_sampled(cfg16, budget=(1638, 819, 1638), n_seqs=2))
 
 
-@pytest.mark.parametrize("n", [4096, 4097, 6000, 9000])
+@pytest.mark.parametrize("n", [4096, 4097, 6000, 9000, 14000])
 def test_select_row_storage_variants(n):
-    """K2 keeps a row in registers (n <= 4096), shared memory (<= 8192) or
-    reads it from global memory (longer): the same exact split from each,
-    at the boundaries of the variants, with a ragged second sequence."""
+    """K2 keeps a row in registers (256 x 16 up to 4096 tokens, 512 x 16 up to
+    8192, 512 x 24 up to 12288) or reads it from global memory (longer; f1
+    rows: shared memory up to 8192): the same exact split
+    from each, at the boundaries of the variants, with a ragged second
+    sequence."""
     cfg = _cfg(n=n, B=2, budget=(n // 10, n // 20, n // 10))
     p = synth.make_problem(cfg, seed=23, page_size=16, seq_lens=[n, n // 3 + 1]).to("cuda")
     rep, _, _ = _check(p)
