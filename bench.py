@@ -321,6 +321,10 @@ def run_ours(args, world, rank, local):
     sgraph = smallkv.DecodeGraph(step, p.slm_q, [], timing=False)   # select only
     # isolated attend launches: CUDA events between the calls (no PDL overlap)
     tgraph = smallkv.DecodeGraph(step, p.slm_q, plan, timing=True) if not slm_part else None
+    # serialised launches: the same step with no attend overlapping the previous
+    # one (each waits for its predecessor before it reads anything)
+    igraph = (smallkv.DecodeGraph(step, p.slm_q, plan, timing=False, overlap=False)
+              if not slm_part and tier is None else None)
 
     seq = [int(x) for x in p.seq_lens.cpu()]
     buds = list(zip(p.k_crit.cpu().tolist(), p.n_recent.cpu().tolist(), p.k_marg.cpu().tolist()))
@@ -392,13 +396,28 @@ def run_ours(args, world, rank, local):
     step_local_ms = elapsed_ms / args.steps
     attend_pipe_ms = max(1e-6, (step_local_ms - select_avg_ms) / L)
     attend_iso_ms = None
+    attend_ev_ms = None
     if tgraph is not None:
         samples = []
         for _ in range(max(5, min(args.steps, 50))):
             tgraph.replay()
             tgraph.stream.synchronize()
             samples.extend(tgraph.segment_ms()[1])
-        attend_iso_ms = statistics.median(samples)
+        attend_ev_ms = statistics.median(samples)
+    if igraph is not None:
+        for _ in range(3):
+            igraph.replay()
+        igraph.stream.synchronize()
+        i0 = torch.cuda.Event(enable_timing=True)
+        i1 = torch.cuda.Event(enable_timing=True)
+        i0.record(igraph.stream)
+        for _ in range(nsel):
+            igraph.replay()
+        i1.record(igraph.stream)
+        i1.synchronize()
+        attend_iso_ms = max(1e-6, (i0.elapsed_time(i1) / nsel - select_avg_ms) / L)
+    elif attend_ev_ms is not None:
+        attend_iso_ms = attend_ev_ms
 
     # ---- end to end: pinned host q', q in; outputs back to pinned host, every step
     e2e = None
@@ -473,10 +492,14 @@ def run_ours(args, world, rank, local):
             "traffic": traffic,
             "algorithmic_bytes_per_launch": attend_bytes,
             "avg_launch_ms": round(launch_ms, 5),
-            "avg_launch_ms_note": ("median isolated launch: CUDA events between the attend "
+            "avg_launch_ms_note": ("serialised launches: (a graph of select + L attends, none "
+                                   "overlapping its predecessor) - select, per layer"
+                                   if igraph is not None else
+                                   "median isolated launch: CUDA events between the attend "
                                    "launches of a timing graph (no cross-layer PDL overlap)"
                                    if attend_iso_ms is not None else
                                    "pipelined-effective: (ms_per_step - select_ms) / L"),
+            "event_bracketed_launch_ms": None if attend_ev_ms is None else round(attend_ev_ms, 5),
             "achieved_pipelined": round(achieved_pipe, 1),
             "frac_pipelined": round(achieved_pipe / hbm, 4),
             "pipelined_ms_per_layer": round(attend_pipe_ms, 5),

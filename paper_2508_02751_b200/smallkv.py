@@ -469,7 +469,9 @@ def from_problem(p, use_plan: bool = True, variant: str = "default",
     """DecodeStep for a smallkv_synth.Problem already on the GPU.  overlap_select
     None: automatic (auto_overlap_select)."""
     if overlap_select is None:
-        overlap_select = False
+        # tuning knob: SMALLKV_OVERLAP_SELECT=1 runs K2 of each SLM-layer chunk on
+        # an auxiliary stream beside K1 of the next chunk
+        overlap_select = os.environ.get("SMALLKV_OVERLAP_SELECT", "0") == "1"
     return DecodeStep(slm_k=p.slm.k, slm_block_table=p.slm.block_table,
                       slm_q_heads=p.cfg.slm.q_heads, llm_k=p.llm.k, llm_v=p.llm.v,
                       llm_block_table=p.llm.block_table, llm_q_heads=p.cfg.llm.q_heads,
@@ -555,8 +557,9 @@ class DecodeGraph:
     """
 
     def __init__(self, step: DecodeStep, slm_q: torch.Tensor, layer_plan, timing: bool = False,
-                 host_io=None, tier: Optional["TieredKV"] = None):
+                 host_io=None, tier: Optional["TieredKV"] = None, overlap: bool = True):
         self.step = step
+        self.overlap = overlap   # False: no attend starts its prologue during the previous one
         self.tier = tier   # variant f4: (tier_update, tiered attend) per layer
         self.slm_q = slm_q
         self.plan = list(layer_plan)
@@ -601,7 +604,7 @@ class DecodeGraph:
         for i, (layer, slot, q, out) in enumerate(self.plan):
             # every attend after the first is separated from select by another
             # attend, so its prologue may overlap the previous kernel's tail
-            self.step.attend(layer, slot, q, out, overlap_prologue=i > 0)
+            self.step.attend(layer, slot, q, out, overlap_prologue=i > 0 and self.overlap)
             if record:
                 self.events[2 + i].record()
 
