@@ -41,6 +41,8 @@ def main():
     ap.add_argument("--variant", default="default")
     ap.add_argument("--no-build", action="store_true")
     ap.add_argument("--json", default=None)
+    ap.add_argument("--emulate-world", type=int, default=1,
+                    help="trace rank 0's batch shard of a G-rank job (small batches)")
     args = ap.parse_args()
     if not args.no_build:
         build_trace_lib()
@@ -53,7 +55,7 @@ def main():
     ns = argparse.Namespace(config=args.config, tau=None, seq_len=None)
     cfg = bench.workload(ns)
     dev = torch.device("cuda:0")
-    p, resident = bench.build_problem(cfg, 0, 1, "batch", dev)
+    p, resident = bench.build_problem(cfg, 0, args.emulate_world, "batch", dev)
     L = cfg.llm.layers
     step = smallkv.from_problem(p, variant=args.variant)
     outs = torch.empty(L, p.batch, p.cfg.llm.q_heads, cfg.llm.head_dim, dtype=torch.float32, device=dev)
