@@ -1102,22 +1102,41 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
     if (!s_last) return;
     __threadfence();
     const float* gp = p.partials + grp * NC * kAttendPartFloats;
-    for (int it = tid; it < G * (D / 4); it += kThreads) {
-      const int h = it / (D / 4), c4 = (it % (D / 4)) * 4;
+    // every rank's (m, l) at once, then per head the rank weights 2^(m_q - M)
+    // and L in rank order; the O rows with 8 ranks' loads in flight per thread
+    __shared__ float s_m[32][8], s_l[32][8], s_L[8];
+    if (tid < NC * 8) {
+      const int q = tid >> 3, h = tid & 7;
+      s_m[q][h] = __ldcg(gp + q * kAttendPartFloats + h);
+      s_l[q][h] = __ldcg(gp + q * kAttendPartFloats + 8 + h);
+    }
+    __syncthreads();
+    if (tid < G) {
       float M = -INFINITY;
-      for (int q = 0; q < NC; ++q) M = fmaxf(M, __ldcg(gp + q * kAttendPartFloats + h));
+      for (int q = 0; q < NC; ++q) M = fmaxf(M, s_m[q][tid]);
       const float Mu = M == -INFINITY ? 0.f : M;
       float L = 0.f;
+      for (int q = 0; q < NC; ++q) {
+        const float f = exp2f(s_m[q][tid] - Mu);
+        L += s_l[q][tid] * f;
+        s_m[q][tid] = f;   // (now the rank's weight)
+      }
+      s_L[tid] = L;
+    }
+    __syncthreads();
+    for (int it = tid; it < G * (D / 4); it += kThreads) {
+      const int h = it / (D / 4), c4 = (it % (D / 4)) * 4;
       float4 oc = make_float4(0.f, 0.f, 0.f, 0.f), om = oc;
+#pragma unroll 8
       for (int q = 0; q < NC; ++q) {
         const float* pq = gp + q * kAttendPartFloats;
-        const float f = exp2f(__ldcg(pq + h) - Mu);
-        L += __ldcg(pq + 8 + h) * f;
+        const float f = s_m[q][h];
         const float4 a = __ldcg(reinterpret_cast<const float4*>(pq + 16 + h * D + c4));
         const float4 m = __ldcg(reinterpret_cast<const float4*>(pq + 16 + 8 * D + h * D + c4));
         oc.x += a.x * f; oc.y += a.y * f; oc.z += a.z * f; oc.w += a.w * f;
         om.x += m.x; om.y += m.y; om.z += m.z; om.w += m.w;
       }
+      const float L = s_L[h];
       const float li = L > 0.f ? 1.f / L : 0.f;
       *reinterpret_cast<float4*>(p.out + (bh0 + h) * D + c4) =
           make_float4(oc.x * li + om.x, oc.y * li + om.y, oc.z * li + om.z, oc.w * li + om.w);
