@@ -107,16 +107,15 @@ __device__ __forceinline__ void long_emit(const float* score, const float* row, 
     }
     int ac = oc + ((incl - own) & 0xffff), am = om + ((incl - own) >> 16);
     for (uint32_t m = cm; m; m &= m - 1u) crit[ac++] = p0 + __ffs(m) - 1;
-    if (mm) {
-#pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        if ((mm >> e) & 1u) {
-          marg[am] = p0 + e;
-          // a' of the current step (Eq. 6); f1: from the logits, not the running sum
-          mw[am] = __expf((row ? row[p0 + e] : v[e]) - lse);
-          ++am;
-        }
-      }
+    // per set bit (a 16-way predicated loop costs every lane ~100 instructions
+    // per step); the value comes back from L1 — this lane loaded it just now
+    // (f1: the logit, not the running sum: a' of the current step, Eq. 6)
+    const float* wsrc = row ? row : score;
+    for (uint32_t m = mm; m; m &= m - 1u) {
+      const int i = p0 + __ffs(m) - 1;
+      marg[am] = i;
+      mw[am] = __expf(wsrc[i] - lse);
+      ++am;
     }
     const int tot = __shfl_sync(0xffffffffu, incl, 31);
     oc += tot & 0xffff;
