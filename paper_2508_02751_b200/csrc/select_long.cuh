@@ -35,7 +35,10 @@ constexpr int kLongThreads = 256;
 constexpr int kLongWarps = kLongThreads / 32;
 constexpr int kLongBins = 2048;
 constexpr int kLongCap = 1024;
-constexpr int kLongU = 4;   // 16-byte loads in flight per thread and pass
+#ifndef SKV_LONG_U
+#define SKV_LONG_U 4
+#endif
+constexpr int kLongU = SKV_LONG_U;   // 16-byte loads in flight per thread and pass
 
 __device__ __forceinline__ int lclamp(int x, int lo, int hi) { return x < lo ? lo : (x > hi ? hi : x); }
 
