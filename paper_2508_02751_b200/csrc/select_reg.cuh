@@ -34,6 +34,7 @@
 namespace skv {
 namespace {
 constexpr int kRegBins = 256;
+constexpr int kRankDirect = 48;   // boundary lists up to this long: ranks counted per position
 
 __device__ __forceinline__ int rclamp(int x, int lo, int hi) { return x < lo ? lo : (x > hi ? hi : x); }
 // 0xff in byte k iff k < r (r positions left in a 4-position word; r <= 0: none)
@@ -42,6 +43,68 @@ __device__ __forceinline__ uint32_t rvalid_bytes(int r) {
 }
 // byte mask (0x00 / 0xff per byte) -> 4-bit mask
 __device__ __forceinline__ uint32_t rbytes_to_bits(uint32_t x) { return ((x & 0x08040201u) * 0x01010101u) >> 24; }
+// The want-th smallest (0-based) of n distinct u64 in shared memory, by one
+// warp: MSB-first 8-bit radix select (h: a 256-word shared histogram of the
+// warp's own).  All lanes return it.
+__device__ __forceinline__ unsigned long long warp_select_u64(const unsigned long long* lst, int n, int want,
+                                                              uint32_t* h, int lane) {
+  unsigned long long prefix = 0ull, mask = 0ull;
+  int rem = want;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) h[lane * 8 + q] = 0u;
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {
+      const unsigned long long v = lst[i];
+      if ((v & mask) == prefix) atomicAdd(&h[static_cast<int>((v >> shift) & 255ull)], 1u);
+    }
+    __syncwarp();
+    int c[8], tot = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      c[q] = static_cast<int>(h[lane * 8 + q]);
+      tot += c[q];
+    }
+    int incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int run = incl - tot, dig = -1, below = 0, cnt = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (rem >= run && rem < run + c[q]) {
+        dig = lane * 8 + q;
+        below = run;
+        cnt = c[q];
+      }
+      run += c[q];
+    }
+    const int src = __ffs(__ballot_sync(0xffffffffu, dig >= 0)) - 1;
+    dig = __shfl_sync(0xffffffffu, dig, src);
+    below = __shfl_sync(0xffffffffu, below, src);
+    cnt = __shfl_sync(0xffffffffu, cnt, src);
+    prefix |= static_cast<unsigned long long>(dig) << shift;
+    mask |= 255ull << shift;
+    rem -= below;
+    __syncwarp();
+    if (cnt == 1) break;   // one value left with this prefix
+  }
+  if (mask == ~0ull) return prefix;
+  unsigned long long found = 0ull;
+  bool hit = false;
+  for (int i = lane; i < n; i += 32) {
+    const unsigned long long v = lst[i];
+    if ((v & mask) == prefix) {
+      found = v;
+      hit = true;
+    }
+  }
+  const int src = __ffs(__ballot_sync(0xffffffffu, hit)) - 1;
+  return __shfl_sync(0xffffffffu, found, src < 0 ? 0 : src);
+}
+
 __device__ __forceinline__ void rlse_combine(float& m, float& s, float m2, float s2) {
   const float mm = fmaxf(m, m2);
   s = s * __expf(m - mm) + s2 * __expf(m2 - mm);
@@ -216,6 +279,26 @@ __device__ __forceinline__ void select_row_reg(const SelectParams& p, const int 
     cand[t][atomicAdd(&s_cnt[t], 1)] = (static_cast<unsigned long long>(desc_key(v)) << 32) | static_cast<uint32_t>(i);
   }
   __syncthreads();
+  const int nA = binA >= 0 ? s_cnt[0] : 0, nB = s_cnt[1];
+  // Long boundary lists (8K-token rows: ~100+ pairs): each boundary's threshold
+  // pair by a one-warp radix select, O(n), broadcast after one more barrier.
+  // Short ones: every boundary position counts its own rank, O(n) per
+  // position, no barrier.
+  // (256-thread rows, <= 4096 tokens: measured faster without it — config 2
+  // 63 vs 66 us — so compiled out there)
+  const bool radix = kRegThreads > 256 && (nA > kRankDirect || nB > kRankDirect);   // (uniform)
+  __shared__ unsigned long long s_thr[2];
+  if (radix) {
+    if (warp < 2 && (warp == 1 || binA >= 0)) {
+      const int t = warp;
+      const unsigned long long* lst = (t == 1 && shared) ? cand[0] : cand[t];
+      const int n = t == 0 || shared ? nA : nB;
+      const int want = (t == 0 ? rA - aboveA : rB - aboveB) - 1;
+      const unsigned long long thr = warp_select_u64(lst, n, want, &hist[t][0], lane);
+      if (lane == 0) s_thr[t] = thr;
+    }
+    __syncthreads();
+  }
 
   // ---- 5. classification.  Bins strictly above a boundary bin are inside it
   // (bins are monotone in the score), bins below outside; a boundary-bin
@@ -230,8 +313,21 @@ __device__ __forceinline__ void select_row_reg(const SelectParams& p, const int 
     cm |= c4 << (4 * q);
     bsel |= b4 << (4 * q);
   }
-  if (exm) {
-    const int nA = binA >= 0 ? s_cnt[0] : 0, nB = s_cnt[1];
+  if (exm && radix) {
+    for (uint32_t m = exm; m; m &= m - 1u) {
+      const int e = __ffs(m) - 1;
+      const int i = i0 + e;
+      const float v = __ldg(row + i);
+      const int bin = rclamp(static_cast<int>((bv(v) - blo) * scale), 0, kRegBins - 1);
+      const unsigned long long kv = (static_cast<unsigned long long>(desc_key(v)) << 32) | static_cast<uint32_t>(i);
+      if (bin == binA) {
+        if (kv <= s_thr[0]) cm |= 1u << e;
+        if (!shared || kv <= s_thr[1]) bsel |= 1u << e;
+      } else if (kv <= s_thr[1]) {
+        bsel |= 1u << e;
+      }
+    }
+  } else if (exm) {
     for (uint32_t m = exm; m; m &= m - 1u) {
       const int e = __ffs(m) - 1;
       const int i = i0 + e;
