@@ -90,16 +90,26 @@ __device__ __forceinline__ void long_emit(const float* score, const float* row, 
 #pragma unroll
       for (int e = 0; e < 16; ++e) v[e] = p0 + e < s1 ? score[p0 + e] : 0.f;
     }
-    uint32_t cm = 0u, bm = 0u;
+    // (score, i) <= (X, I): for a whole step with i <= I that is score >= X,
+    // with i > I score > X; only the one step holding I compares both
+    auto sel16 = [&](float X, int I) {
+      uint32_t r = 0u;
+      if (p0 + 15 <= I) {
 #pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const int i = p0 + e;
-      const bool valid = i < s1;
-      const bool isC = valid && (v[e] > XA || (v[e] == XA && i <= IA));
-      const bool inB = valid && (v[e] > XB || (v[e] == XB && i <= IB));
-      cm |= static_cast<uint32_t>(isC) << e;
-      bm |= static_cast<uint32_t>(inB) << e;
-    }
+        for (int e = 0; e < 16; ++e) r |= static_cast<uint32_t>(v[e] >= X) << e;
+      } else if (p0 > I) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) r |= static_cast<uint32_t>(v[e] > X) << e;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          r |= static_cast<uint32_t>(v[e] > X || (v[e] == X && p0 + e <= I)) << e;
+      }
+      return r;
+    };
+    const uint32_t vmask = s1 - p0 >= 16 ? 0xffffu : (s1 > p0 ? (1u << (s1 - p0)) - 1u : 0u);
+    const uint32_t cm = sel16(XA, IA) & vmask;   // (NaN XA when there is no target A: none)
+    const uint32_t bm = sel16(XB, IB) & vmask;
     const uint32_t mm = bm & ~cm;
     const int own = __popc(cm) | (__popc(mm) << 16);
     int incl = own;
