@@ -1303,7 +1303,10 @@ __global__ void __launch_bounds__(kTierThreads) tier_update_kernel(const TierPar
   const int njob = s_nmiss;
   const int32_t* bt = p.block_table + static_cast<int64_t>(b) * p.max_blocks;
   constexpr int CH = D / 8;
-  constexpr int kTierU = 4;
+#ifndef SKV_TIER_U
+#define SKV_TIER_U 4
+#endif
+  constexpr int kTierU = SKV_TIER_U;
   unsigned long long rows = 0;
   for (int it0 = tid; it0 < njob * 2 * CH; it0 += kTierU * kTierThreads) {
     uint4 v[kTierU];
