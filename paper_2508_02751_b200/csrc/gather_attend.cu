@@ -1202,11 +1202,14 @@ __global__ void __launch_bounds__(kTierThreads) tier_update_kernel(const TierPar
   const int g = blockIdx.x, b = blockIdx.y, layer = t.layer_begin + blockIdx.z, tid = threadIdx.x;
   build_layout(p, layer, b, g, L);
   const int n = L.n, T = L.T;
+  const int64_t grp = (static_cast<int64_t>(layer) * p.batch + b) * p.kv_heads + g;
   if (T > t.cap) {   // the list does not fit the group's slots: reported, nothing changed
-    if (tid == 0) atomicAdd(t.counters + 1, 1ull);
+    if (tid == 0) {
+      atomicAdd(t.counters + 1, 1ull);
+      t.njob[grp] = 0;
+    }
     return;
   }
-  const int64_t grp = (static_cast<int64_t>(layer) * p.batch + b) * p.kv_heads + g;
   // per-entry scratch in global memory (L2): [cap] entry positions | [cap]
   // free slots | [cap] missing positions
   int* s_pos = t.scratch + grp * 3 * t.cap;
@@ -1216,13 +1219,6 @@ __global__ void __launch_bounds__(kTierThreads) tier_update_kernel(const TierPar
   int32_t* pos_of = t.pos_of_slot + grp * t.cap;
   uint8_t* flags = t.slot_flags + grp * t.cap;
   int32_t* es = t.entry_slot + grp * t.cap;
-  // host layer slot: layer mod the host pool's layers (a caller may rotate a subset)
-  const int64_t hl = layer % t.host_layers;
-  const uint16_t* host_k = t.host_k + hl * t.host_layer_stride;
-  const uint16_t* host_v = t.host_v + hl * t.host_layer_stride;
-  const int64_t hot0 = (static_cast<int64_t>(layer) * p.batch + b) * p.kv_heads + g;
-  uint16_t* hot_k = t.hot_k + hot0 * t.cap * D;
-  uint16_t* hot_v = t.hot_v + hot0 * t.cap * D;
   for (int i = tid; i < (n + 31) / 32; i += kTierThreads) need_v[i] = need_k[i] = claimed[i] = 0u;
   if (tid == 0) s_nfree = s_nmiss = 0;
   __syncthreads();
@@ -1241,7 +1237,10 @@ __global__ void __launch_bounds__(kTierThreads) tier_update_kernel(const TierPar
     atomicOr(&need_v[pos >> 5], 1u << (pos & 31));
     if (k) atomicOr(&need_k[pos >> 5], 1u << (pos & 31));
   }
-  if (!__syncthreads_or(changed)) return;
+  if (!__syncthreads_or(changed)) {
+    if (tid == 0) t.njob[grp] = 0;
+    return;
+  }
   // (2) free the slots of positions no longer needed; collect free slots
   for (int sl = tid; sl < t.cap; sl += kTierThreads) {
     int pos = pos_of[sl];
@@ -1297,14 +1296,35 @@ __global__ void __launch_bounds__(kTierThreads) tier_update_kernel(const TierPar
     s_jpos[j] = pos;
   }
   __syncthreads();
-  // (5) the copies over the host link: 16-byte chunks, consecutive threads on
-  // consecutive chunks of a row (V then K: 2 x D*2 contiguous bytes per job),
-  // kTierU chunk loads in flight per thread before their stores
-  const int njob = s_nmiss;
+  // (5) the copies: the next launch (tier_copy_kernel), whose threads keep
+  // more host loads in flight than this kernel's register budget allows
+  if (tid == 0) t.njob[grp] = s_nmiss;
+}
+
+// The host-link copies of tier_update's fetch jobs: 16-byte chunks,
+// consecutive threads on consecutive chunks of a row (V then K: 2 x D*2
+// contiguous bytes per job), kTierU chunk loads in flight per thread before
+// their stores (zero-copy loads of pinned host memory over the link).
+template <int D>
+__global__ void __launch_bounds__(kTierThreads) tier_copy_kernel(const TierParams t) {
+  const AttendParams& p = t.a;
+  const int g = blockIdx.x, b = blockIdx.y, layer = t.layer_begin + blockIdx.z, tid = threadIdx.x;
+  const int64_t grp = (static_cast<int64_t>(layer) * p.batch + b) * p.kv_heads + g;
+  const int njob = t.njob[grp];
+  if (njob == 0) return;
+  const int* s_job = t.scratch + grp * 3 * t.cap + t.cap;        // slot | getv << 30 | getk << 31
+  const int* s_jpos = t.scratch + grp * 3 * t.cap + 2 * t.cap;   // its position
+  // host layer slot: layer mod the host pool's layers (a caller may rotate a subset)
+  const int64_t hl = layer % t.host_layers;
+  const uint16_t* host_k = t.host_k + hl * t.host_layer_stride;
+  const uint16_t* host_v = t.host_v + hl * t.host_layer_stride;
+  const int64_t hot0 = (static_cast<int64_t>(layer) * p.batch + b) * p.kv_heads + g;
+  uint16_t* hot_k = t.hot_k + hot0 * t.cap * D;
+  uint16_t* hot_v = t.hot_v + hot0 * t.cap * D;
   const int32_t* bt = p.block_table + static_cast<int64_t>(b) * p.max_blocks;
   constexpr int CH = D / 8;
 #ifndef SKV_TIER_U
-#define SKV_TIER_U 4
+#define SKV_TIER_U 16
 #endif
   constexpr int kTierU = SKV_TIER_U;
   unsigned long long rows = 0;
@@ -1477,6 +1497,10 @@ cudaError_t launch_tier_update(const TierParams& t, cudaStream_t s) {
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
   cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   k<<<grid, kTierThreads, sm, s>>>(t);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  auto kc = t.a.head_dim == 64 ? tier_copy_kernel<64> : tier_copy_kernel<128>;
+  kc<<<grid, kTierThreads, 0, s>>>(t);
   return cudaGetLastError();
 }
 

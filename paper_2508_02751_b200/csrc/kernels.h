@@ -150,6 +150,7 @@ struct TierParams {
   uint8_t* slot_flags;        // [L][B][H_kv][cap]          bit0 V resident, bit1 K resident
   int32_t* entry_slot;        // [L][B][H_kv][cap]
   int32_t* prev_T;            // [L][B][H_kv] list length of the last refresh (-1: none)
+  int32_t* njob;              // [L][B][H_kv] fetch jobs the update left for the copy launch
   unsigned long long* counters;   // [0] rows fetched (K or V), [1] capacity overflows
   int32_t* scratch;           // [L][B][H_kv][3][cap] per-entry work lists
   int32_t cap, max_seq_len, layer_begin, layer_count;

@@ -665,7 +665,7 @@ int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
 
 namespace {
 struct TierState {
-  size_t sop, pos_of, entry, prev_t, flags, counters, scratch, total;
+  size_t sop, pos_of, entry, prev_t, flags, njob, counters, scratch, total;
 };
 TierState tier_layout(const smallkv_cache* llm, const smallkv_batch* b, int32_t L, int32_t cap) {
   TierState t;
@@ -675,7 +675,8 @@ TierState tier_layout(const smallkv_cache* llm, const smallkv_batch* b, int32_t 
   t.entry = t.pos_of + round256(groups * cap * 4);
   t.prev_t = t.entry + round256(groups * cap * 4);
   t.flags = t.prev_t + round256(groups * 4);
-  t.scratch = t.flags + round256(groups * cap);
+  t.njob = t.flags + round256(groups * cap);
+  t.scratch = t.njob + round256(groups * 4);
   t.counters = t.scratch + round256(groups * cap * 3 * 4);   // last 256 bytes (TieredKV.counters)
   t.total = t.counters + 256;
   return t;
@@ -748,6 +749,7 @@ int smallkv_tier_update(int32_t layer_begin, int32_t layer_count, const smallkv_
   tp.host_layers = host_llm->num_layers;
   tp.scratch = reinterpret_cast<int32_t*>(st + T.scratch);
   tp.prev_T = reinterpret_cast<int32_t*>(st + T.prev_t);
+  tp.njob = reinterpret_cast<int32_t*>(st + T.njob);
   tp.hot_k = hot_k;
   tp.hot_v = hot_v;
   tp.slot_of_pos = reinterpret_cast<int32_t*>(st + T.sop);

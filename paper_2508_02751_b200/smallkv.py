@@ -712,7 +712,8 @@ class DecodeGraph:
         else:   # f2: slm_score, group score, the split (+ to-do), group weights
             H_kv = self.step.llm.num_kv_heads
             sel = 3 + split_launches(self.step.llm_layers * H_kv, B, S)
-        tier = (0 if self.tier is None else len(self.plan) if self.tier.per_layer
-                else (2 if self.tier.plan_buf is not None else 1))   # f4
+        # f4: tier update + copy (per layer, or for all layers), + the tiered plan
+        tier = (0 if self.tier is None else 2 * len(self.plan) if self.tier.per_layer
+                else (3 if self.tier.plan_buf is not None else 2))
         return (1 + sel + tier + (1 if self.step.plan_buf is not None else 0)
                 + len(self.plan))
