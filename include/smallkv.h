@@ -176,6 +176,14 @@ size_t smallkv_select_workspace_size(const smallkv_cache* slm,
  *               (H_s * B * max_seq_len * 4 bytes per layer) within 48 MB, at
  *               least one, so the split re-reads them from L2 (long contexts).
  *               Both streams must be on the current device; capturable.
+ * Launches (all on `stream` / aux_stream, nothing host-synchronous): the
+ * image flags, then per SLM-layer chunk the scoring (K1) and the split (K2).
+ * Rows of up to 12288 tokens (without `acc`) take the register split, long
+ * rows at small batch the cluster split; both hand the rare rows they do not
+ * finish (all scores equal, a boundary bin too full for their pair lists) to a
+ * to-do list in `ws` that a small second launch completes right after, with
+ * the exact radix-select fallback.  The result does not depend on which split
+ * ran.
  * Errors: NULL pointers, H_s % H_kv_s != 0, head_dim not in {64,128},
  * page_size not a power of two in [1,256], misaligned pointers, small ws,
  * non-sm_100 device.
@@ -341,9 +349,11 @@ int smallkv_attend(int32_t llm_layer, int32_t cache_layer, const uint16_t* q,
  *                  entries' slots, and two uint64 counters (rows fetched over
  *                  the host link; capacity overflows).  Initialise once with
  *                  smallkv_tier_init.
- * smallkv_tier_update (LLM layers [layer_begin, layer_begin+layer_count) in one
- * launch — e.g. all of them right after smallkv_select / _select_group, so the
- * refresh of every layer runs ahead of the attends):
+ * smallkv_tier_update (LLM layers [layer_begin, layer_begin+layer_count) in two
+ * launches — the lists' bookkeeping, then the host-link copies — e.g. all of
+ * them right after smallkv_select / _select_group, so the refresh of every
+ * layer runs ahead of the attends; a group whose list is unchanged
+ * since its last refresh only compares it):
  * frees the slots of positions the group's list no longer holds, gives every
  * newly listed position a free slot, and copies from host memory only what is
  * missing — V for every new position, K only where a critical or recent entry
