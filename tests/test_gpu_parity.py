@@ -299,6 +299,44 @@ def test_dense_boundary_bin_refinement(n):
     print("refinement", rep)
 
 
+@pytest.mark.parametrize("n", [8000, 12000])
+def test_register_split_radix_threshold(n):
+    """Rows of 4097..12288 tokens take the 512-thread register split; a
+    boundary bin of more than 48 pairs gets its exact threshold pair by a
+    one-warp radix select instead of per-position rank counting.  Outliers
+    (one row per page x3) squeeze the bulk into fewer of the 256 linear bins so
+    that some boundary bin of some row is that long (checked on the GPU's own
+    logits with the split's bin formula), and the split matches the oracle."""
+    import numpy as np
+    cfg = _cfg(n=n, B=2, budget=(n // 10, n // 64, n // 10))
+    p = synth.make_problem(cfg, seed=19, page_size=64, seq_lens=[n, n - 777])
+    k = p.slm.k.clone()
+    k[:, :, :, 5] *= 3.0
+    p = dataclasses.replace(p, slm=dataclasses.replace(p.slm, k=k)).to("cuda")
+    rep, out_sel, _ = _check(p)
+    logits = out_sel.logits.float().cpu().numpy()
+    longest = 0
+    for j in sorted(set(p.head_map.cpu().tolist())):   # the rows K1 scored
+        for b in range(p.batch):
+            nb = int(p.seq_lens[b])
+            R = min(int(p.n_recent[b]), nb)
+            N = nb - R
+            K = min(int(p.k_crit[b]), N)
+            M = min(int(p.k_marg[b]), N - K)
+            v = logits[j, b, :N].astype(np.float32)
+            if N == 0 or not v.max() > v.min():
+                continue
+            scale = np.float32(255.99) / (np.float32(v.max()) - np.float32(v.min()))
+            bins = np.clip(((v - np.float32(v.min())) * scale).astype(np.int32), 0, 255)
+            cnt = np.bincount(bins, minlength=256)[::-1]
+            cum = np.cumsum(cnt)
+            for r in (K, K + M):
+                if r > 0:
+                    longest = max(longest, int(cnt[np.searchsorted(cum, r)]))
+    assert longest > 48, longest   # the radix-select branch ran for some row
+    print("radix threshold", n, "longest boundary bin", longest, rep)
+
+
 def _head_shard(p, g0, g1):
     from paper_2508_02751_b200 import dist as pdist
     L, H, Hkv = p.cfg.llm.layers, p.cfg.llm.q_heads, p.cfg.llm.kv_heads
