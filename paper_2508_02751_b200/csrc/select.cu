@@ -24,6 +24,10 @@
 // Both lists are then emitted in ascending order by one writing pass with
 // per-warp ballot prefix sums (per-warp counts come from the per-warp
 // histograms and the boundary candidates; the fallback adds a counting pass).
+// Dispatch (launch_select): rows of up to kRegMaxLen tokens without f1's
+// running sums take the register split (select_reg.cuh: 256 x 16, 512 x 16 or
+// 512 x 24 positions, five barriers, rare rows to the to-do launch); longer
+// rows the long split (select_long.cuh).  The generic split below serves f1.
 // Row storage by length: up to kThreads*kRegRow (4096) tokens the row lives in
 // registers (16 consecutive positions per thread, bins packed 4 per register,
 // SIMD byte compares for the candidate and emission passes, output offsets
