@@ -27,6 +27,10 @@ SKV_DEV void cp_async16(uint32_t dst, const void* src, bool pred) {
                "r"(sz)
                : "memory");
 }
+// 16-byte global->shared copy of a row that is certainly present (no zero fill)
+SKV_DEV void cp_async16_full(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+}
 SKV_DEV void cp_async4(uint32_t dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(src) : "memory");
 }

@@ -607,6 +607,24 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
   }
   SKV_T(2);
 
+  // Full tiles (all but a run's last) take a lean issue path: per lane the
+  // shared-memory offsets (row, swizzled 16-B chunk) and the chunk's byte
+  // offset in a row are fixed, so each 16-B copy is one add and one LDGSTS
+  // with no zero-fill predicate.
+  constexpr int HV = D / 64;   // 128-byte halves of a row
+  const uint32_t wst_u32 = smem_u32(wst);
+  const int lr = lane >> 3, lc = lane & 7;
+  uint32_t ldst[HV][2];   // [half][tile group parity]: row lr of the group, swizzled chunk
+  uint32_t lsrc[HV];      // the chunk's byte offset in a row
+#pragma unroll
+  for (int hf = 0; hf < HV; ++hf) {
+    lsrc[hf] = static_cast<uint32_t>((hf * 8 + lc) * 16);
+#pragma unroll
+    for (int par = 0; par < 2; ++par)
+      ldst[hf][par] = static_cast<uint32_t>(lr * ROWB + (((hf * 8 + lc) ^ (par * 4 + lr)) << 4));
+  }
+  const char* kpool_b = reinterpret_cast<const char*>(kpool);
+  const char* vpool_b = reinterpret_cast<const char*>(vpool);
   auto issue = [&](int x, int j, int slot) {
     if (x >= 0) {
       uint8_t* st = wst + (slot % NSTAGE) * SB;
@@ -614,6 +632,34 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
       const int e_b = e_lo + x * kBatch;
       const uint32_t td = BTT(x)[1 + warp + j * kWarps];
       const int e0 = static_cast<int>(td & 0xffffu), cnt = static_cast<int>((td >> 16) & 0xffu);
+      const uint32_t stb = wst_u32 + static_cast<uint32_t>((slot % NSTAGE) * SB);
+      if (!(td >> 24) && cnt == kTile) {
+        // full K+V tile: 16 rows, K half then V half
+#pragma unroll
+        for (int grp = 0; grp < kTile / 4; ++grp) {
+          const size_t rb = static_cast<size_t>(xoff[e0 + grp * 4 + lr]) * 2;
+#pragma unroll
+          for (int hf = 0; hf < HV; ++hf) {
+            const uint32_t d = stb + grp * 4 * ROWB + ldst[hf][grp & 1];
+            cp_async16_full(d, kpool_b + rb + lsrc[hf]);
+            cp_async16_full(d + KV_BYTES, vpool_b + rb + lsrc[hf]);
+          }
+        }
+        cp_async_commit();
+        return;
+      }
+      if ((td >> 24) == 1u && cnt == 2 * kTile) {
+        // full V-only tile: 32 V rows fill the stage
+#pragma unroll
+        for (int grp = 0; grp < 2 * kTile / 4; ++grp) {
+          const size_t rb = static_cast<size_t>(xoff[e0 + grp * 4 + lr]) * 2;
+#pragma unroll
+          for (int hf = 0; hf < HV; ++hf)
+            cp_async16_full(stb + grp * 4 * ROWB + ldst[hf][grp & 1], vpool_b + rb + lsrc[hf]);
+        }
+        cp_async_commit();
+        return;
+      }
       if (td >> 25) {
         // f2 marginal tile: 16 V rows in the V half, their per-head weights
         // [16][8] fp32 (512 B) at the start of the K half
