@@ -858,6 +858,9 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
       const uint8_t* st = wst + ((tbase + i) % NSTAGE) * SB;
       const uint8_t* kb = st;
       const uint8_t* vb = st + KV_BYTES;
+      // (shared-window addresses for ldmatrix: one conversion per tile)
+      const uint32_t kb32 = wst_u32 + static_cast<uint32_t>(((tbase + i) % NSTAGE) * SB);
+      const uint32_t vb32 = kb32 + KV_BYTES;
       const uint32_t td = BTT(x)[1 + warp + i * kWarps];
       const int e0 = static_cast<int>(td & 0xffffu), cnt = static_cast<int>((td >> 16) & 0xffu);
       if (td >> 25) {
@@ -878,7 +881,7 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
           const int r = ((mi >> 1) << 3) + (lane & 7);
           const int ch = 2 * mt + (mi & 1);
           uint32_t a0, a1, a2, a3;
-          ldsm_x4_t(smem_u32(vb + r * ROWB + ((ch ^ (r & 7)) << 4)), a0, a1, a2, a3);
+          ldsm_x4_t(vb32 + r * ROWB + ((ch ^ (r & 7)) << 4), a0, a1, a2, a3);
           mma_bf16(om[mt], a0, a1, a2, a3, bh0_, bh1_);
           mma_bf16(om[mt], a0, a1, a2, a3, bl0_, bl1_);
         }
@@ -922,7 +925,7 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
         const int r = ((mi & 1) << 3) + (lane & 7);
         const int ch = 2 * kk + (mi >> 1);
         uint32_t a0, a1, a2, a3;
-        ldsm_x4(smem_u32(kb + r * ROWB + ((ch ^ (r & 7)) << 4)), a0, a1, a2, a3);
+        ldsm_x4(kb32 + r * ROWB + ((ch ^ (r & 7)) << 4), a0, a1, a2, a3);
         mma_bf16(sc[kk & 3], a0, a1, a2, a3, qa[kk][0], qa[kk][1]);
       }
       float s4[4];
@@ -982,7 +985,7 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
         const int r = ((mi >> 1) << 3) + (lane & 7);
         const int ch = 2 * mt + (mi & 1);
         uint32_t a0, a1, a2, a3;
-        ldsm_x4_t(smem_u32(vb + r * ROWB + ((ch ^ (r & 7)) << 4)), a0, a1, a2, a3);
+        ldsm_x4_t(vb32 + r * ROWB + ((ch ^ (r & 7)) << 4), a0, a1, a2, a3);
         mma_bf16(oc[mt], a0, a1, a2, a3, bh0_, bh1_);
         mma_bf16(oc[mt], a0, a1, a2, a3, bl0_, bl1_);
       }
