@@ -91,7 +91,10 @@ def main():
             torch.cuda.synchronize()
             if cap_scale == 0:
                 assert tier.counters()[1] > 0
-                assert torch.isnan(out).all(), "overflowed groups must read as NaN"
+                # the first two sequences' lists exceed 64 slots (NaN heads); the
+                # one-token sequence fits (finite)
+                assert torch.isnan(out[:2]).all(), "overflowed groups must read as NaN"
+                assert torch.isfinite(out[2]).all(), "a group that fits must be finite"
         print("f4 ok", flush=True)
     if "f3" in which:
         g = torch.Generator(device="cuda").manual_seed(1)
