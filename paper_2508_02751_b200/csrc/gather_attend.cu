@@ -306,39 +306,44 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const AttendParams p
   build_layout(p, layer, b, g, L);
   uint8_t* rec = p.plan + ((static_cast<int64_t>(layer) * p.batch + b) * p.kv_heads + g) *
                               plan_record_bytes(NC);
-  if (threadIdx.x < sizeof(GroupLayout) / 4)
+  // this CTA's ranks [c_lo, c_hi) of the record (blockIdx.z: a group's list
+  // split over many ranks — small batches — is staged by several CTAs)
+  const int per = (NC + static_cast<int>(gridDim.z) - 1) / static_cast<int>(gridDim.z);
+  const int c_lo = static_cast<int>(blockIdx.z) * per, c_hi = min(NC, c_lo + per);
+  if (blockIdx.z == 0 && threadIdx.x < sizeof(GroupLayout) / 4)
     reinterpret_cast<int*>(rec)[threadIdx.x] = reinterpret_cast<const int*>(&L)[threadIdx.x];
   // variant f4: a list longer than the hot pool was skipped by tier_update (its
   // entry slots are stale); the header alone tells the attend to write NaN
-  if (p.entry_slot && L.T > p.hot_cap) return;
+  if ((p.entry_slot && L.T > p.hot_cap) || c_lo >= c_hi) return;
+  const int nr = c_hi - c_lo;
   const int32_t* bt = p.block_table + static_cast<int64_t>(b) * p.max_blocks;
   // flattened over the group's list: entry x belongs to the rank whose
   // byte-balanced share contains it and is staged if it is in that rank's
-  // first batch
+  // first batch (s_split[k] = start of rank c_lo + k)
   __shared__ int s_split[33];
-  if (threadIdx.x <= NC) s_split[threadIdx.x] = split_begin(L, threadIdx.x, NC);
+  if (threadIdx.x <= nr) s_split[threadIdx.x] = split_begin(L, c_lo + threadIdx.x, NC);
   __syncthreads();
   // only the staged entries are visited: flattened over the ranks' first
-  // batches (s_pre[c] = staged entries of ranks < c)
-  // (thread 32: the tile-table builders below are threads < NC <= 32, and
+  // batches (s_pre[k] = staged entries of this CTA's ranks before c_lo + k)
+  // (thread 32: the tile-table builders below are threads < nr <= 32, and
   // their serial builds overlap the staging loop)
   __shared__ int s_pre[33];
   if (threadIdx.x == 32) {
     int a = 0;
-    for (int c = 0; c < NC; ++c) {
-      s_pre[c] = a;
-      a += min(kBatch, s_split[c + 1] - s_split[c]);
+    for (int k = 0; k < nr; ++k) {
+      s_pre[k] = a;
+      a += min(kBatch, s_split[k + 1] - s_split[k]);
     }
-    s_pre[NC] = a;
+    s_pre[nr] = a;
   }
   __syncthreads();
-  if (threadIdx.x < NC) {   // each rank's first-batch tile table
-    const int c = threadIdx.x, e0 = s_split[c];
-    build_tile_table(L, e0, min(kBatch, s_split[c + 1] - e0), p.group_sel != 0,
-                     reinterpret_cast<uint32_t*>(rec + kHdrBytes + c * kTileTableBytes));
+  if (threadIdx.x < nr) {   // each rank's first-batch tile table
+    const int k = threadIdx.x, e0 = s_split[k];
+    build_tile_table(L, e0, min(kBatch, s_split[k + 1] - e0), p.group_sel != 0,
+                     reinterpret_cast<uint32_t*>(rec + kHdrBytes + (c_lo + k) * kTileTableBytes));
   }
   constexpr int U = 1024 / kPlanThreads;
-  const int F = s_pre[NC];
+  const int F = s_pre[nr];
   for (int base = threadIdx.x; base < F; base += U * kPlanThreads) {
     int pos[U], slot_i[U];
     uint32_t mk[U];
@@ -351,11 +356,11 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const AttendParams p
       mk[u] = 0u;
       wt[u] = 0.f;
       if (f >= F) continue;
-      int c = 0;
-      while (c < NC - 1 && f >= s_pre[c + 1]) ++c;
-      const int i = f - s_pre[c];
-      const int x0 = s_split[c] + i;
-      slot_i[u] = c * kBatch + i;
+      int k = 0;
+      while (k < nr - 1 && f >= s_pre[k + 1]) ++k;
+      const int i = f - s_pre[k];
+      const int x0 = s_split[k] + i;
+      slot_i[u] = k * kBatch + i;   // (local rank k: rank c_lo + k)
       const ListEntry le = list_entry(p, L, b, x0, allc);
       pos[u] = le.pos;
       mk[u] = le.mask;
@@ -381,7 +386,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const AttendParams p
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (slot_i[u] < 0) continue;
-      const int c = slot_i[u] / kBatch, i = slot_i[u] % kBatch;
+      const int c = c_lo + slot_i[u] / kBatch, i = slot_i[u] % kBatch;
       uint32_t* slot = reinterpret_cast<uint32_t*>(rec + plan_slot_offset(NC, c));
       slot[i] = ro[u];
       slot[kBatch + i] = mk[u];
@@ -1524,7 +1529,9 @@ int64_t plan_bytes(int32_t n_layers, int32_t batch, int32_t kv_heads, int32_t ma
 
 cudaError_t launch_plan(const AttendParams& p, int32_t n_layers, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.kv_heads, n_layers * p.batch);
+  // a record split over many ranks (small batches) is staged by one CTA per
+  // rank; one CTA per record otherwise
+  cfg.gridDim = dim3(p.kv_heads, n_layers * p.batch, p.max_chunks > 2 ? p.max_chunks : 1);
   cfg.blockDim = dim3(kPlanThreads);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
