@@ -1561,7 +1561,11 @@ cudaError_t launch_tier_update(const TierParams& t, cudaStream_t s) {
 }
 
 cudaError_t launch_attend(const AttendParams& p, cudaStream_t s) {
-  const bool async = p.row_stride > kAsyncStageMinLen;
+  static const int forced = [] {
+    const char* e = getenv("SMALLKV_ATTEND_ASYNC");   // tuning knob: 0 / 1
+    return e ? atoi(e) : -1;
+  }();
+  const bool async = forced >= 0 ? forced != 0 : p.row_stride > kAsyncStageMinLen;
   cudaError_t e = p.head_dim == 64 ? (async ? launch_d<64, true>(p, s) : launch_d<64, false>(p, s))
                                    : (async ? launch_d<128, true>(p, s) : launch_d<128, false>(p, s));
   if (e != cudaSuccess) return e;
