@@ -344,6 +344,43 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const AttendParams p
   }
   constexpr int U = 1024 / kPlanThreads;
   const int F = s_pre[nr];
+  if (nr == 1 && !p.entry_slot) {
+    // one rank (every CTA unless a record's two ranks share it): entries
+    // x0 = split + f, one slot array, no rank search per entry
+    const int x_base = s_split[0];
+    uint32_t* slot = reinterpret_cast<uint32_t*>(rec + plan_slot_offset(NC, c_lo));
+    for (int base = threadIdx.x; base < F; base += U * kPlanThreads) {
+      int pos[U];
+      uint32_t mk[U];
+      float wt[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int f = base + u * kPlanThreads;
+        pos[u] = 0;
+        mk[u] = 0u;
+        wt[u] = 0.f;
+        if (f < F) {
+          const ListEntry le = list_entry(p, L, b, x_base + f, allc);
+          pos[u] = le.pos;
+          mk[u] = le.mask;
+          wt[u] = le.w;
+        }
+      }
+      int page[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) page[u] = base + u * kPlanThreads < F ? __ldg(bt + (pos[u] >> p.ps_shift)) : 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int f = base + u * kPlanThreads;
+        if (f >= F) continue;
+        slot[f] = static_cast<uint32_t>(((static_cast<int64_t>(page[u]) * p.kv_heads + g) * p.page_size +
+                                         (pos[u] & (p.page_size - 1))) * D);
+        slot[kBatch + f] = mk[u];
+        reinterpret_cast<float*>(slot)[2 * kBatch + f] = wt[u];
+      }
+    }
+    return;
+  }
   for (int base = threadIdx.x; base < F; base += U * kPlanThreads) {
     int pos[U], slot_i[U];
     uint32_t mk[U];
