@@ -240,23 +240,25 @@ __global__ void row_flags_kernel(const int32_t* __restrict__ head_map, int32_t n
   }
   __syncthreads();
   for (int i = threadIdx.x; i < n_slm; i += blockDim.x) needed[i] = flags[i];
+  // one warp: the compact ascending list, and layer_off[l] = number of image
+  // rows with flat head < l * heads_per_layer taken from the same running count
   if (threadIdx.x < 32) {
+    const int n_layers = n_slm / heads_per_layer;
     int base = 0;
     for (int i0 = 0; i0 < n_slm; i0 += 32) {
       const int i = i0 + threadIdx.x;
       const bool f = i < n_slm && flags[i];
       const uint32_t bal = __ballot_sync(0xffffffffu, f);
-      if (f) rows[base + __popc(bal & lanemask_lt())] = i;
+      const uint32_t below = __popc(bal & lanemask_lt());
+      if (f) rows[base + below] = i;
+      // lane k: the layer boundary l * heads_per_layer that falls on position i
+      if (i % heads_per_layer == 0 && i / heads_per_layer <= n_layers) layer_off[i / heads_per_layer] = base + below;
       base += __popc(bal);
     }
-    if (threadIdx.x == 0) *n_rows = base;
-  }
-  // layer_off[l] = number of image rows with flat head < l * heads_per_layer
-  const int n_layers = n_slm / heads_per_layer;
-  for (int l = threadIdx.x; l <= n_layers; l += blockDim.x) {
-    int cnt = 0;
-    for (int i = 0; i < l * heads_per_layer; ++i) cnt += flags[i];
-    layer_off[l] = cnt;
+    if (threadIdx.x == 0) {
+      *n_rows = base;
+      layer_off[n_layers] = base;
+    }
   }
 }
 }  // namespace
