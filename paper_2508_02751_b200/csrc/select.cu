@@ -293,15 +293,23 @@ cudaError_t launch_select(const SelectParams& p, int32_t max_rows, int32_t max_s
   cfg.numAttrs = overlap_previous ? 1 : 0;
   cudaError_t e;
   if (max_seq_len <= kRegMaxLen && !p.acc && !reg_generic()) {
-    if (max_seq_len <= 4096) {
-      e = cudaLaunchKernelEx(&cfg, p.log_bins ? select_reg_kernel<true, 256, 16> : select_reg_kernel<false, 256, 16>, p);
-    } else if (max_seq_len <= 8192) {
-      cfg.blockDim = dim3(512);
-      e = cudaLaunchKernelEx(&cfg, p.log_bins ? select_reg_kernel<true, 512, 16> : select_reg_kernel<false, 512, 16>, p);
-    } else {
-      cfg.blockDim = dim3(512);
-      e = cudaLaunchKernelEx(&cfg, p.log_bins ? select_reg_kernel<true, 512, 24> : select_reg_kernel<false, 512, 24>, p);
-    }
+    // dynamic shared memory (512-thread rows): the row as loaded, 4 B per position
+    auto reg = [&](auto kern, int threads, int per) -> cudaError_t {
+      cfg.blockDim = dim3(threads);
+      cfg.dynamicSmemBytes = threads > 256 ? static_cast<size_t>(threads) * per * 4 : 0;
+      if (cfg.dynamicSmemBytes) {
+        const cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(cfg.dynamicSmemBytes));
+        if (r != cudaSuccess) return r;
+      }
+      return cudaLaunchKernelEx(&cfg, kern, p);
+    };
+    if (max_seq_len <= 4096)
+      e = reg(p.log_bins ? select_reg_kernel<true, 256, 16> : select_reg_kernel<false, 256, 16>, 256, 16);
+    else if (max_seq_len <= 8192)
+      e = reg(p.log_bins ? select_reg_kernel<true, 512, 16> : select_reg_kernel<false, 512, 16>, 512, 16);
+    else
+      e = reg(p.log_bins ? select_reg_kernel<true, 512, 24> : select_reg_kernel<false, 512, 24>, 512, 24);
     if (e != cudaSuccess) return e;
     return launch_select_todo(p, s);
   } else if (max_seq_len <= kThreads * kRegRow) {
