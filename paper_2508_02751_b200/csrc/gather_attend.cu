@@ -781,7 +781,39 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
     uint32_t* yoff = BOFF(y);
     uint32_t* ymk = BMK(y);
     float* yw = BW(y);
-    if (sstep == 0) {
+    if (sstep == 0 && L.nrows == 1) {
+      // one SLM row (group-coherent maps): its list bases once per batch
+      const uint32_t yoff32 = smem_u32(yoff), yw32 = smem_u32(yw), spg32 = smem_u32(spg);
+      const int64_t rb0 = static_cast<int64_t>(L.rj[0]) * p.batch + b;
+      const int32_t* cb = p.crit_idx + rb0 * p.max_crit;
+      const int32_t* mb = p.marg_idx + rb0 * p.max_marg;
+      const float* wb = p.marg_w + rb0 * p.max_marg;
+      const int K0 = L.rK[0];
+      const uint32_t hm = L.rhm[0];
+      for (int k = 0; k < kBatch / kThreads; ++k) {
+        const int i = tid + k * kThreads;
+        if (i >= E) break;
+        const int xv = eb + i;
+        if (es) cp_async4(spg32 + 4u * i, es + xv);
+        if (xv < L.Rc) {
+          yoff[i] = static_cast<uint32_t>(L.n - L.Rc + xv);
+          ymk[i] = allc;
+          yw[i] = 0.f;
+          continue;
+        }
+        const int xr = xv - L.Rc;
+        if (xr < K0) {
+          cp_async4(yoff32 + 4u * i, cb + xr);
+          ymk[i] = hm;
+          yw[i] = 0.f;
+        } else {
+          cp_async4(yoff32 + 4u * i, mb + (xr - K0));
+          ymk[i] = hm << 8;
+          if (!gs) cp_async4(yw32 + 4u * i, wb + (xr - K0));
+          else yw[i] = 0.f;
+        }
+      }
+    } else if (sstep == 0) {
       for (int k = 0; k < kBatch / kThreads; ++k) {
         const int i = tid + k * kThreads;
         if (i >= E) break;
@@ -812,11 +844,12 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
         }
       }
     } else if (sstep == 1) {
+      const uint32_t spg32 = smem_u32(spg);
       if (!es)
         for (int k = 0; k < kBatch / kThreads; ++k) {
           const int i = tid + k * kThreads;
           if (i >= E) break;
-          cp_async4(smem_u32(spg + i), btg + (static_cast<int>(yoff[i]) >> p.ps_shift));
+          cp_async4(spg32 + 4u * i, btg + (static_cast<int>(yoff[i]) >> p.ps_shift));
         }
     } else if (sstep == 2) {
       for (int k = 0; k < kBatch / kThreads; ++k) {
