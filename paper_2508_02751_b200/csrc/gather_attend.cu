@@ -353,17 +353,48 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const AttendParams p
       int pos[U];
       uint32_t mk[U];
       float wt[U];
+      if (L.nrows == 1) {
+        // one SLM row (group-coherent maps): list bases hoisted out of the entries
+        const int64_t rb0 = static_cast<int64_t>(L.rj[0]) * p.batch + b;
+        const int32_t* cb = p.crit_idx + rb0 * p.max_crit;
+        const int32_t* mb = p.marg_idx + rb0 * p.max_marg;
+        const float* wb = p.marg_w + rb0 * p.max_marg;
+        const int Rc = L.Rc, K0 = L.rK[0], n0 = L.n - L.Rc;
+        const uint32_t hm = L.rhm[0];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int f = base + u * kPlanThreads;
-        pos[u] = 0;
-        mk[u] = 0u;
-        wt[u] = 0.f;
-        if (f < F) {
-          const ListEntry le = list_entry(p, L, b, x_base + f, allc);
-          pos[u] = le.pos;
-          mk[u] = le.mask;
-          wt[u] = le.w;
+        for (int u = 0; u < U; ++u) {
+          const int f = base + u * kPlanThreads;
+          const int x = x_base + f;
+          pos[u] = 0;
+          mk[u] = 0u;
+          wt[u] = 0.f;
+          if (f < F) {
+            if (x < Rc) {
+              pos[u] = n0 + x;
+              mk[u] = allc;
+            } else if (x - Rc < K0) {
+              pos[u] = __ldg(cb + (x - Rc));
+              mk[u] = hm;
+            } else {
+              pos[u] = __ldg(mb + (x - Rc - K0));
+              mk[u] = hm << 8;
+              wt[u] = p.group_sel ? 0.f : __ldg(wb + (x - Rc - K0));
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int f = base + u * kPlanThreads;
+          pos[u] = 0;
+          mk[u] = 0u;
+          wt[u] = 0.f;
+          if (f < F) {
+            const ListEntry le = list_entry(p, L, b, x_base + f, allc);
+            pos[u] = le.pos;
+            mk[u] = le.mask;
+            wt[u] = le.w;
+          }
         }
       }
       int page[U];
