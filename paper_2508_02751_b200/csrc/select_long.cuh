@@ -146,6 +146,7 @@ __device__ __forceinline__ void select_row_long(const SelectParams& p, const int
   __shared__ int s_i[16];            // [0,1] cell count, [2,3] bin, [4,5] above, [6,7] cand count
   __shared__ uint32_t s_u[4];        // [0,1] radix prefix, [2,3] threshold key
   __shared__ int s_ti[2], s_rem[2];
+  __shared__ float s_thr[2][2];      // target t's cell [lo, hi) in score order
 
   const int n = p.seq_lens[b];
   const int64_t rb = static_cast<int64_t>(j) * p.batch + b;
@@ -281,14 +282,21 @@ __device__ __forceinline__ void select_row_long(const SelectParams& p, const int
   const float scale1 = (static_cast<float>(kLongBins) - 0.01f) / (bv(vhi) - blo);
   const bool all_equal = !(vhi > vlo);
   const bool bad_range = !all_equal && !isfinite(scale1);
-  constexpr float kTop = static_cast<float>(kLongBins) - 0.5f;
-  auto bin1 = [&](float v) { return static_cast<int>(fminf(fmaxf((bv(v) - blo) * scale1, 0.f), kTop)); };
+  // bin = min(trunc_u32(fma(v, scale, off)), top): one FFMA, a saturating
+  // conversion (negatives and NaN -> 0) and a min.  Only monotonicity in the
+  // score matters (the thresholds are then found exactly), not where the bin
+  // edges fall.
+  const float off1 = -blo * scale1;
+  auto bin1 = [&](float v) {
+    return static_cast<int>(min(__float2uint_rz(fmaf(bv(v), scale1, off1)), static_cast<unsigned>(kLongBins - 1)));
+  };
   // level-2 sub-bins inside boundary bin B of target t
   float lo2[2] = {0.f, 0.f}, sc2[2] = {0.f, 0.f};
   int b1[2] = {-1, -1}, b2[2] = {-1, -1};
   bool lv2[2] = {false, false};
   auto bin2 = [&](float v, int t) {
-    return static_cast<int>(fminf(fmaxf((bv(v) - lo2[t]) * sc2[t], 0.f), kTop));
+    return static_cast<int>(min(__float2uint_rz(fmaf(bv(v), sc2[t], -lo2[t] * sc2[t])),
+                                static_cast<unsigned>(kLongBins - 1)));
   };
   // target t's cell: -1 below (worse), 0 inside, +1 above (better)
   auto where = [&](float v, int t) -> int {
@@ -311,7 +319,22 @@ __device__ __forceinline__ void select_row_long(const SelectParams& p, const int
     __syncthreads();
     const int bsrc = t_src >= 0 ? b1[t_src] : -1;
     const uint32_t hist_s = smem_u32(hist);
-    for (int base = 4 * tid; base < N; base += 4 * kLongThreads * kLongU) {
+    int base = 4 * tid;
+    if (bsrc < 0) {
+      // level 1, whole chunks: no bound or cell test per position
+      for (; base + 4 * kLongThreads * (kLongU - 1) + 3 < N; base += 4 * kLongThreads * kLongU) {
+        float4 v4[kLongU];
+        loadU(score, base, 4 * kLongThreads, N, v4);
+#pragma unroll
+        for (int u = 0; u < kLongU; ++u) {
+          const float vv[4] = {v4[u].x, v4[u].y, v4[u].z, v4[u].w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            asm volatile("red.shared.add.u32 [%0], 1;\n" ::"r"(hist_s + 4u * static_cast<uint32_t>(fn(vv[k]))) : "memory");
+        }
+      }
+    }
+    for (; base < N; base += 4 * kLongThreads * kLongU) {
       float4 v4[kLongU];
       loadU(score, base, 4 * kLongThreads, N, v4);
 #pragma unroll
@@ -476,13 +499,70 @@ __device__ __forceinline__ void select_row_long(const SelectParams& p, const int
     }
   } else if (!all_equal) {
     // ---- candidates of the boundary cells, per-warp counts above them
-    if (tid < 2) s_i[6 + tid] = 0;
+    // `where` is monotone in the score, so target t's cell is one interval
+    // [lo_t, hi_t) of floats and "above" is v >= hi_t: warp t finds both
+    // bounds exactly by a 32-way search over the order-preserving float keys
+    // (7 rounds each); a bound no float reaches is NaN (every compare false).
+    if (warp < 2) {
+      const int t = warp;
+      if (lane == 0) s_i[6 + t] = 0;
+      float bnd[2] = {__int_as_float(0x7fc00000), __int_as_float(0x7fc00000)};
+      if (t == 1 || rA > 0) {
+        auto from_key = [](uint32_t k) {
+          return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+        };
+#pragma unroll 1
+        for (int e = 0; e < 2; ++e) {
+          // smallest float f with where(f, t) >= e (e = 0: cell or above; 1: above)
+          auto pred = [&](uint32_t k) { return where(from_key(k), t) >= e; };
+          constexpr uint32_t kNegInf = 0x007fffffu, kPosInf = 0xff800000u;   // keys of -inf, +inf
+          if (!__any_sync(0xffffffffu, lane == 0 && pred(kPosInf))) continue;
+          long long L = static_cast<long long>(kNegInf) - 1, H = kPosInf;   // pred(L) false, pred(H) true
+          while (H - L > 1) {
+            const long long step = (H - L + 31) / 32;
+            const long long k = min(L + step * (lane + 1), H);
+            const uint32_t bal = __ballot_sync(0xffffffffu, pred(static_cast<uint32_t>(k)));
+            const int f = __ffs(bal) - 1;   // lane 31 holds H: some lane is true
+            const long long nH = min(L + step * (f + 1), H);
+            L = f == 0 ? L : L + step * f;
+            H = nH;
+          }
+          bnd[e] = from_key(static_cast<uint32_t>(H));
+        }
+      }
+      if (lane == 0) {
+        s_thr[t][0] = bnd[0];
+        s_thr[t][1] = bnd[1];
+      }
+    }
     __syncthreads();
     int ab[2] = {0, 0};
-    // targets' level-1 bins (rA == 0: target 0 never matches, bin above all)
-    const int c0 = rA > 0 ? b1[0] : kLongBins, c1 = b1[1];
-    const bool any2 = lv2[0] || lv2[1];
-    for (int base0 = s0; base0 < s1; base0 += 128 * kLongU) {
+    const float lo0 = s_thr[0][0], hi0 = s_thr[0][1], lo1 = s_thr[1][0], hi1 = s_thr[1][1];
+    auto cand_one = [&](float v, int i) {
+      const bool a0 = v >= hi0, a1 = v >= hi1;
+      ab[0] += a0 ? 1 : 0;
+      ab[1] += a1 ? 1 : 0;
+      const bool in0 = v >= lo0 && !a0, in1 = v >= lo1 && !a1;
+      if (in0 || in1) {   // rare: a boundary cell
+        const unsigned long long key = (static_cast<unsigned long long>(desc_key(v)) << 32) | static_cast<uint32_t>(i);
+        if (in0) cand[0][atomicAdd(&s_i[6], 1)] = key;
+        if (in1) cand[1][atomicAdd(&s_i[7], 1)] = key;
+      }
+    };
+    int base0 = s0;
+    for (; base0 + 128 * kLongU <= s1; base0 += 128 * kLongU) {   // whole chunks
+      float4 v4[kLongU];
+      loadU(score, base0 + 4 * lane, 128, s1, v4);
+#pragma unroll
+      for (int u = 0; u < kLongU; ++u) {
+        const int i = base0 + 128 * u + 4 * lane;
+        cand_one(v4[u].x, i);
+        cand_one(v4[u].y, i + 1);
+        cand_one(v4[u].z, i + 2);
+        cand_one(v4[u].w, i + 3);
+      }
+    }
+    for (; base0 < s1; base0 += 128 * kLongU) {
       float4 v4[kLongU];
       loadU(score, base0 + 4 * lane, 128, s1, v4);
 #pragma unroll
@@ -490,30 +570,8 @@ __device__ __forceinline__ void select_row_long(const SelectParams& p, const int
         const int i = base0 + 128 * u + 4 * lane;
         const float vv[4] = {v4[u].x, v4[u].y, v4[u].z, v4[u].w};
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const bool valid = i + k < s1;
-          const int x = bin1(vv[k]);
-          ab[0] += (valid && x > c0) ? 1 : 0;
-          ab[1] += (valid && x > c1) ? 1 : 0;
-          if (valid && (x == c0 || x == c1)) {   // rare: a boundary bin
-#pragma unroll
-            for (int t = 0; t < 2; ++t) {
-              if (x != (t == 0 ? c0 : c1)) continue;
-              int w = 0;
-              if (any2 && lv2[t]) {
-                const int y = bin2(vv[k], t);
-                w = y == b2[t] ? 0 : (y > b2[t] ? 1 : -1);
-              }
-              if (w > 0) {
-                ++ab[t];
-              } else if (w == 0) {
-                const int slot = atomicAdd(&s_i[6 + t], 1);
-                cand[t][slot] = (static_cast<unsigned long long>(desc_key(vv[k])) << 32) |
-                                static_cast<uint32_t>(i + k);
-              }
-            }
-          }
-        }
+        for (int k = 0; k < 4; ++k)
+          if (i + k < s1) cand_one(vv[k], i + k);
       }
     }
     ab[0] = warp_sum_i(ab[0]);
