@@ -77,6 +77,16 @@ __global__ void __launch_bounds__(kThreads, kRegE > 0 ? SKV_SELECT_REG_MINB : (k
     select_row<kInSmem, kLogBins, kRegE>(p, p.rows[r], blockIdx.x);
 }
 
+// Rows longer than kSmemCap: the long split (select_long.cuh), kT threads per CTA.
+template <bool kLogBins, int kT>
+__global__ void __launch_bounds__(kT, kT >= 1024 ? 1 : (kT >= 512 ? 2 : 4)) select_long_kernel(const SelectParams p) {
+  griddep_launch_dependents();
+  griddep_wait();
+  const int r = p.layer_off[p.layer_begin] + static_cast<int>(blockIdx.y);
+  if (r >= p.layer_off[p.layer_end]) return;
+  select_row_long<kLogBins, kT>(p, p.rows[r], blockIdx.x);
+}
+
 #ifndef SKV_SELECT_REGK_MINB
 #define SKV_SELECT_REGK_MINB 5
 #endif
@@ -321,7 +331,21 @@ cudaError_t launch_select(const SelectParams& p, int32_t max_rows, int32_t max_s
                          static_cast<int>(cfg.dynamicSmemBytes));
     e = cudaLaunchKernelEx(&cfg, k, p);
   } else {
-    e = cudaLaunchKernelEx(&cfg, p.log_bins ? select_kernel<false, true, 0> : select_kernel<false, false, 0>, p);
+    static const int long_cta = [] {
+      const char* v = getenv("SMALLKV_LONG_CTA");   // tuning knob: 256, 512 or 1024
+      // 256: measured fastest at configs 3 and 4 (1024 threads, one CTA per
+      // SM, reads the row from DRAM once — 4.0 -> 1.46 GB at config 4 — but
+      // the CTA's serial phases then idle the SM: 1.13 vs 0.97 ms)
+      const int t = v ? atoi(v) : 256;
+      return (t == 512 || t == 1024) ? t : 256;
+    }();
+    cfg.blockDim = dim3(long_cta);
+    if (long_cta == 256)
+      e = cudaLaunchKernelEx(&cfg, p.log_bins ? select_long_kernel<true, 256> : select_long_kernel<false, 256>, p);
+    else if (long_cta == 512)
+      e = cudaLaunchKernelEx(&cfg, p.log_bins ? select_long_kernel<true, 512> : select_long_kernel<false, 512>, p);
+    else
+      e = cudaLaunchKernelEx(&cfg, p.log_bins ? select_long_kernel<true, 1024> : select_long_kernel<false, 1024>, p);
   }
   if (e != cudaSuccess) return e;
   return cudaGetLastError();

@@ -136,13 +136,16 @@ __device__ __forceinline__ void long_emit(const float* score, const float* row, 
   }
 }
 
-template <bool kLogBins>
+// kT threads per CTA: 256 (several CTAs per SM) or 1024 (one per SM: only
+// 148 rows live, so at 128K tokens passes 2 and 3 find the row in L2)
+template <bool kLogBins, int kT = kLongThreads>
 __device__ __forceinline__ void select_row_long(const SelectParams& p, const int j, const int b) {
+  constexpr int kW = kT / 32;
   __shared__ uint32_t hist[kLongBins];
   __shared__ unsigned long long cand[2][kLongCap];
-  __shared__ float red[4][kLongWarps];
-  __shared__ int wab[kLongWarps][2];
-  __shared__ int wsel[kLongWarps][2];
+  __shared__ float red[4][kW];
+  __shared__ int wab[kW][2];
+  __shared__ int wsel[kW][2];
   __shared__ int s_i[16];            // [0,1] cell count, [2,3] bin, [4,5] above, [6,7] cand count
   __shared__ uint32_t s_u[4];        // [0,1] radix prefix, [2,3] threshold key
   __shared__ int s_ti[2], s_rem[2];
@@ -227,16 +230,16 @@ __device__ __forceinline__ void select_row_long(const SelectParams& p, const int
   if (accrow) {
     // f1: acc[v] += a'_v for v < n (in place), rank on acc; range over [0, N)
     float lo = FLT_MAX, hi = -FLT_MAX;
-    for (int base = 4 * tid; base < n; base += 4 * kLongThreads * kLongU) {
+    for (int base = 4 * tid; base < n; base += 4 * kT * kLongU) {
       float4 a[kLongU], s[kLongU];
 #pragma unroll
       for (int u = 0; u < kLongU; ++u) {
-        a[u] = load4(accrow, base + 4 * kLongThreads * u, n);
-        s[u] = load4(row, base + 4 * kLongThreads * u, n);
+        a[u] = load4(accrow, base + 4 * kT * u, n);
+        s[u] = load4(row, base + 4 * kT * u, n);
       }
 #pragma unroll
       for (int u = 0; u < kLongU; ++u) {
-        const int i = base + 4 * kLongThreads * u;
+        const int i = base + 4 * kT * u;
         float av[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
         const float sv[4] = {s[u].x, s[u].y, s[u].z, s[u].w};
 #pragma unroll
@@ -261,7 +264,7 @@ __device__ __forceinline__ void select_row_long(const SelectParams& p, const int
     __syncthreads();
     vlo = FLT_MAX;
     vhi = -FLT_MAX;
-    for (int w = 0; w < kLongWarps; ++w) {
+    for (int w = 0; w < kW; ++w) {
       vlo = fminf(vlo, red[2][w]);
       vhi = fmaxf(vhi, red[3][w]);
     }
@@ -272,7 +275,7 @@ __device__ __forceinline__ void select_row_long(const SelectParams& p, const int
 
   // per-warp contiguous segments of [0, N) (index order = output order),
   // multiples of 128 positions (4 consecutive per lane per step)
-  const int seg = ((N + kLongWarps * 128 - 1) / (kLongWarps * 128)) * 128;
+  const int seg = ((N + kW * 128 - 1) / (kW * 128)) * 128;
   const int s0 = min(N, warp * seg), s1 = min(N, s0 + seg);
 
   auto bv = [&](float v) {
@@ -315,16 +318,16 @@ __device__ __forceinline__ void select_row_long(const SelectParams& p, const int
   // all) under bin function `fn`, then the boundary bin of each target in
   // `tmask` from the top: s_i[t] count in the bin, s_i[2+t] bin, s_i[4+t] above
   auto level = [&](int t_src, auto fn, uint32_t tmask, const int* want) {
-    for (int i = tid; i < kLongBins; i += kLongThreads) hist[i] = 0u;
+    for (int i = tid; i < kLongBins; i += kT) hist[i] = 0u;
     __syncthreads();
     const int bsrc = t_src >= 0 ? b1[t_src] : -1;
     const uint32_t hist_s = smem_u32(hist);
     int base = 4 * tid;
     if (bsrc < 0) {
       // level 1, whole chunks: no bound or cell test per position
-      for (; base + 4 * kLongThreads * (kLongU - 1) + 3 < N; base += 4 * kLongThreads * kLongU) {
+      for (; base + 4 * kT * (kLongU - 1) + 3 < N; base += 4 * kT * kLongU) {
         float4 v4[kLongU];
-        loadU(score, base, 4 * kLongThreads, N, v4);
+        loadU(score, base, 4 * kT, N, v4);
 #pragma unroll
         for (int u = 0; u < kLongU; ++u) {
           const float vv[4] = {v4[u].x, v4[u].y, v4[u].z, v4[u].w};
@@ -334,12 +337,12 @@ __device__ __forceinline__ void select_row_long(const SelectParams& p, const int
         }
       }
     }
-    for (; base < N; base += 4 * kLongThreads * kLongU) {
+    for (; base < N; base += 4 * kT * kLongU) {
       float4 v4[kLongU];
-      loadU(score, base, 4 * kLongThreads, N, v4);
+      loadU(score, base, 4 * kT, N, v4);
 #pragma unroll
       for (int u = 0; u < kLongU; ++u) {
-        const int i = base + 4 * kLongThreads * u;
+        const int i = base + 4 * kT * u;
         const float vv[4] = {v4[u].x, v4[u].y, v4[u].z, v4[u].w};
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -417,9 +420,9 @@ __device__ __forceinline__ void select_row_long(const SelectParams& p, const int
     for (int pass = 0; pass < 4; ++pass) {
       const int shift = 24 - 8 * pass;
       const uint32_t hmask = pass == 0 ? 0u : (0xffffffffu << (shift + 8));
-      for (int i = tid; i < 512; i += kLongThreads) rh[i >> 8][i & 255] = 0;
+      for (int i = tid; i < 512; i += kT) rh[i >> 8][i & 255] = 0;
       __syncthreads();
-      for (int base = warp * 32; base < N; base += kLongThreads) {
+      for (int base = warp * 32; base < N; base += kT) {
         const int i = base + lane;
         const bool valid = i < N;
         const uint32_t k = valid ? desc_key(score[i]) : 0u;
@@ -586,7 +589,7 @@ __device__ __forceinline__ void select_row_long(const SelectParams& p, const int
       if (t == 0 && rA == 0) continue;
       const int nc = s_i[6 + t];
       const int want = (t == 0 ? rA : rB) - above_g[t] - 1;
-      for (int c = tid; c < nc; c += kLongThreads) {
+      for (int c = tid; c < nc; c += kT) {
         const unsigned long long v = cand[t][c];
         int rank = 0;
         for (int d = 0; d < nc; ++d) rank += cand[t][d] < v ? 1 : 0;
@@ -633,13 +636,13 @@ __device__ __forceinline__ void select_row_long(const SelectParams& p, const int
       mbase += wab[w][1] - wab[w][0];
     }
   } else {
-    if (tid < 2 * kLongWarps) (&wsel[0][0])[tid] = 0;
+    if (tid < 2 * kW) (&wsel[0][0])[tid] = 0;
     __syncthreads();
     for (int t = 0; t < 2; ++t) {
       if (t == 0 && rA == 0) continue;
       const unsigned long long thr = (static_cast<unsigned long long>(TK[t]) << 32) | static_cast<uint32_t>(TI[t]);
       const int nc = s_i[6 + t];
-      for (int c = tid; c < nc; c += kLongThreads) {
+      for (int c = tid; c < nc; c += kT) {
         const unsigned long long v = cand[t][c];
         if (v <= thr) atomicAdd(&wsel[static_cast<int>(v & 0xffffffffu) / seg][t], 1);
       }

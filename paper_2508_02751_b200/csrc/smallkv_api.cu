@@ -317,8 +317,9 @@ cudaError_t launch_split(const skv::SelectParams& se, int32_t max_rows, int32_t 
   // measured on B200 (config 4, 131072 tokens): with >= 1024 (row, sequence)
   // pairs one CTA per pair fills the GPU (B = 8: 3.13 ms vs 3.29 with clusters
   // of 4); with fewer, clusters of 2 halve the split (B = 1: 0.58 vs 1.05 ms)
+  static const bool forced = getenv("SMALLKV_SPLIT_CLUSTER") != nullptr;   // tuning knob (select_cluster.cu)
   const int64_t pairs = static_cast<int64_t>(max_rows) * se.batch;
-  if (!se.acc && max_seq_len > skv::kClusterSplitMinLen && pairs < 1024)
+  if (!se.acc && max_seq_len > skv::kClusterSplitMinLen && (pairs < 1024 || forced))
     return skv::launch_select_cluster(se, max_rows, pairs < 256 ? 4 : 2, s);
   return skv::launch_select(se, max_rows, max_seq_len, overlap_previous, s);
 }
