@@ -132,12 +132,13 @@ def test_duplicate_keys_exact_ties():
     _check(p)
 
 
-@pytest.mark.parametrize("n", [4000, 8000, 12000])
+@pytest.mark.parametrize("n", [4000, 8000, 12000, 14000, 20000])
 def test_massive_ties_radix_fallback(n):
     """Two distinct K' rows (alternating by page): two distinct logits, so the
     boundary bins (and their sub-bins) hold thousands of equal keys and K2 takes
-    the exact radix select + index tie-break.  n covers the three K2 variants
-    (register rows, shared-memory rows, global rows)."""
+    the exact radix select + index tie-break.  n covers the K2 variants at
+    B = 1: register rows (256 x 16, 512 x 16, 512 x 24), the long split
+    (14000) and the cluster split (20000 > 16384 with < 1024 pairs)."""
     cfg = _cfg(n=n, B=1, budget=(n // 10, 20, n // 10))
     p = synth.make_problem(cfg, seed=21, page_size=256, seq_lens=[n])
     k = p.slm.k.clone()
@@ -283,7 +284,7 @@ def test_two_valued_logits_radix_fallback():
     _check(p)
 
 
-@pytest.mark.parametrize("n", [32000, 4000])
+@pytest.mark.parametrize("n", [32000, 14000, 4000])
 def test_dense_boundary_bin_refinement(n):
     """A few outlier logits stretch the value-linear histogram so that the
     boundary bin holds thousands of positions: K2 refines inside that bin
@@ -806,3 +807,24 @@ def test_decode_graph_host_io_tiered():
     g.stream.synchronize()
     for l in range(L):
         assert torch.equal(h_out[l], refs[l].cpu()), l
+
+
+@pytest.mark.parametrize("cta", ["512", "1024"])
+def test_long_split_cta_sizes(cta):
+    """The long split's CTA size is a launch-time knob (SMALLKV_LONG_CTA, read
+    once per process; 256 by default): rerun the long-row cases — ties with the
+    radix fallback, the sub-bin refinement, two ragged sequences — in a fresh
+    process at 512 and 1024 threads per CTA."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sel = ("test_massive_ties_radix_fallback and 14000 or test_dense_boundary_bin_refinement and 14000"
+           " or test_select_row_storage_variants and 14000")
+    env = dict(os.environ, SMALLKV_LONG_CTA=cta)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", sel,
+                        os.path.join(root, "tests", "test_gpu_parity.py")],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "3 passed" in r.stdout, r.stdout[-2000:]
+
