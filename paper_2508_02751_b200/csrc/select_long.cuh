@@ -553,16 +553,43 @@ __device__ __forceinline__ void select_row_long(const SelectParams& p, const int
       }
     };
     int base0 = s0;
+    static_assert(kLongU * 4 <= 32, "one mask bit per position of a chunk");
     for (; base0 + 128 * kLongU <= s1; base0 += 128 * kLongU) {   // whole chunks
       float4 v4[kLongU];
       loadU(score, base0 + 4 * lane, 128, s1, v4);
+      // per position: four compares and three predicated bit sets (above A,
+      // above B, boundary cell); the counts are two popcounts per chunk and
+      // the rare boundary positions are inserted after the chunk
+      uint32_t m0 = 0u, m1 = 0u, mr = 0u;
 #pragma unroll
       for (int u = 0; u < kLongU; ++u) {
-        const int i = base0 + 128 * u + 4 * lane;
-        cand_one(v4[u].x, i);
-        cand_one(v4[u].y, i + 1);
-        cand_one(v4[u].z, i + 2);
-        cand_one(v4[u].w, i + 3);
+        const float vv[4] = {v4[u].x, v4[u].y, v4[u].z, v4[u].w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float v = vv[k];
+          const bool a0 = v >= hi0, a1 = v >= hi1;
+          const uint32_t bit = 1u << (4 * u + k);
+          if (a0) m0 |= bit;
+          if (a1) m1 |= bit;
+          if ((v >= lo0 && !a0) || (v >= lo1 && !a1)) mr |= bit;
+        }
+      }
+      ab[0] += __popc(m0);
+      ab[1] += __popc(m1);
+      while (mr) {
+        const int e = __ffs(mr) - 1;
+        mr &= mr - 1u;
+        float v = 0.f;   // the value back out of this lane's registers
+#pragma unroll
+        for (int u = 0; u < kLongU; ++u) {
+          const float w = (e & 3) == 0 ? v4[u].x : (e & 3) == 1 ? v4[u].y : (e & 3) == 2 ? v4[u].z : v4[u].w;
+          v = (e >> 2) == u ? w : v;
+        }
+        const int i = base0 + 128 * (e >> 2) + 4 * lane + (e & 3);
+        const bool in0 = v >= lo0 && !(v >= hi0), in1 = v >= lo1 && !(v >= hi1);
+        const unsigned long long key = (static_cast<unsigned long long>(desc_key(v)) << 32) | static_cast<uint32_t>(i);
+        if (in0) cand[0][atomicAdd(&s_i[6], 1)] = key;
+        if (in1) cand[1][atomicAdd(&s_i[7], 1)] = key;
       }
     }
     for (; base0 < s1; base0 += 128 * kLongU) {
