@@ -92,14 +92,23 @@ __device__ __forceinline__ void long_emit(const float* score, const float* row, 
     }
     // (score, i) <= (X, I): for a whole step with i <= I that is score >= X,
     // with i > I score > X; only the one step holding I compares both
+    // Whole steps take the sign of a difference: v >= X iff v - X has a clear
+    // sign bit (IEEE without flush-to-zero: distinct floats never subtract to
+    // zero, equal ones give +0; inf - inf is the canonical, positive NaN), and
+    // v > X iff X - v has it set; one FADD and one funnel shift per position.
     auto sel16 = [&](float X, int I) {
       uint32_t r = 0u;
+      if (X != X) return 0u;   // no target (NaN threshold): nothing selected
       if (p0 + 15 <= I) {
+        uint32_t sg = 0u;
 #pragma unroll
-        for (int e = 0; e < 16; ++e) r |= static_cast<uint32_t>(v[e] >= X) << e;
+        for (int e = 15; e >= 0; --e) sg = __funnelshift_l(__float_as_uint(v[e] - X), sg, 1);
+        r = ~sg & 0xffffu;
       } else if (p0 > I) {
+        uint32_t sg = 0u;
 #pragma unroll
-        for (int e = 0; e < 16; ++e) r |= static_cast<uint32_t>(v[e] > X) << e;
+        for (int e = 15; e >= 0; --e) sg = __funnelshift_l(__float_as_uint(X - v[e]), sg, 1);
+        r = sg & 0xffffu;
       } else {
 #pragma unroll
         for (int e = 0; e < 16; ++e)
