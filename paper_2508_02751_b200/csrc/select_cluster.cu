@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(kCT, 3) select_cluster_kernel(const SelectPara
   __shared__ float sred[4];
   __shared__ int s_i[8];
   __shared__ int wab[kCW][2], wsel[kCW][2], s_pre[kCW][2];
+  __shared__ float s_bnd[2][2];   // target t's boundary bin as a float interval [lo, hi)
   __shared__ int s_cnt[2][16], s_abv[2][16], s_off[2][17];
 
   griddep_launch_dependents();
@@ -254,13 +255,66 @@ __global__ void __launch_bounds__(kCT, 3) select_cluster_kernel(const SelectPara
     return;
   }
 
-  // ---- 3. candidates of the boundary bins, per-warp counts above them
-  if (tid < 2) cs.ncand[tid] = 0;
+  // ---- 3. candidates of the boundary bins, per-warp counts above them.
+  // bin1 is monotone in the score, so target t's bin is one float interval
+  // [lo, hi): warp t finds both bounds exactly (select_long.cuh), and a
+  // position is then decided by compares (b1 = kCBins: no target, NaN bounds).
+  if (warp < 2) {
+    const int t = warp, bt = b1[t];
+    float lo = __int_as_float(0x7fc00000), hi = lo;
+    if (bt < kCBins) {
+      lo = warp_first_float([&](float f) { return bin1(f) >= bt; }, lane);
+      hi = warp_first_float([&](float f) { return bin1(f) > bt; }, lane);
+    }
+    if (lane == 0) {
+      s_bnd[t][0] = lo;
+      s_bnd[t][1] = hi;
+      cs.ncand[t] = 0;
+    }
+  }
   __syncthreads();
   {
     int ab[2] = {0, 0};
-    const int c0 = b1[0], c1 = b1[1];
-    for (int base0 = s0; base0 < s1; base0 += 128 * kCU) {
+    const float lo0 = s_bnd[0][0], hi0 = s_bnd[0][1], lo1 = s_bnd[1][0], hi1 = s_bnd[1][1];
+    auto insert = [&](float v, int i) {
+      const bool in0 = v >= lo0 && !(v >= hi0), in1 = v >= lo1 && !(v >= hi1);
+      const unsigned long long kv = (static_cast<unsigned long long>(desc_key(v)) << 32) | static_cast<uint32_t>(i);
+      if (in0) cown[0][atomicAdd(&cs.ncand[0], 1)] = kv;
+      if (in1) cown[1][atomicAdd(&cs.ncand[1], 1)] = kv;
+    };
+    int base0 = s0;
+    for (; base0 + 128 * kCU <= s1; base0 += 128 * kCU) {   // whole chunks: masks, as in select_long.cuh
+      float4 v4[kCU];
+      long_loadU<kCU>(row, base0 + 4 * lane, 128, s1, al, v4);
+      uint32_t m0 = 0u, m1 = 0u, mr = 0u;
+#pragma unroll
+      for (int u = 0; u < kCU; ++u) {
+        const float vv[4] = {v4[u].x, v4[u].y, v4[u].z, v4[u].w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float v = vv[k];
+          const bool a0 = v >= hi0, a1 = v >= hi1;
+          const uint32_t bit = 1u << (4 * u + k);
+          if (a0) m0 |= bit;
+          if (a1) m1 |= bit;
+          if ((v >= lo0 && !a0) || (v >= lo1 && !a1)) mr |= bit;
+        }
+      }
+      ab[0] += __popc(m0);
+      ab[1] += __popc(m1);
+      while (mr) {
+        const int e = __ffs(mr) - 1;
+        mr &= mr - 1u;
+        float v = 0.f;
+#pragma unroll
+        for (int u = 0; u < kCU; ++u) {
+          const float w = (e & 3) == 0 ? v4[u].x : (e & 3) == 1 ? v4[u].y : (e & 3) == 2 ? v4[u].z : v4[u].w;
+          v = (e >> 2) == u ? w : v;
+        }
+        insert(v, base0 + 128 * (e >> 2) + 4 * lane + (e & 3));
+      }
+    }
+    for (; base0 < s1; base0 += 128 * kCU) {
       float4 v4[kCU];
       long_loadU<kCU>(row, base0 + 4 * lane, 128, s1, al, v4);
 #pragma unroll
@@ -269,16 +323,10 @@ __global__ void __launch_bounds__(kCT, 3) select_cluster_kernel(const SelectPara
         const float vv[4] = {v4[u].x, v4[u].y, v4[u].z, v4[u].w};
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const bool valid = i + k < s1;
-          const int x = bin1(vv[k]);
-          ab[0] += (valid && x > c0) ? 1 : 0;
-          ab[1] += (valid && x > c1) ? 1 : 0;
-          if (valid && (x == c0 || x == c1)) {
-            const unsigned long long kv =
-                (static_cast<unsigned long long>(desc_key(vv[k])) << 32) | static_cast<uint32_t>(i + k);
-            if (x == c0) cown[0][atomicAdd(&cs.ncand[0], 1)] = kv;
-            if (x == c1) cown[1][atomicAdd(&cs.ncand[1], 1)] = kv;
-          }
+          if (i + k >= s1) continue;
+          ab[0] += vv[k] >= hi0 ? 1 : 0;
+          ab[1] += vv[k] >= hi1 ? 1 : 0;
+          insert(vv[k], i + k);
         }
       }
     }

@@ -42,6 +42,28 @@ constexpr int kLongU = SKV_LONG_U;   // 16-byte loads in flight per thread and p
 
 __device__ __forceinline__ int lclamp(int x, int lo, int hi) { return x < lo ? lo : (x > hi ? hi : x); }
 
+// The smallest float f (value order, -inf .. +inf) with pred(f) true, for a
+// predicate monotone in f (false below some f, true from it on); NaN when no
+// float satisfies it.  One warp, a 32-way search over the order-preserving
+// float keys: 7 ballot rounds.  All lanes return it.
+template <typename Pred>
+__device__ __forceinline__ float warp_first_float(Pred pred, int lane) {
+  auto from_key = [](uint32_t k) { return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k); };
+  constexpr uint32_t kNegInf = 0x007fffffu, kPosInf = 0xff800000u;   // keys of -inf, +inf
+  if (!__any_sync(0xffffffffu, lane == 0 && pred(from_key(kPosInf)))) return __int_as_float(0x7fc00000);
+  long long L = static_cast<long long>(kNegInf) - 1, H = kPosInf;   // pred(L) false, pred(H) true
+  while (H - L > 1) {
+    const long long step = (H - L + 31) / 32;
+    const long long k = min(L + step * (lane + 1), H);
+    const uint32_t bal = __ballot_sync(0xffffffffu, pred(from_key(static_cast<uint32_t>(k))));
+    const int f = __ffs(bal) - 1;   // lane 31 holds H: some lane is true
+    const long long nH = min(L + step * (f + 1), H);
+    L = f == 0 ? L : L + step * f;
+    H = nH;
+  }
+  return from_key(static_cast<uint32_t>(H));
+}
+
 // U float4 loads of positions base + stride*u (+0..3) of src: unguarded when
 // the last one is fully inside [0, lim) (and the row is 16-byte aligned)
 template <int U>
@@ -520,27 +542,9 @@ __device__ __forceinline__ void select_row_long(const SelectParams& p, const int
       if (lane == 0) s_i[6 + t] = 0;
       float bnd[2] = {__int_as_float(0x7fc00000), __int_as_float(0x7fc00000)};
       if (t == 1 || rA > 0) {
-        auto from_key = [](uint32_t k) {
-          return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
-        };
+        // smallest float with where(f, t) >= e (e = 0: cell or above; 1: above)
 #pragma unroll 1
-        for (int e = 0; e < 2; ++e) {
-          // smallest float f with where(f, t) >= e (e = 0: cell or above; 1: above)
-          auto pred = [&](uint32_t k) { return where(from_key(k), t) >= e; };
-          constexpr uint32_t kNegInf = 0x007fffffu, kPosInf = 0xff800000u;   // keys of -inf, +inf
-          if (!__any_sync(0xffffffffu, lane == 0 && pred(kPosInf))) continue;
-          long long L = static_cast<long long>(kNegInf) - 1, H = kPosInf;   // pred(L) false, pred(H) true
-          while (H - L > 1) {
-            const long long step = (H - L + 31) / 32;
-            const long long k = min(L + step * (lane + 1), H);
-            const uint32_t bal = __ballot_sync(0xffffffffu, pred(static_cast<uint32_t>(k)));
-            const int f = __ffs(bal) - 1;   // lane 31 holds H: some lane is true
-            const long long nH = min(L + step * (f + 1), H);
-            L = f == 0 ? L : L + step * f;
-            H = nH;
-          }
-          bnd[e] = from_key(static_cast<uint32_t>(H));
-        }
+        for (int e = 0; e < 2; ++e) bnd[e] = warp_first_float([&](float f) { return where(f, t) >= e; }, lane);
       }
       if (lane == 0) {
         s_thr[t][0] = bnd[0];
