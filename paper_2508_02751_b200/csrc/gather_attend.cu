@@ -199,6 +199,23 @@ __device__ __forceinline__ int split_begin(const GroupLayout& L, int c, int NC) 
   return x;
 }
 
+// First entry of share q of group grp = b * H_kv + g.  Per-group ranks
+// (flat_shares == 0): rank q of NC, split_begin above.  Stream-K
+// (flat_shares == S > #groups Gt): CTA s owns the interval [s*Gt, (s+1)*Gt) of
+// the line where group grp is [grp*S, (grp+1)*S), every group's bytes being
+// one unit; share q of grp is its intersection with CTA floor(grp*S/Gt) + q,
+// so its boundaries are the byte-balanced points (s*Gt - grp*S) / S.
+template <bool kFlat = true>
+__device__ __forceinline__ int share_begin(const AttendParams& p, const GroupLayout& L, int grp, int q,
+                                           int NC) {
+  if (!kFlat || p.flat_shares == 0) return split_begin(L, q, NC);
+  const int64_t S = p.flat_shares, Gt = static_cast<int64_t>(p.batch) * p.kv_heads;
+  const int64_t s_first = grp * S / Gt;
+  int64_t num = q == 0 ? 0 : (s_first + q) * Gt - grp * S;
+  if (num > S) num = S;
+  return split_begin(L, static_cast<int>(num), static_cast<int>(S));
+}
+
 // One thread: the tile table of entries [e_b, e_b + E) of the group's list —
 // runs of K+V entries (recent / critical) in 16-row tiles, runs of V-only
 // (marginal) entries in 32-row tiles (both fill one 8 KB stage, so the tile
@@ -321,7 +338,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const AttendParams p
   // byte-balanced share contains it and is staged if it is in that rank's
   // first batch (s_split[k] = start of rank c_lo + k)
   __shared__ int s_split[33];
-  if (threadIdx.x <= nr) s_split[threadIdx.x] = split_begin(L, c_lo + threadIdx.x, NC);
+  if (threadIdx.x <= nr) s_split[threadIdx.x] = share_begin(p, L, b * p.kv_heads + g, c_lo + threadIdx.x, NC);
   __syncthreads();
   // only the staged entries are visited: flattened over the ranks' first
   // batches (s_pre[k] = staged entries of this CTA's ranks before c_lo + k)
@@ -466,8 +483,11 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const AttendParams p
 // kAsync: batch x+1 is staged asynchronously during batch x (long lists);
 // otherwise CTA-synchronously at the start of batch x (short lists rarely have
 // a second batch, and the leaner kernel keeps fewer registers live)
-template <int D, bool kAsync>
-__global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const AttendParams p) {
+// One share (c of the group's NC record slots) of group (b, g); nmerge = the
+// group's shares that the global merge waits for (= NC unless stream-K).
+template <int D, bool kAsync, bool kFlat>
+__device__ __forceinline__ void attend_share(const AttendParams& p, const int c, const int g, const int b,
+                                             const int NC, const int nmerge) {
   constexpr int NSTAGE = stages_for<D>();
   constexpr int ROWB = D * 2;                // bytes per K or V row
   constexpr int KV_BYTES = kTile * ROWB;
@@ -490,8 +510,6 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
   auto BW = [&](int x) { return reinterpret_cast<float*>((x & 1) ? soff1 + 2 * kBatch : smk + kBatch); };
   auto BTT = [&](int x) { return (x & 1) ? s_tt1 : s_tt; };
 
-  const int c = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
-  const int NC = gridDim.x;
   // Without the overlap flag nothing is read before the previous kernel on the
   // stream has completed.  With it, the prologue below (plan / selection
   // outputs, page tables, K/V tiles) may run during that kernel's tail.
@@ -618,8 +636,8 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
     }
     return;
   }
-  const int e_lo = split_begin(L, c, NC);
-  const int e_hi = split_begin(L, c + 1, NC);
+  const int e_lo = share_begin<kFlat>(p, L, b * p.kv_heads + g, c, NC);
+  const int e_hi = share_begin<kFlat>(p, L, b * p.kv_heads + g, c + 1, NC);
   (void)T;
   SKV_T(1);
 
@@ -1252,7 +1270,7 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
     __threadfence();
     __syncthreads();
     __shared__ int s_last;
-    if (tid == 0) s_last = atomicAdd(p.tickets + grp, 1) == NC - 1;
+    if (tid == 0) s_last = atomicAdd(p.tickets + grp, 1) == nmerge - 1;
     __syncthreads();
     if (!s_last) return;
     __threadfence();
@@ -1260,7 +1278,7 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
     // every rank's (m, l) at once, then per head the rank weights 2^(m_q - M)
     // and L in rank order; the O rows with 8 ranks' loads in flight per thread
     __shared__ float s_m[32][8], s_l[32][8], s_L[8];
-    if (tid < NC * 8) {
+    if (tid < nmerge * 8) {
       const int q = tid >> 3, h = tid & 7;
       s_m[q][h] = __ldcg(gp + q * kAttendPartFloats + h);
       s_l[q][h] = __ldcg(gp + q * kAttendPartFloats + 8 + h);
@@ -1268,10 +1286,10 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
     __syncthreads();
     if (tid < G) {
       float M = -INFINITY;
-      for (int q = 0; q < NC; ++q) M = fmaxf(M, s_m[q][tid]);
+      for (int q = 0; q < nmerge; ++q) M = fmaxf(M, s_m[q][tid]);
       const float Mu = M == -INFINITY ? 0.f : M;
       float L = 0.f;
-      for (int q = 0; q < NC; ++q) {
+      for (int q = 0; q < nmerge; ++q) {
         const float f = exp2f(s_m[q][tid] - Mu);
         L += s_l[q][tid] * f;
         s_m[q][tid] = f;   // (now the rank's weight)
@@ -1283,7 +1301,7 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
       const int h = it / (D / 4), c4 = (it % (D / 4)) * 4;
       float4 oc = make_float4(0.f, 0.f, 0.f, 0.f), om = oc;
 #pragma unroll 8
-      for (int q = 0; q < NC; ++q) {
+      for (int q = 0; q < nmerge; ++q) {
         const float* pq = gp + q * kAttendPartFloats;
         const float f = s_m[q][h];
         const float4 a = __ldcg(reinterpret_cast<const float4*>(pq + 16 + h * D + c4));
@@ -1328,6 +1346,36 @@ __global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const Atte
   }
   cluster_sync();   // keep every rank's shared memory alive until all reads are done
   SKV_T(6);
+}
+
+template <int D, bool kAsync, bool kFlat>
+__global__ void __launch_bounds__(kThreads, 8 / kWarps) attend_kernel(const AttendParams p) {
+  if constexpr (!kFlat) {
+    attend_share<D, kAsync, false>(p, blockIdx.x, blockIdx.y, blockIdx.z, p.max_chunks, p.max_chunks);
+    return;
+  }
+  // per-group ranks: grid (NC, H_kv, B), one share each.  Stream-K: grid (S),
+  // CTA s runs the shares of the (at most two when S > #groups) groups its
+  // interval meets, in group order (share_begin).
+  const int64_t S = p.flat_shares, Gt = static_cast<int64_t>(p.batch) * p.kv_heads;
+  const int s = blockIdx.x;
+  const int grp_lo = S ? static_cast<int>(s * Gt / S) : 0;
+  const int grp_hi = S ? static_cast<int>(((s + 1) * Gt - 1) / S) : 0;
+  for (int grp = grp_lo; grp <= grp_hi; ++grp) {
+    int c = blockIdx.x, g = blockIdx.y, b = blockIdx.z, nmerge = p.max_chunks;
+    if (S) {
+      const int64_t s_first = grp * S / Gt, s_last = ((grp + 1) * S + Gt - 1) / Gt - 1;
+      c = static_cast<int>(s - s_first);
+      nmerge = static_cast<int>(s_last - s_first + 1);
+      g = grp % p.kv_heads;
+      b = grp / p.kv_heads;
+    }
+    if (grp > grp_lo) {   // the previous share's copies, barriers and shared memory are done
+      cp_async_wait<0>();
+      __syncthreads();
+    }
+    attend_share<D, kAsync, kFlat>(p, c, g, b, p.max_chunks, nmerge);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1521,7 +1569,7 @@ extern "C" int skv_debug_set_trace(long long* buf) {
 static int32_t clusters_fit(int nc) {
   static int cache[17] = {0};
   if (cache[nc]) return cache[nc] > 0 ? cache[nc] : 0;
-  auto kern = attend_kernel<128, true>;
+  auto kern = attend_kernel<128, true, false>;
   const size_t sm = smem_bytes<128>();
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
   if (nc > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -1571,7 +1619,27 @@ static int32_t num_sms() {
 // a global workspace (attend_split_in_cluster false).
 // (Config 2: 128 groups -> 1; config 4 at one GPU: 64 groups -> 2, cluster;
 // at one sequence per GPU: 8 groups -> 18, global merge.)
+// Stream-K (SMALLKV_ATTEND_FLAT=1): when the groups do not divide the SMs,
+// #SMs CTAs take equal byte shares of all groups laid end to end, so no SM
+// idles (config 2: 128 groups leave 20 of 148 SMs without a stream of their
+// own).  Needs #groups < #SMs and at most 32 shares per group.
+int32_t attend_flat_shares(int32_t batch, int32_t kv_heads) {
+  static const int32_t mode = [] {
+    const char* e = getenv("SMALLKV_ATTEND_FLAT");   // tuning knob: 0 / 1
+    return e ? atoi(e) : 0;
+  }();
+  if (mode == 0) return 0;
+  const int64_t groups = static_cast<int64_t>(batch) * kv_heads, S = num_sms();
+  if (groups <= 0 || groups >= S || S % groups == 0) return 0;
+  if ((S + groups - 1) / groups + 1 > 32) return 0;
+  return static_cast<int32_t>(S);
+}
+
 int32_t attend_ctas_per_group(int32_t batch, int32_t kv_heads) {
+  if (const int32_t S = attend_flat_shares(batch, kv_heads)) {
+    const int32_t groups = batch * kv_heads;
+    return (S + groups - 1) / groups + 1;   // record slots: shares per group at most
+  }
   static const int32_t forced = [] {
     const char* e = getenv("SMALLKV_ATTEND_CTAS");   // tuning knob
     return e ? atoi(e) : 0;
@@ -1587,6 +1655,7 @@ bool attend_split_in_cluster(int32_t batch, int32_t kv_heads) {
     const char* e = getenv("SMALLKV_ATTEND_GLOBAL_MERGE");   // tuning knob
     return e ? atoi(e) : 0;
   }();
+  if (attend_flat_shares(batch, kv_heads)) return false;
   const int32_t nc = attend_ctas_per_group(batch, kv_heads);
   if (nc <= 1) return true;
   if (force_global || nc > 16) return false;
@@ -1594,20 +1663,21 @@ bool attend_split_in_cluster(int32_t batch, int32_t kv_heads) {
   return static_cast<int64_t>(clusters_fit(nc)) >= groups;
 }
 
-template <int D, bool kAsync>
-static cudaError_t launch_d(const AttendParams& p, cudaStream_t s) {
+template <int D, bool kAsync, bool kFlat>
+static cudaError_t launch_dk(const AttendParams& p, cudaStream_t s) {
   const size_t sm = smem_bytes<D>();
-  cudaError_t e = cudaFuncSetAttribute(attend_kernel<D, kAsync>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(attend_kernel<D, kAsync, kFlat>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(sm));
   if (e != cudaSuccess) return e;
+  if (p.flat_shares && !p.global_merge) return cudaErrorInvalidValue;
   if (p.max_chunks > 8 && !p.global_merge) {
-    e = cudaFuncSetAttribute(attend_kernel<D, kAsync>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaFuncSetAttribute(attend_kernel<D, kAsync, kFlat>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
-  e = cudaFuncSetAttribute(attend_kernel<D, kAsync>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  e = cudaFuncSetAttribute(attend_kernel<D, kAsync, kFlat>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.max_chunks, p.kv_heads, p.batch);
+  cfg.gridDim = p.flat_shares ? dim3(p.flat_shares) : dim3(p.max_chunks, p.kv_heads, p.batch);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = sm;
   cfg.stream = s;
@@ -1620,7 +1690,12 @@ static cudaError_t launch_d(const AttendParams& p, cudaStream_t s) {
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = p.global_merge ? 1 : 2;   // the global merge needs no cluster
-  return cudaLaunchKernelEx(&cfg, attend_kernel<D, kAsync>, p);
+  return cudaLaunchKernelEx(&cfg, attend_kernel<D, kAsync, kFlat>, p);
+}
+
+template <int D, bool kAsync>
+static cudaError_t launch_d(const AttendParams& p, cudaStream_t s) {
+  return p.flat_shares ? launch_dk<D, kAsync, true>(p, s) : launch_dk<D, kAsync, false>(p, s);
 }
 
 int64_t plan_bytes(int32_t n_layers, int32_t batch, int32_t kv_heads, int32_t max_seq_len) {

@@ -129,6 +129,10 @@ struct AttendParams {
   // split without a cluster (max_chunks > the clusters the GPU co-schedules):
   // every CTA writes its partial state, the last one of the group merges
   int32_t global_merge;
+  // stream-K split (> 0): S CTAs in a 1-D grid over all groups' bytes, CTA s
+  // owning [s*Gt, (s+1)*Gt) of the groups laid end to end at S units each;
+  // max_chunks is then the record slots per group and the merge is global
+  int32_t flat_shares;
   float* partials;            // [B][H_kv][max_chunks][kAttendPartFloats]
   int32_t* tickets;           // [B][H_kv], zero between launches
 };
@@ -161,6 +165,7 @@ cudaError_t launch_plan(const AttendParams& p, int32_t n_layers, cudaStream_t s)
 int64_t plan_bytes(int32_t n_layers, int32_t batch, int32_t kv_heads, int32_t max_seq_len);
 int32_t attend_ctas_per_group(int32_t batch, int32_t kv_heads);
 bool attend_split_in_cluster(int32_t batch, int32_t kv_heads);   // else the global merge
+int32_t attend_flat_shares(int32_t batch, int32_t kv_heads);      // stream-K CTAs, 0: off
 
 // ---------------------------------------------------------------- variant f3 prefill scores (R17)
 struct PrefillParams {

@@ -575,6 +575,7 @@ int fill_attend_params(skv::AttendParams& ap, const smallkv_cache* llm, const sm
   ap.sync_stage = sync_stage_env;
   ap.max_chunks = skv::attend_ctas_per_group(batch->batch, llm->num_kv_heads);
   ap.global_merge = skv::attend_split_in_cluster(batch->batch, llm->num_kv_heads) ? 0 : 1;
+  ap.flat_shares = skv::attend_flat_shares(batch->batch, llm->num_kv_heads);
   ap.scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(llm->head_dim));
   return SMALLKV_OK;
 }

@@ -828,3 +828,29 @@ def test_long_split_cta_sizes(cta):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert "3 passed" in r.stdout, r.stdout[-2000:]
 
+
+
+def test_attend_stream_k_split():
+    """Stream-K attend (SMALLKV_ATTEND_FLAT=1, read once per process): when the
+    groups do not divide the SMs, #SMs CTAs take equal byte shares of all
+    groups laid end to end (a CTA spans the tail of one group and the head of
+    the next; a group's shares merge in share order through the workspace).
+    Rerun in a fresh process the parity cases whose group counts trigger it —
+    6 groups (3 x 2; 26 shares per group at most), 8 and 16 (the shape
+    cases), 128 (config 2 at full size: 148 CTAs, a group spans 2 or 3) — plus
+    per-sequence budget mixes, empty / marginal-only budgets and ragged
+    lengths, against the fp64 oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sel = ("test_small_parity_pages_maps or test_shapes_parity or test_full_budget_is_dense_attention"
+           " or test_marginal_only_and_empty or test_clamp_short_sequences or test_extreme_logits"
+           " or test_qwen7b_full_size_sampled or test_per_sequence_budgets")
+    env = dict(os.environ, SMALLKV_ATTEND_FLAT="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", sel,
+                        os.path.join(root, "tests", "test_gpu_parity.py"),
+                        os.path.join(root, "tests", "test_gpu_corners.py")],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout and "failed" not in r.stdout, r.stdout[-2000:]
