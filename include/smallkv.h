@@ -312,9 +312,12 @@ size_t smallkv_attend_workspace_size(const smallkv_cache* llm,
  *               zero-filled once by the caller (smallkv_workspace_init) and
  *               left zeroed by every call: when a group's list is split over
  *               more CTAs than the GPU co-schedules as one thread-block
- *               cluster, the CTAs merge their partial states through it (a
- *               per-group arrival counter + partial rows, merged in rank
- *               order: deterministic); otherwise it is unused.
+ *               cluster, or under the stream-K split (long lists over
+ *               >= 32 groups that do not divide the SMs: #SMs CTAs take
+ *               equal byte shares of all groups end to end), the CTAs merge
+ *               their partial states through it (a per-group arrival counter
+ *               + partial rows, merged in rank / share order:
+ *               deterministic); otherwise it is unused.
  *               SMALLKV_ATTEND_GROUP_SELECTION (variant f2, R16): the
  *               selection inputs are smallkv_select_group's group-indexed
  *               outputs; every head of group g attends over the group's

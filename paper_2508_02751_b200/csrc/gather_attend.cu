@@ -1619,24 +1619,28 @@ static int32_t num_sms() {
 // a global workspace (attend_split_in_cluster false).
 // (Config 2: 128 groups -> 1; config 4 at one GPU: 64 groups -> 2, cluster;
 // at one sequence per GPU: 8 groups -> 18, global merge.)
-// Stream-K (SMALLKV_ATTEND_FLAT=1): when the groups do not divide the SMs,
-// #SMs CTAs take equal byte shares of all groups laid end to end, so no SM
-// idles (config 2: 128 groups leave 20 of 148 SMs without a stream of their
-// own).  Needs #groups < #SMs and at most 32 shares per group.
-int32_t attend_flat_shares(int32_t batch, int32_t kv_heads) {
+// Stream-K: when the groups do not divide the SMs, #SMs CTAs take equal byte
+// shares of all groups laid end to end, so no SM idles (config 4: 64 groups
+// leave 20 of 148 SMs without a stream of their own).  Needs #groups < #SMs
+// and at most 32 shares per group.  On by default for long lists
+// (max_seq_len >= 65536) over >= 32 groups, where it measured faster (config 4
+// +2.1%, its B = 4 rank +3.6%); short lists lose the cross-layer overlap and
+// pay a second prologue (config 2: -32%).  SMALLKV_ATTEND_FLAT=0 / 1 forces it.
+int32_t attend_flat_shares(int32_t batch, int32_t kv_heads, int32_t max_seq_len) {
   static const int32_t mode = [] {
     const char* e = getenv("SMALLKV_ATTEND_FLAT");   // tuning knob: 0 / 1
-    return e ? atoi(e) : 0;
+    return e ? atoi(e) : -1;
   }();
   if (mode == 0) return 0;
   const int64_t groups = static_cast<int64_t>(batch) * kv_heads, S = num_sms();
   if (groups <= 0 || groups >= S || S % groups == 0) return 0;
   if ((S + groups - 1) / groups + 1 > 32) return 0;
+  if (mode < 0 && (max_seq_len < 65536 || groups < 32)) return 0;
   return static_cast<int32_t>(S);
 }
 
-int32_t attend_ctas_per_group(int32_t batch, int32_t kv_heads) {
-  if (const int32_t S = attend_flat_shares(batch, kv_heads)) {
+int32_t attend_ctas_per_group(int32_t batch, int32_t kv_heads, int32_t max_seq_len) {
+  if (const int32_t S = attend_flat_shares(batch, kv_heads, max_seq_len)) {
     const int32_t groups = batch * kv_heads;
     return (S + groups - 1) / groups + 1;   // record slots: shares per group at most
   }
@@ -1650,13 +1654,13 @@ int32_t attend_ctas_per_group(int32_t batch, int32_t kv_heads) {
   return nc < 1 ? 1 : (nc > 32 ? 32 : static_cast<int32_t>(nc));
 }
 
-bool attend_split_in_cluster(int32_t batch, int32_t kv_heads) {
+bool attend_split_in_cluster(int32_t batch, int32_t kv_heads, int32_t max_seq_len) {
   static const int32_t force_global = [] {
     const char* e = getenv("SMALLKV_ATTEND_GLOBAL_MERGE");   // tuning knob
     return e ? atoi(e) : 0;
   }();
-  if (attend_flat_shares(batch, kv_heads)) return false;
-  const int32_t nc = attend_ctas_per_group(batch, kv_heads);
+  if (attend_flat_shares(batch, kv_heads, max_seq_len)) return false;
+  const int32_t nc = attend_ctas_per_group(batch, kv_heads, max_seq_len);
   if (nc <= 1) return true;
   if (force_global || nc > 16) return false;
   const int64_t groups = static_cast<int64_t>(batch) * kv_heads;
@@ -1700,7 +1704,7 @@ static cudaError_t launch_d(const AttendParams& p, cudaStream_t s) {
 
 int64_t plan_bytes(int32_t n_layers, int32_t batch, int32_t kv_heads, int32_t max_seq_len) {
   return static_cast<int64_t>(n_layers) * batch * kv_heads *
-         plan_record_bytes(attend_ctas_per_group(batch, kv_heads));
+         plan_record_bytes(attend_ctas_per_group(batch, kv_heads, max_seq_len));
 }
 
 cudaError_t launch_plan(const AttendParams& p, int32_t n_layers, cudaStream_t s) {

@@ -163,9 +163,9 @@ cudaError_t launch_tier_update(const TierParams& p, cudaStream_t s);
 cudaError_t launch_attend(const AttendParams& p, cudaStream_t s);
 cudaError_t launch_plan(const AttendParams& p, int32_t n_layers, cudaStream_t s);
 int64_t plan_bytes(int32_t n_layers, int32_t batch, int32_t kv_heads, int32_t max_seq_len);
-int32_t attend_ctas_per_group(int32_t batch, int32_t kv_heads);
-bool attend_split_in_cluster(int32_t batch, int32_t kv_heads);   // else the global merge
-int32_t attend_flat_shares(int32_t batch, int32_t kv_heads);      // stream-K CTAs, 0: off
+int32_t attend_ctas_per_group(int32_t batch, int32_t kv_heads, int32_t max_seq_len);
+bool attend_split_in_cluster(int32_t batch, int32_t kv_heads, int32_t max_seq_len);   // else the global merge
+int32_t attend_flat_shares(int32_t batch, int32_t kv_heads, int32_t max_seq_len);      // stream-K CTAs, 0: off
 
 // ---------------------------------------------------------------- variant f3 prefill scores (R17)
 struct PrefillParams {

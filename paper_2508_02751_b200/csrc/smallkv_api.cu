@@ -160,8 +160,8 @@ struct AttendWs {
 // by the caller, left zeroed by every launch).
 AttendWs attend_ws_layout(const smallkv_cache* llm, const smallkv_batch* b) {
   AttendWs w;
-  w.ctas = skv::attend_ctas_per_group(b->batch, llm->num_kv_heads);
-  w.cluster = skv::attend_split_in_cluster(b->batch, llm->num_kv_heads);
+  w.ctas = skv::attend_ctas_per_group(b->batch, llm->num_kv_heads, b->max_seq_len);
+  w.cluster = skv::attend_split_in_cluster(b->batch, llm->num_kv_heads, b->max_seq_len);
   const size_t groups = static_cast<size_t>(b->batch) * llm->num_kv_heads;
   w.tickets = 0;
   w.partials = round256(groups * 4);
@@ -573,9 +573,9 @@ int fill_attend_params(skv::AttendParams& ap, const smallkv_cache* llm, const sm
     return e ? atoi(e) : 0;
   }();
   ap.sync_stage = sync_stage_env;
-  ap.max_chunks = skv::attend_ctas_per_group(batch->batch, llm->num_kv_heads);
-  ap.global_merge = skv::attend_split_in_cluster(batch->batch, llm->num_kv_heads) ? 0 : 1;
-  ap.flat_shares = skv::attend_flat_shares(batch->batch, llm->num_kv_heads);
+  ap.max_chunks = skv::attend_ctas_per_group(batch->batch, llm->num_kv_heads, batch->max_seq_len);
+  ap.global_merge = skv::attend_split_in_cluster(batch->batch, llm->num_kv_heads, batch->max_seq_len) ? 0 : 1;
+  ap.flat_shares = skv::attend_flat_shares(batch->batch, llm->num_kv_heads, batch->max_seq_len);
   ap.scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(llm->head_dim));
   return SMALLKV_OK;
 }

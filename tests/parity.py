@@ -232,7 +232,8 @@ def compare_group(p, gpu, sel, layer_slot, out_gpu=None, llm_view=None):
 
 
 def attend_split(step) -> int:
-    """CTAs per (sequence, kv-group) the attend of a DecodeStep launches,
+    """CTAs per (sequence, kv-group) the attend of a DecodeStep launches (under
+    the stream-K split: the record slots, the most shares a group has),
     recovered from smallkv_plan_size: L*B*H_kv records of 256 + NC * (384 +
     1024 x 12) bytes (gather_attend.cu plan_record_bytes)."""
     import ctypes

@@ -224,7 +224,9 @@ def test_attend_many_staging_batches():
                              budget=(n // 10, n // 20, n // 10))
     p = synth.make_problem(cfg, seed=65, page_size=64).to("cuda")
     step, sel_gpu, outs = parity.run_gpu_step(p)
-    assert parity.attend_split(step) <= 2   # several batches per CTA
+    # several batches per CTA: 2 ranks per group, or (stream-K, the default at
+    # n >= 65536 over >= 32 groups) 148 CTAs over 64 groups, <= 4 shares each
+    assert parity.attend_split(step) <= 4
     pc = p.to("cpu")
     sel = parity.oracle_select(pc)
     sg = parity.sel_from_gpu(pc, sel_gpu, sel)
