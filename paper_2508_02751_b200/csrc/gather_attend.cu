@@ -1621,8 +1621,8 @@ static int32_t num_sms() {
 // at one sequence per GPU: 8 groups -> 18, global merge.)
 // Stream-K: when the groups do not divide the SMs, #SMs CTAs take equal byte
 // shares of all groups laid end to end, so no SM idles (config 4: 64 groups
-// leave 20 of 148 SMs without a stream of their own).  Needs #groups < #SMs
-// and at most 32 shares per group.  On by default for long lists
+// leave 20 of 148 SMs without a stream of their own; with more groups than
+// SMs, the last wave's tail).  At most 32 shares per group.  On by default for long lists
 // (max_seq_len >= 65536) over >= 32 groups, where it measured faster (config 4
 // +2.1%, its B = 4 rank +3.6%); short lists lose the cross-layer overlap and
 // pay a second prologue (config 2: -32%).  SMALLKV_ATTEND_FLAT=0 / 1 forces it.
@@ -1633,7 +1633,9 @@ int32_t attend_flat_shares(int32_t batch, int32_t kv_heads, int32_t max_seq_len)
   }();
   if (mode == 0) return 0;
   const int64_t groups = static_cast<int64_t>(batch) * kv_heads, S = num_sms();
-  if (groups <= 0 || groups >= S || S % groups == 0) return 0;
+  if (groups <= 0 || S % groups == 0) return 0;
+  // more groups than SMs (config 5: 512 groups = 3.46 waves): forced only
+  if (groups >= S && (mode != 1 || groups % S == 0)) return 0;
   if ((S + groups - 1) / groups + 1 > 32) return 0;
   if (mode < 0 && (max_seq_len < 65536 || groups < 32)) return 0;
   return static_cast<int32_t>(S);
