@@ -839,8 +839,9 @@ def test_attend_stream_k_split():
     6 groups (3 x 2; 26 shares per group at most), 8 and 16 (the shape
     cases), 128 (config 2 at full size: 148 CTAs, a group spans 2 or 3) — plus
     per-sequence budget mixes, empty / marginal-only budgets and ragged
-    lengths, against the fp64 oracle; and the tiered pool (f4) and the decode
-    graph, bitwise against the HBM-resident / device runs of the same mode."""
+    lengths, against the fp64 oracle; per-KV-head shared selection (f2); and
+    the tiered pool (f4) and the decode graph, bitwise against the
+    HBM-resident / device runs of the same mode."""
     import os
     import subprocess
     import sys
@@ -848,7 +849,8 @@ def test_attend_stream_k_split():
     sel = ("test_small_parity_pages_maps or test_shapes_parity or test_full_budget_is_dense_attention"
            " or test_marginal_only_and_empty or test_clamp_short_sequences or test_extreme_logits"
            " or test_qwen7b_full_size_sampled or test_per_sequence_budgets"
-           " or test_f4_tiered_pool_bitwise or test_f4_long_context or test_decode_graph")
+           " or test_f4_tiered_pool_bitwise or test_f4_long_context or test_decode_graph"
+           " or test_f2_group_selection_parity or test_f2_shapes")
     env = dict(os.environ, SMALLKV_ATTEND_FLAT="1")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", sel,
                         os.path.join(root, "tests", "test_gpu_parity.py"),
